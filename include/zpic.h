@@ -1,0 +1,175 @@
+/*
+ * zpic.h — C ABI of the B200-native 2D3V EM-PIC hot path (ZPIC em2d, arxiv 2106.12485).
+ *
+ * The step this library runs is the paper's main loop (Fig. 1):
+ *   (1) bilinear field interpolation at each particle "with the field values from the
+ *       previous iteration",
+ *   (2) leapfrog + relativistic Boris particle advance,
+ *   (3) "exact charge conserving" current deposition (Villasenor-Buneman
+ *       trajectory split at cell crossings per BASELINE.json north_star), the ghost-cell
+ *       current reduction and the optional digital filter,
+ *   (4) Yee-mesh FDTD field advance and the ghost-field update,
+ * plus particle boundaries (periodic / open / moving window) and the per-tile
+ * particle re-sort.  Readings of everything the paper leaves open: SURVEY.md §8(c) R1-R25,
+ * repeated in DESIGN.md.  All arithmetic is fp32 on the device; energies are fp64.
+ *
+ * Conventions (normalised units, c = 1):
+ *   - grid quantities are returned as [component][y][x] fp32, interior cells only;
+ *     Yee staggering Ex(i+1/2,j) Ey(i,j+1/2) Ez(i,j) Bx(i,j+1/2) By(i+1/2,j) Bz(i+1/2,j+1/2);
+ *   - a particle is (ix, iy) cell index + (x, y) in-cell offset in [0,1) + proper momentum
+ *     (ux, uy, uz) = gamma v;
+ *   - per-particle charge q_s = sign(m_q) * n_s / (ppc_x * ppc_y) (R8).
+ *
+ * Errors: every function returns a zpic_status; nothing throws across the ABI.  Device
+ * errors (capacity overflow, |displacement| >= 1 cell) are sticky: they are raised on the
+ * device, and reported by the next synchronising call (get_*, zpic_energy, zpic_sync).
+ * zpic_last_error() gives a one-line message.  A ctx is not thread-safe.
+ *
+ * Ownership: the library owns every device buffer (allocated through the optional allocator
+ * hooks in zpic_options — the Python binding passes PyTorch's caching allocator — else
+ * cudaMalloc).  The caller owns every host buffer; get_* fill them by copy.  Work is enqueued
+ * on options->stream (a cudaStream_t; NULL = a stream the library creates).
+ */
+#ifndef ZPIC_H
+#define ZPIC_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  ZPIC_OK = 0,
+  ZPIC_E_INVALID = -1,    /* bad argument / config (message in zpic_last_error) */
+  ZPIC_E_CFL = -2,        /* dt >= 1/sqrt(dx^-2 + dy^-2) */
+  ZPIC_E_EMPTY_GRID = -3, /* nx or ny < 1 */
+  ZPIC_E_DECOMP = -4,     /* slab rows < 2 or ny % world != 0 */
+  ZPIC_E_LASER = -5,
+  ZPIC_E_OOM = -6,
+  ZPIC_E_CUDA = -7,
+  ZPIC_E_NCCL = -8,
+  ZPIC_E_OVERFLOW = -9,   /* mover buffer capacity exceeded (particles would be lost) */
+  ZPIC_E_MIGRATION = -10, /* a particle moved >= 1 cell in one step (CFL / logic bug) */
+  ZPIC_E_BUFSIZE = -11,   /* caller buffer too small */
+  ZPIC_E_STATE = -12      /* call not valid in the current state */
+} zpic_status;
+
+typedef struct {
+  int32_t nx, ny; /* cells (global) */
+  double dx, dy;  /* cell size, c/omega_p */
+} zpic_grid;
+
+typedef enum {
+  ZPIC_BC_PERIODIC = 0,
+  ZPIC_BC_OPEN = 1,          /* particles removed at the edge; Mur-1 on tangential E (R13) */
+  ZPIC_BC_MOVING_WINDOW = 2  /* x only: window moves at c; fresh plasma injected (R14, R15) */
+} zpic_bc;
+
+typedef struct {
+  zpic_bc x, y;
+} zpic_boundaries;
+
+typedef enum {
+  ZPIC_DENS_UNIFORM = 0, /* n everywhere */
+  ZPIC_DENS_SLAB = 1,    /* n for cell-centre x in [x0, x1), 0 elsewhere */
+  ZPIC_DENS_NONE = 2     /* no particles from zpic_init: load them with zpic_set_particles */
+} zpic_dens;
+
+/* One species.  The device injector (zpic_init) fills the ppc_x x ppc_y regular sub-lattice
+ * x = (k+1/2)/ppc_x, y = (l+1/2)/ppc_y of every filled cell, u = ufl + uth * N(0,1) with the
+ * counter-based generator of DESIGN.md "RNG" keyed by (seed, species index, particle id). */
+typedef struct {
+  double m_q;         /* mass / charge (-1 electrons) */
+  int32_t ppc[2];     /* particles per cell along x, y */
+  double n;           /* density (sets q_s) */
+  zpic_dens profile;
+  double x0, x1;      /* slab limits (physical x) */
+  double ufl[3], uth[3];
+} zpic_species;
+
+typedef void* (*zpic_alloc_fn)(size_t bytes, void* user);
+typedef void (*zpic_free_fn)(void* ptr, void* user);
+
+/* Optional settings; pass NULL for defaults. */
+typedef struct {
+  int32_t filter_passes;      /* 0 = no filter; n passes of (1/4,1/2,1/4) along x */
+  int32_t filter_compensated; /* 1 = add the (-n/4, 1+n/2, -n/4) compensator pass (R12) */
+  int32_t track_ids;          /* 1 = carry a uint32 id per particle (validation runs) */
+  int32_t tile[2];            /* tile size in cells (default 16 x 16) */
+  double capacity_slack;      /* per-tile capacity = slack * initial count (default 1.5) */
+  double mover_fraction;      /* mover buffer capacity as a fraction of particles (default 0.05) */
+  int32_t profile;            /* 1 = record per-kernel CUDA-event times (zpic_kernel_times) */
+  void* stream;               /* cudaStream_t to enqueue on (NULL: library-owned stream) */
+  zpic_alloc_fn alloc;        /* device allocator hook (NULL: cudaMalloc) */
+  zpic_free_fn free;
+  void* alloc_user;
+} zpic_options;
+
+/* Multi-GPU y-slab decomposition (nullable = 1 GPU). */
+typedef struct {
+  int32_t rank, world;
+  void* nccl_comm; /* ncclComm_t shared with torch's ProcessGroupNCCL */
+  int32_t device;
+} zpic_dist;
+
+typedef struct zpic_ctx zpic_ctx;
+
+/* Validate, allocate, inject every species (profile != NONE) and zero the fields.
+ * Errors: ZPIC_E_INVALID, ZPIC_E_CFL, ZPIC_E_EMPTY_GRID, ZPIC_E_DECOMP, ZPIC_E_OOM, ZPIC_E_CUDA. */
+zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zpic_species* species,
+                      int32_t n_species, const zpic_boundaries* bc, uint64_t seed,
+                      const zpic_options* options, const zpic_dist* dist);
+
+/* Replace the particles of one species by n host particles (global ix, iy).  id may be NULL
+ * (then ids are 0..n-1 if track_ids).  Particles outside the local slab are an error. */
+zpic_status zpic_set_particles(zpic_ctx* ctx, int32_t species, int64_t n, const int32_t* ix,
+                               const int32_t* iy, const float* x, const float* y, const float* ux,
+                               const float* uy, const float* uz, const uint32_t* id);
+
+/* Overwrite E (which=0) or B (which=1) interior values from host [comp][y][x] (laser init). */
+zpic_status zpic_set_fields(zpic_ctx* ctx, int32_t which, const float* in, size_t in_len);
+
+/* Enqueue n time steps (asynchronous w.r.t. the host). */
+zpic_status zpic_step(zpic_ctx* ctx, int32_t n);
+
+/* Block until all enqueued work is done; surface sticky device errors. */
+zpic_status zpic_sync(zpic_ctx* ctx);
+
+/* which: 0 = E, 1 = B, 2 = J used by the last field advance (after reduction and filter),
+ * 3 = J of the last step before the filter.  out: 3*nx*ny_local floats [comp][y][x]. */
+zpic_status zpic_get_fields(zpic_ctx* ctx, int32_t which, float* out, size_t out_len);
+
+/* Size query when ix == NULL (count_inout <- count).  Otherwise fills up to *count_inout
+ * particles (order unspecified) with global ix, iy; id requires track_ids (may be NULL). */
+zpic_status zpic_get_particles(zpic_ctx* ctx, int32_t species, int64_t* count_inout, int32_t* ix,
+                               int32_t* iy, float* x, float* y, float* ux, float* uy, float* uz,
+                               uint32_t* id);
+
+/* Energies of the input state of the last step taken (time level iter = steps-1):
+ * field = 1/2 dx dy sum(E^2 + B^2), kinetic[s] = q_s m_q,s dx dy sum(gamma - 1) (R8).
+ * Before any step: iter = -1 and zeros. */
+zpic_status zpic_energy(zpic_ctx* ctx, int64_t* iter, double* field, double* kinetic);
+
+/* Local slab rows [y0, y0 + ny_local). */
+zpic_status zpic_layout(zpic_ctx* ctx, int32_t* y0, int32_t* ny_local);
+
+/* Counters: out[0] particles (all species), out[1] movers of the last step, out[2] max
+ * tile occupancy / capacity in per-mille, out[3] re-packs done, out[4] steps taken,
+ * out[5] number of tiles. */
+zpic_status zpic_counters(zpic_ctx* ctx, int64_t* out, int32_t n);
+
+/* Per-kernel device time (ms) summed over the steps since the last call, when
+ * options->profile: names of the kernels in order, up to n entries; returns count. */
+zpic_status zpic_kernel_times(zpic_ctx* ctx, const char** names, double* ms, int32_t* launches,
+                              int32_t* n_inout);
+
+void zpic_free(zpic_ctx* ctx);
+
+/* Message of the last failure on ctx (NULL ctx: the last failed zpic_init on this thread). */
+const char* zpic_last_error(const zpic_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ZPIC_H */
