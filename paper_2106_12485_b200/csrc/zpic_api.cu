@@ -1,0 +1,639 @@
+// zpic_api.cu — host runtime behind include/zpic.h: validation, device memory, the step
+// sequence, exports, energies, profiling.  No compute happens on the host:
+// every stage of the step is one of the kernels in zpic_kernels.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "zpic_internal.h"
+
+namespace zpic {
+void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st);
+void launch_insert(const PushParams& p, int grid, cudaStream_t st);
+void launch_loose(const PushParams& p, int grid, cudaStream_t st);
+void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st);
+void launch_guard_x(float* F, const GridDesc& g, int mode, int keep, cudaStream_t st);
+void launch_guard_y(float* F, const GridDesc& g, int mode, int keep, cudaStream_t st);
+void launch_yee(const YeeParams& p, cudaStream_t st);
+void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4, int* mc,
+                     int* sic, int* soc, int* stats, cudaStream_t st);
+void launch_inject(const InjectParams& q, int ntiles, cudaStream_t st);
+void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
+                const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err,
+                cudaStream_t st);
+void launch_export(const PStore& ps, int ntiles, const int64_t* prefix, int y0, int32_t* ix, int32_t* iy, float* x,
+                   float* y, float* ux, float* uy, float* uz, uint32_t* id, cudaStream_t st);
+}  // namespace zpic
+
+using namespace zpic;
+
+namespace {
+thread_local std::string g_init_error;
+
+uint64_t host_mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+struct Fail {
+  zpic_status st;
+  std::string msg;
+};
+
+#define CUDA_OR_THROW(x)                                                                          \
+  do {                                                                                            \
+    cudaError_t e_ = (x);                                                                         \
+    if (e_ != cudaSuccess) throw Fail{ZPIC_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)}; \
+  } while (0)
+
+void* dev_alloc(zpic_ctx* c, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void* p = nullptr;
+  if (c->opt.alloc) {
+    p = c->opt.alloc(bytes, c->opt.alloc_user);
+    if (!p) throw Fail{ZPIC_E_OOM, "allocator hook returned NULL for " + std::to_string(bytes) + " bytes"};
+  } else {
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) throw Fail{ZPIC_E_OOM, "cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e)};
+  }
+  c->allocations.push_back(p);
+  return p;
+}
+
+void dev_free(zpic_ctx* c, void* p) {
+  if (!p) return;
+  auto it = std::find(c->allocations.begin(), c->allocations.end(), p);
+  if (it == c->allocations.end()) return;
+  c->allocations.erase(it);
+  if (c->opt.free) c->opt.free(p, c->opt.alloc_user);
+  else cudaFree(p);
+}
+
+template <class T>
+T* alloc_n(zpic_ctx* c, size_t n) {
+  T* p = (T*)dev_alloc(c, n * sizeof(T));
+  CUDA_OR_THROW(cudaMemsetAsync(p, 0, n * sizeof(T), c->stream));
+  return p;
+}
+
+int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+void alloc_store(zpic_ctx* c, int s, int cap) {
+  PStore& ps = c->ps[s];
+  size_t n = (size_t)cap * c->ntiles;
+  ps.cap = cap;
+  ps.cell = alloc_n<int32_t>(c, n);
+  ps.x = alloc_n<float>(c, n);
+  ps.y = alloc_n<float>(c, n);
+  ps.ux = alloc_n<float>(c, n);
+  ps.uy = alloc_n<float>(c, n);
+  ps.uz = alloc_n<float>(c, n);
+  ps.id = c->opt.track_ids ? alloc_n<uint32_t>(c, n) : nullptr;
+  ps.cnt = alloc_n<int32_t>(c, c->ntiles);
+}
+
+void free_store(zpic_ctx* c, int s) {
+  PStore& ps = c->ps[s];
+  dev_free(c, ps.cell); dev_free(c, ps.x); dev_free(c, ps.y); dev_free(c, ps.ux); dev_free(c, ps.uy);
+  dev_free(c, ps.uz); dev_free(c, ps.id); dev_free(c, ps.cnt);
+  ps = PStore{};
+}
+
+PList alloc_list(zpic_ctx* c, int cap) {
+  PList L{};
+  L.cap = cap;
+  L.cell = alloc_n<int32_t>(c, cap);
+  L.x = alloc_n<float>(c, cap);
+  L.y = alloc_n<float>(c, cap);
+  L.ux = alloc_n<float>(c, cap);
+  L.uy = alloc_n<float>(c, cap);
+  L.uz = alloc_n<float>(c, cap);
+  L.id = c->opt.track_ids ? alloc_n<uint32_t>(c, cap) : nullptr;
+  L.species = alloc_n<int32_t>(c, cap);
+  L.count = alloc_n<int32_t>(c, 1);
+  return L;
+}
+
+// Guard mode of an axis for a field (E, B) or the current.
+int field_guard_mode(int bc) { return bc == ZPIC_BC_PERIODIC ? 1 : 2; }
+
+void refresh_field_guards(zpic_ctx* c, float* F, bool is_E) {
+  const int kx = (is_E && c->bcx == ZPIC_BC_OPEN) ? 0b110 : 0;  // Ey, Ez keep node nx
+  const int ky = (is_E && c->bcy == ZPIC_BC_OPEN) ? 0b101 : 0;  // Ex, Ez keep node ny
+  launch_guard_x(F, c->g, kx ? 3 : field_guard_mode(c->bcx), kx, c->stream);
+  launch_guard_y(F, c->g, ky ? 3 : field_guard_mode(c->bcy), ky, c->stream);
+}
+
+// ---- profiling ---------------------------------------------------------------------------
+enum KId { K_PUSH = 0, K_INSERT, K_ASSEMBLE, K_LOOSE, K_FOLD, K_YEE, K_EPI, K_COUNT };
+const char* kNames[K_COUNT] = {"k_push_tiles", "k_insert", "k_assemble_j", "k_push_loose", "k_guard_fold", "k_yee",
+                               "k_epilogue"};
+
+struct ProfScope {
+  zpic_ctx* c;
+  int id;
+  cudaEvent_t a = nullptr, b = nullptr;
+  ProfScope(zpic_ctx* c_, int id_) : c(c_), id(id_) {
+    if (!c->prof) return;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, c->stream);
+  }
+  ~ProfScope() {
+    if (!c->prof) return;
+    cudaEventRecord(b, c->stream);
+    c->prof_ev.push_back(a);
+    c->prof_ev.push_back(b);
+    c->prof_pending.push_back({id, (int)c->prof_ev.size() - 2});
+  }
+};
+
+void drain_profile(zpic_ctx* c) {
+  for (auto& pr : c->prof_pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(c->prof_ev[pr.second + 1]);
+    cudaEventElapsedTime(&ms, c->prof_ev[pr.second], c->prof_ev[pr.second + 1]);
+    c->prof_ms[pr.first] += ms;
+    c->prof_count[pr.first] += 1;
+  }
+  for (auto e : c->prof_ev) cudaEventDestroy(e);
+  c->prof_ev.clear();
+  c->prof_pending.clear();
+}
+
+PushParams push_params(zpic_ctx* c) {
+  PushParams p{};
+  p.g = c->g;
+  p.E = c->E[c->cur];
+  p.B = c->B[c->cur];
+  p.J = c->J;
+  p.Jt = c->Jt;
+  p.T = c->T; p.ntx = c->ntx; p.nty = c->nty;
+  p.nspecies = c->nspecies;
+  for (int s = 0; s < c->nspecies; ++s) { p.sc[s] = c->sc[s]; p.ps[s] = c->ps[s]; }
+  p.movers = c->movers;
+  p.spill_in = c->spill[c->steps & 1];
+  p.spill_out = c->spill[(c->steps + 1) & 1];
+  p.dtdx = (float)(c->dt / c->dx);
+  p.dtdy = (float)(c->dt / c->dy);
+  p.bcx = c->bcx; p.bcy = c->bcy;
+  p.ke_slots = c->ke_slots;
+  p.err = c->err;
+  return p;
+}
+
+zpic_status check_sticky(zpic_ctx* c) {
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) { c->last_error = std::string("CUDA: ") + cudaGetErrorString(e); return ZPIC_E_CUDA; }
+  int err = 0;
+  cudaMemcpy(&err, c->err, sizeof(int), cudaMemcpyDeviceToHost);
+  if (err & ERR_OVERFLOW) { c->last_error = "particle capacity overflow (mover / loose list full)"; return ZPIC_E_OVERFLOW; }
+  if (err & ERR_MIGRATION) { c->last_error = "a particle moved >= 1 cell in one step"; return ZPIC_E_MIGRATION; }
+  return ZPIC_OK;
+}
+
+}  // namespace
+
+// =============================================================================================
+extern "C" {
+
+const char* zpic_last_error(const zpic_ctx* ctx) { return ctx ? ctx->last_error.c_str() : g_init_error.c_str(); }
+
+zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zpic_species* species, int32_t n_species,
+                      const zpic_boundaries* bc, uint64_t seed, const zpic_options* options, const zpic_dist* dist) {
+  if (!out || !grid || !species || !bc) { g_init_error = "NULL argument"; return ZPIC_E_INVALID; }
+  *out = nullptr;
+  if (grid->nx < 1 || grid->ny < 1) { g_init_error = "nx, ny must be >= 1"; return ZPIC_E_EMPTY_GRID; }
+  if (grid->nx < 2 || grid->ny < 2 || grid->nx > 32767 || grid->ny > 32767) {
+    g_init_error = "nx, ny must be in [2, 32767]"; return ZPIC_E_INVALID;
+  }
+  if (!(grid->dx > 0) || !(grid->dy > 0) || !(dt > 0)) { g_init_error = "dx, dy, dt must be > 0"; return ZPIC_E_INVALID; }
+  const double cfl = 1.0 / std::sqrt(1.0 / (grid->dx * grid->dx) + 1.0 / (grid->dy * grid->dy));
+  if (dt >= cfl) { g_init_error = "CFL: dt >= " + std::to_string(cfl); return ZPIC_E_CFL; }
+  if (n_species < 0 || n_species > kMaxSpecies) { g_init_error = "n_species must be in [0, 4]"; return ZPIC_E_INVALID; }
+  for (int s = 0; s < n_species; ++s) {
+    const zpic_species& sp = species[s];
+    if (sp.ppc[0] < 1 || sp.ppc[1] < 1 || sp.m_q == 0.0 || !(sp.n >= 0))
+      { g_init_error = "species " + std::to_string(s) + ": ppc >= 1, m_q != 0, n >= 0"; return ZPIC_E_INVALID; }
+    for (int k = 0; k < 3; ++k)
+      if (sp.uth[k] < 0) { g_init_error = "species " + std::to_string(s) + ": uth >= 0"; return ZPIC_E_INVALID; }
+  }
+  if (bc->y == ZPIC_BC_MOVING_WINDOW) { g_init_error = "moving window is x only"; return ZPIC_E_INVALID; }
+  if (bc->x == ZPIC_BC_MOVING_WINDOW) { g_init_error = "moving window not supported yet"; return ZPIC_E_INVALID; }
+  if (bc->x == ZPIC_BC_OPEN || bc->y == ZPIC_BC_OPEN) { g_init_error = "open boundaries not supported yet"; return ZPIC_E_INVALID; }
+  int world = 1, rank = 0;
+  if (dist && dist->world > 1) {
+    g_init_error = "multi-GPU slabs not supported yet"; return ZPIC_E_DECOMP;
+  }
+  (void)rank; (void)world;
+
+  zpic_ctx* c = new zpic_ctx();
+  try {
+    c->opt = zpic_options{};
+    c->opt.tile[0] = c->opt.tile[1] = 16;
+    c->opt.capacity_slack = 1.25;
+    c->opt.mover_fraction = 0.05;
+    if (options) {
+      c->opt = *options;
+      if (c->opt.tile[0] == 0) c->opt.tile[0] = c->opt.tile[1] = 16;
+      if (c->opt.capacity_slack <= 0) c->opt.capacity_slack = 1.25;
+      if (c->opt.mover_fraction <= 0) c->opt.mover_fraction = 0.05;
+    }
+    if (c->opt.tile[0] != c->opt.tile[1] || (c->opt.tile[0] != 8 && c->opt.tile[0] != 16 && c->opt.tile[0] != 32))
+      throw Fail{ZPIC_E_INVALID, "tile must be 8x8, 16x16 or 32x32"};
+    if (c->opt.stream) { c->stream = (cudaStream_t)c->opt.stream; c->own_stream = false; }
+    else { CUDA_OR_THROW(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)); c->own_stream = true; }
+    c->prof = c->opt.profile != 0;
+    c->prof_ms.assign(K_COUNT, 0.0);
+    c->prof_count.assign(K_COUNT, 0);
+    if (dist) c->dist = *dist; else c->dist = zpic_dist{0, 1, nullptr, 0};
+    c->nx_global = grid->nx; c->ny_global = grid->ny; c->y0 = 0;
+    c->dx = grid->dx; c->dy = grid->dy; c->dt = dt;
+    c->bcx = bc->x; c->bcy = bc->y;
+    c->nspecies = n_species;
+    c->seed = seed;
+    for (int s = 0; s < n_species; ++s) c->species[s] = species[s];
+    GridDesc& g = c->g;
+    g.nx = grid->nx; g.ny = grid->ny;
+    g.pitch = round_up(g.nx + kXOff + 2, 32);
+    g.rows = g.ny + 3;
+    g.plane = (long)g.rows * g.pitch;
+    c->T = c->opt.tile[0];
+    c->ntx = (g.nx + c->T - 1) / c->T;
+    c->nty = (g.ny + c->T - 1) / c->T;
+    c->ntiles = c->ntx * c->nty;
+    for (int s = 0; s < n_species; ++s) {
+      const zpic_species& sp = species[s];
+      const int ppc = sp.ppc[0] * sp.ppc[1];
+      SpeciesConst& k = c->sc[s];
+      const double q = (sp.m_q > 0 ? 1.0 : -1.0) * sp.n / ppc;   // R8
+      k.q = (float)q;
+      k.h = (float)(0.5 * dt / sp.m_q);
+      k.jx = (float)(q * grid->dx / dt);
+      k.jy = (float)(q * grid->dy / dt);
+      k.ke_scale = q * sp.m_q * grid->dx * grid->dy;
+    }
+    // fields
+    for (int b = 0; b < 2; ++b) { c->E[b] = alloc_n<float>(c, 3 * g.plane); c->B[b] = alloc_n<float>(c, 3 * g.plane); }
+    c->J = alloc_n<float>(c, 3 * g.plane);
+    c->Jpre = nullptr;
+    const int WJ = c->T + 3;
+    c->Jt = alloc_n<float>(c, (size_t)c->ntiles * 3 * WJ * WJ);
+    c->ke_slots = alloc_n<double>(c, kMaxSpecies * kEnergySlots);
+    c->fe_slots = alloc_n<double>(c, kEnergySlots);
+    c->energy = alloc_n<double>(c, 1 + 2 * kMaxSpecies);
+    c->err = alloc_n<int>(c, 1);
+    c->stats = alloc_n<int>(c, 4);
+    {
+      double kes[kMaxSpecies] = {0, 0, 0, 0};
+      for (int s = 0; s < n_species; ++s) kes[s] = c->sc[s].ke_scale;
+      CUDA_OR_THROW(cudaMemcpyAsync(c->energy + 1 + kMaxSpecies, kes, sizeof(kes), cudaMemcpyHostToDevice, c->stream));
+    }
+    // particles: per-tile capacity from the largest initial tile count
+    int64_t total = 0;
+    for (int s = 0; s < n_species; ++s) {
+      const zpic_species& sp = species[s];
+      const int ppc = sp.ppc[0] * sp.ppc[1];
+      int col_lo = 0, col_hi = g.nx;
+      if (sp.profile == ZPIC_DENS_SLAB) {
+        col_lo = (int)std::ceil(sp.x0 / grid->dx - 0.5);
+        col_hi = (int)std::ceil(sp.x1 / grid->dx - 0.5);
+        col_lo = std::max(0, std::min(g.nx, col_lo));
+        col_hi = std::max(col_lo, std::min(g.nx, col_hi));
+      }
+      int maxcount = c->T * c->T * ppc;
+      if (sp.profile == ZPIC_DENS_NONE || sp.n == 0.0) { col_lo = col_hi = 0; }
+      const int cap = std::max(32, round_up((int)std::ceil(maxcount * c->opt.capacity_slack), 32));
+      if ((double)cap * c->ntiles > 2.0e9) throw Fail{ZPIC_E_INVALID, "particle store exceeds 2^31 slots"};
+      alloc_store(c, s, cap);
+      if (col_hi > col_lo) {
+        InjectParams q{};
+        q.ps = c->ps[s];
+        q.T = c->T; q.ntx = c->ntx; q.nx_global = g.nx; q.y0 = c->y0; q.ny = g.ny;
+        q.px = sp.ppc[0]; q.py = sp.ppc[1];
+        q.col_lo = col_lo; q.col_hi = col_hi;
+        q.key = host_mix64(host_mix64(seed) + (uint64_t)s);
+        for (int k = 0; k < 3; ++k) { q.ufl[k] = sp.ufl[k]; q.uth[k] = sp.uth[k]; }
+        launch_inject(q, c->ntiles, c->stream);
+        total += (int64_t)(col_hi - col_lo) * g.ny * ppc;
+      }
+    }
+    const int mcap = std::max<int64_t>(65536, (int64_t)std::ceil(total * c->opt.mover_fraction));
+    c->movers = alloc_list(c, (int)mcap);
+    c->spill[0] = alloc_list(c, (int)mcap);
+    c->spill[1] = alloc_list(c, (int)mcap);
+    c->cur = 0;
+    c->steps = 0;
+    CUDA_OR_THROW(cudaGetLastError());
+    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  } catch (const Fail& f) {
+    g_init_error = f.msg;
+    zpic_free(c);
+    return f.st;
+  }
+  *out = c;
+  return ZPIC_OK;
+}
+
+zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t* ix, const int32_t* iy, const float* x,
+                               const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id) {
+  if (!c) return ZPIC_E_INVALID;
+  if (s < 0 || s >= c->nspecies || n < 0 || (n > 0 && (!ix || !iy || !x || !y || !ux || !uy || !uz))) {
+    c->last_error = "set_particles: bad arguments"; return ZPIC_E_INVALID;
+  }
+  try {
+    std::vector<int> counts(c->ntiles, 0);
+    for (int64_t k = 0; k < n; ++k) {
+      const int cx = ix[k], cy = iy[k] - c->y0;
+      if (cx < 0 || cx >= c->g.nx || cy < 0 || cy >= c->g.ny || !(x[k] >= 0.f && x[k] < 1.f) || !(y[k] >= 0.f && y[k] < 1.f))
+        throw Fail{ZPIC_E_INVALID, "set_particles: particle " + std::to_string(k) + " outside the local slab or offset not in [0,1)"};
+      counts[(cy / c->T) * c->ntx + cx / c->T]++;
+    }
+    int maxc = 0;
+    for (int v : counts) maxc = std::max(maxc, v);
+    const int ppc = c->species[s].ppc[0] * c->species[s].ppc[1];
+    const int cap = std::max({32, round_up((int)std::ceil(maxc * c->opt.capacity_slack), 32),
+                              round_up((int)std::ceil(c->T * c->T * ppc * c->opt.capacity_slack), 32)});
+    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+    free_store(c, s);
+    alloc_store(c, s, cap);
+    if (n > 0) {
+      char* tmp = (char*)dev_alloc(c, (size_t)n * (7 * 4 + 4));
+      int32_t* dix = (int32_t*)tmp;
+      int32_t* diy = dix + n;
+      float* dx_ = (float*)(diy + n);
+      float* dy_ = dx_ + n;
+      float* dux = dy_ + n;
+      float* duy = dux + n;
+      float* duz = duy + n;
+      uint32_t* did = (uint32_t*)(duz + n);
+      CUDA_OR_THROW(cudaMemcpyAsync(dix, ix, n * 4, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(diy, iy, n * 4, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(dx_, x, n * 4, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(dy_, y, n * 4, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(dux, ux, n * 4, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(duy, uy, n * 4, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(duz, uz, n * 4, cudaMemcpyHostToDevice, c->stream));
+      if (id) CUDA_OR_THROW(cudaMemcpyAsync(did, id, n * 4, cudaMemcpyHostToDevice, c->stream));
+      launch_bin(c->ps[s], c->T, c->ntx, c->y0, (long)n, dix, diy, dx_, dy_, dux, duy, duz, id ? did : nullptr, c->err,
+                 c->stream);
+      CUDA_OR_THROW(cudaGetLastError());
+      CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+      dev_free(c, tmp);
+    }
+    // movers / loose lists sized for the new population
+    int64_t total = 0;
+    for (int q = 0; q < c->nspecies; ++q) {
+      std::vector<int> cnt(c->ntiles);
+      CUDA_OR_THROW(cudaMemcpy(cnt.data(), c->ps[q].cnt, c->ntiles * 4, cudaMemcpyDeviceToHost));
+      for (int v : cnt) total += v;
+    }
+    const int need = (int)std::max<int64_t>(65536, (int64_t)std::ceil(total * c->opt.mover_fraction));
+    if (need > c->movers.cap) {
+      for (PList* L : {&c->movers, &c->spill[0], &c->spill[1]}) {
+        dev_free(c, L->cell); dev_free(c, L->x); dev_free(c, L->y); dev_free(c, L->ux); dev_free(c, L->uy);
+        dev_free(c, L->uz); dev_free(c, L->id); dev_free(c, L->species); dev_free(c, L->count);
+        *L = alloc_list(c, need);
+      }
+    }
+    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  } catch (const Fail& f) {
+    c->last_error = f.msg;
+    return f.st;
+  }
+  return check_sticky(c);
+}
+
+zpic_status zpic_set_fields(zpic_ctx* c, int32_t which, const float* in, size_t in_len) {
+  if (!c || !in || (which != 0 && which != 1)) return ZPIC_E_INVALID;
+  const GridDesc& g = c->g;
+  if (in_len < (size_t)3 * g.nx * g.ny) { c->last_error = "set_fields: buffer too small"; return ZPIC_E_BUFSIZE; }
+  float* F = which == 0 ? c->E[c->cur] : c->B[c->cur];
+  for (int k = 0; k < 3; ++k) {
+    cudaError_t e = cudaMemcpy2DAsync(F + k * g.plane + g.at(0, 0), g.pitch * 4, in + (size_t)k * g.nx * g.ny, g.nx * 4,
+                                      g.nx * 4, g.ny, cudaMemcpyHostToDevice, c->stream);
+    if (e != cudaSuccess) { c->last_error = cudaGetErrorString(e); return ZPIC_E_CUDA; }
+  }
+  refresh_field_guards(c, F, which == 0);
+  return check_sticky(c);
+}
+
+zpic_status zpic_step(zpic_ctx* c, int32_t n) {
+  if (!c || n < 0) return ZPIC_E_INVALID;
+  const int grid_small = 148 * 4;
+  for (int k = 0; k < n; ++k) {
+    PushParams p = push_params(c);
+    { ProfScope ps(c, K_PUSH); launch_push_tiles(p, c->ntiles, c->stream); }
+    { ProfScope ps(c, K_INSERT); launch_insert(p, grid_small, c->stream); }
+    { ProfScope ps(c, K_ASSEMBLE); launch_assemble(c->J, c->Jt, c->g, c->T, c->ntx, c->nty, c->stream); }
+    { ProfScope ps(c, K_LOOSE); launch_loose(p, grid_small, c->stream); }
+    {
+      ProfScope ps(c, K_FOLD);
+      launch_guard_x(c->J, c->g, c->bcx == ZPIC_BC_PERIODIC ? 0 : 2, 0, c->stream);
+      launch_guard_y(c->J, c->g, c->bcy == ZPIC_BC_PERIODIC ? 0 : 2, 0, c->stream);
+    }
+    {
+      ProfScope ps(c, K_YEE);
+      YeeParams y{};
+      y.g = c->g;
+      y.E0 = c->E[c->cur]; y.B0 = c->B[c->cur]; y.J = c->J;
+      y.E1 = c->E[c->cur ^ 1]; y.B1 = c->B[c->cur ^ 1];
+      y.dt = (float)c->dt;
+      y.dtdx = (float)(c->dt / c->dx); y.dtdy = (float)(c->dt / c->dy);
+      y.hdx = (float)(0.5 * c->dt / c->dx); y.hdy = (float)(0.5 * c->dt / c->dy);
+      y.bcx = c->bcx; y.bcy = c->bcy;
+      y.fe_slots = c->fe_slots;
+      y.fe_scale = 0.5 * c->dx * c->dy;
+      launch_yee(y, c->stream);
+    }
+    {
+      ProfScope ps(c, K_EPI);
+      launch_epilogue(c->ke_slots, c->fe_slots, c->energy, c->nspecies, c->energy + 1 + kMaxSpecies, c->movers.count,
+                      p.spill_in.count, p.spill_out.count, c->stats, c->stream);
+    }
+    c->cur ^= 1;
+    c->steps += 1;
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) { c->last_error = std::string("launch: ") + cudaGetErrorString(e); return ZPIC_E_CUDA; }
+  return ZPIC_OK;
+}
+
+zpic_status zpic_sync(zpic_ctx* c) {
+  if (!c) return ZPIC_E_INVALID;
+  return check_sticky(c);
+}
+
+zpic_status zpic_get_fields(zpic_ctx* c, int32_t which, float* out, size_t out_len) {
+  if (!c || !out || which < 0 || which > 3) return ZPIC_E_INVALID;
+  zpic_status st = check_sticky(c);
+  if (st != ZPIC_OK) return st;
+  const GridDesc& g = c->g;
+  if (out_len < (size_t)3 * g.nx * g.ny) { c->last_error = "get_fields: buffer too small"; return ZPIC_E_BUFSIZE; }
+  const float* F = which == 0 ? c->E[c->cur] : which == 1 ? c->B[c->cur] : (which == 3 && c->Jpre) ? c->Jpre : c->J;
+  for (int k = 0; k < 3; ++k) {
+    cudaError_t e = cudaMemcpy2DAsync(out + (size_t)k * g.nx * g.ny, g.nx * 4, F + k * g.plane + g.at(0, 0), g.pitch * 4,
+                                      g.nx * 4, g.ny, cudaMemcpyDeviceToHost, c->stream);
+    if (e != cudaSuccess) { c->last_error = cudaGetErrorString(e); return ZPIC_E_CUDA; }
+  }
+  return check_sticky(c);
+}
+
+zpic_status zpic_get_particles(zpic_ctx* c, int32_t s, int64_t* count_inout, int32_t* ix, int32_t* iy, float* x,
+                               float* y, float* ux, float* uy, float* uz, uint32_t* id) {
+  if (!c || !count_inout || s < 0 || s >= c->nspecies) return ZPIC_E_INVALID;
+  zpic_status st = check_sticky(c);
+  if (st != ZPIC_OK) return st;
+  if (id && !c->opt.track_ids) { c->last_error = "get_particles: ids requested without track_ids"; return ZPIC_E_STATE; }
+  try {
+    std::vector<int> cnt(c->ntiles);
+    CUDA_OR_THROW(cudaMemcpy(cnt.data(), c->ps[s].cnt, c->ntiles * 4, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> prefix(c->ntiles + 1, 0);
+    for (int t = 0; t < c->ntiles; ++t) prefix[t + 1] = prefix[t] + std::min(cnt[t], c->ps[s].cap);
+    // loose particles of this species
+    const PList& L = c->spill[c->steps & 1];
+    int nl = 0;
+    CUDA_OR_THROW(cudaMemcpy(&nl, L.count, 4, cudaMemcpyDeviceToHost));
+    nl = std::min(nl, L.cap);
+    std::vector<int32_t> lsp(nl), lcell(nl);
+    std::vector<float> lf[5];
+    std::vector<uint32_t> lid(nl);
+    int nls = 0;
+    if (nl > 0) {
+      CUDA_OR_THROW(cudaMemcpy(lsp.data(), L.species, nl * 4, cudaMemcpyDeviceToHost));
+      for (int k = 0; k < nl; ++k) nls += lsp[k] == s;
+    }
+    const int64_t total = prefix[c->ntiles] + nls;
+    if (!ix) { *count_inout = total; return ZPIC_OK; }
+    if (*count_inout < total) { c->last_error = "get_particles: buffer too small"; *count_inout = total; return ZPIC_E_BUFSIZE; }
+    const int64_t nt = prefix[c->ntiles];
+    if (nt > 0) {
+      int64_t* dprefix = (int64_t*)dev_alloc(c, (c->ntiles + 1) * 8);
+      char* tmp = (char*)dev_alloc(c, (size_t)nt * 32);
+      int32_t* dix = (int32_t*)tmp;
+      int32_t* diy = dix + nt;
+      float* dxx = (float*)(diy + nt);
+      float* dyy = dxx + nt;
+      float* dux = dyy + nt;
+      float* duy = dux + nt;
+      float* duz = duy + nt;
+      uint32_t* did = (uint32_t*)(duz + nt);
+      CUDA_OR_THROW(cudaMemcpyAsync(dprefix, prefix.data(), (c->ntiles + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+      launch_export(c->ps[s], c->ntiles, dprefix, c->y0, dix, diy, dxx, dyy, dux, duy, duz, id ? did : nullptr, c->stream);
+      CUDA_OR_THROW(cudaGetLastError());
+      CUDA_OR_THROW(cudaMemcpyAsync(ix, dix, nt * 4, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(iy, diy, nt * 4, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(x, dxx, nt * 4, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(y, dyy, nt * 4, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(ux, dux, nt * 4, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(uy, duy, nt * 4, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(uz, duz, nt * 4, cudaMemcpyDeviceToHost, c->stream));
+      if (id) CUDA_OR_THROW(cudaMemcpyAsync(id, did, nt * 4, cudaMemcpyDeviceToHost, c->stream));
+      CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+      dev_free(c, tmp);
+      dev_free(c, dprefix);
+    }
+    if (nls > 0) {
+      for (auto& v : lf) v.resize(nl);
+      CUDA_OR_THROW(cudaMemcpy(lcell.data(), L.cell, nl * 4, cudaMemcpyDeviceToHost));
+      CUDA_OR_THROW(cudaMemcpy(lf[0].data(), L.x, nl * 4, cudaMemcpyDeviceToHost));
+      CUDA_OR_THROW(cudaMemcpy(lf[1].data(), L.y, nl * 4, cudaMemcpyDeviceToHost));
+      CUDA_OR_THROW(cudaMemcpy(lf[2].data(), L.ux, nl * 4, cudaMemcpyDeviceToHost));
+      CUDA_OR_THROW(cudaMemcpy(lf[3].data(), L.uy, nl * 4, cudaMemcpyDeviceToHost));
+      CUDA_OR_THROW(cudaMemcpy(lf[4].data(), L.uz, nl * 4, cudaMemcpyDeviceToHost));
+      if (L.id) CUDA_OR_THROW(cudaMemcpy(lid.data(), L.id, nl * 4, cudaMemcpyDeviceToHost));
+      int64_t o = nt;
+      for (int k = 0; k < nl; ++k) {
+        if (lsp[k] != s) continue;
+        ix[o] = lcell[k] & 0xffff;
+        iy[o] = (lcell[k] >> 16) + c->y0;
+        x[o] = lf[0][k]; y[o] = lf[1][k]; ux[o] = lf[2][k]; uy[o] = lf[3][k]; uz[o] = lf[4][k];
+        if (id) id[o] = lid[k];
+        ++o;
+      }
+    }
+    *count_inout = total;
+  } catch (const Fail& f) {
+    c->last_error = f.msg;
+    return f.st;
+  }
+  return ZPIC_OK;
+}
+
+zpic_status zpic_energy(zpic_ctx* c, int64_t* iter, double* field, double* kinetic) {
+  if (!c) return ZPIC_E_INVALID;
+  zpic_status st = check_sticky(c);
+  if (st != ZPIC_OK) return st;
+  double e[1 + kMaxSpecies] = {0, 0, 0, 0, 0};
+  if (c->steps > 0) cudaMemcpy(e, c->energy, sizeof(e), cudaMemcpyDeviceToHost);
+  if (iter) *iter = c->steps - 1;
+  if (field) *field = e[0];
+  if (kinetic)
+    for (int s = 0; s < c->nspecies; ++s) kinetic[s] = e[1 + s];
+  return ZPIC_OK;
+}
+
+zpic_status zpic_layout(zpic_ctx* c, int32_t* y0, int32_t* ny_local) {
+  if (!c) return ZPIC_E_INVALID;
+  if (y0) *y0 = c->y0;
+  if (ny_local) *ny_local = c->g.ny;
+  return ZPIC_OK;
+}
+
+zpic_status zpic_counters(zpic_ctx* c, int64_t* out, int32_t n) {
+  if (!c || !out) return ZPIC_E_INVALID;
+  zpic_status st = check_sticky(c);
+  if (st != ZPIC_OK) return st;
+  int stats[4] = {0, 0, 0, 0};
+  cudaMemcpy(stats, c->stats, sizeof(stats), cudaMemcpyDeviceToHost);
+  int64_t total = 0;
+  int maxfill = 0;
+  for (int s = 0; s < c->nspecies; ++s) {
+    std::vector<int> cnt(c->ntiles);
+    cudaMemcpy(cnt.data(), c->ps[s].cnt, c->ntiles * 4, cudaMemcpyDeviceToHost);
+    for (int v : cnt) { total += v; maxfill = std::max(maxfill, (int)(1000.0 * v / c->ps[s].cap)); }
+  }
+  int nl = 0;
+  cudaMemcpy(&nl, c->spill[c->steps & 1].count, 4, cudaMemcpyDeviceToHost);
+  const int64_t v[6] = {total + nl, stats[0], maxfill, c->repacks, c->steps, c->ntiles};
+  for (int k = 0; k < n && k < 6; ++k) out[k] = v[k];
+  return ZPIC_OK;
+}
+
+zpic_status zpic_kernel_times(zpic_ctx* c, const char** names, double* ms, int32_t* launches, int32_t* n_inout) {
+  if (!c || !n_inout) return ZPIC_E_INVALID;
+  cudaStreamSynchronize(c->stream);
+  drain_profile(c);
+  const int n = std::min<int>(*n_inout, K_COUNT);
+  for (int k = 0; k < n; ++k) {
+    if (names) names[k] = kNames[k];
+    if (ms) ms[k] = c->prof_ms[k];
+    if (launches) launches[k] = c->prof_count[k];
+    c->prof_ms[k] = 0.0;
+    c->prof_count[k] = 0;
+  }
+  *n_inout = K_COUNT;
+  return ZPIC_OK;
+}
+
+void zpic_free(zpic_ctx* c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto e : c->prof_ev) cudaEventDestroy(e);
+  for (void* p : c->allocations) {
+    if (c->opt.free) c->opt.free(p, c->opt.alloc_user);
+    else cudaFree(p);
+  }
+  c->allocations.clear();
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+}  // extern "C"

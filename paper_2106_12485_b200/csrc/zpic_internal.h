@@ -1,0 +1,140 @@
+// zpic_internal.h — device data layout and kernel parameter blocks of the B200 EM-PIC path.
+// Not part of the ABI (include/zpic.h is).  Layouts are documented in DESIGN.md "Data layout".
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/zpic.h"
+
+namespace zpic {
+
+constexpr int kMaxSpecies = 4;
+constexpr int kXOff = 4;          // interior column 0 sits at column 4 of a padded row (16 B aligned)
+constexpr int kEnergySlots = 256; // fp64 partial-sum slots (spread the atomics), per quantity
+constexpr int kBlock = 256;       // threads per CTA of the particle kernels
+
+// A guard-extended field grid: 3 planes of `rows` x `pitch` floats; interior cell (i, j) of a
+// plane is at (j + 1) * pitch + (i + kXOff), valid for -1 <= i <= nx + 1, -1 <= j <= ny + 1
+// (guards 1 low / 2 high per axis).
+struct GridDesc {
+  int nx, ny;      // local interior cells
+  int pitch;       // floats per row (multiple of 32)
+  int rows;        // ny + 3
+  long plane;      // rows * pitch
+  __host__ __device__ long at(int i, int j) const { return (long)(j + 1) * pitch + (i + kXOff); }
+};
+
+// One species' tile-sorted SoA particle store.  Tile t owns slots [t * cap, t * cap + cnt[t]).
+// cell packs the local cell index: ix | iy << 16.
+struct PStore {
+  int32_t* cell;
+  float *x, *y, *ux, *uy, *uz;
+  uint32_t* id;   // nullptr unless track_ids
+  int32_t* cnt;   // [ntiles]
+  int cap;        // slots per tile (multiple of 32)
+};
+
+// Particles that left their tile (or could not be inserted): a flat SoA list.
+struct PList {
+  int32_t* cell;
+  float *x, *y, *ux, *uy, *uz;
+  uint32_t* id;
+  int32_t* species;
+  int32_t* count;  // device counter
+  int cap;
+};
+
+struct SpeciesConst {
+  float q;      // per-particle charge q_s = sign(m_q) n / ppc (R8)
+  float h;      // dt / (2 m_q)  (Boris half-kick factor)
+  float jx, jy; // q dx/dt, q dy/dt (deposit flux scales)
+  double ke_scale;  // q m_q dx dy
+};
+
+// Everything the particle kernels need, passed by value.
+struct PushParams {
+  GridDesc g;
+  const float* E;   // current E (3 planes)
+  const float* B;
+  float* J;         // assembled J grid (loose-particle deposits)
+  float* Jt;        // per-tile J blocks [ntiles][3][(T+3)^2]
+  int T, ntx, nty;
+  int nspecies;
+  SpeciesConst sc[kMaxSpecies];
+  PStore ps[kMaxSpecies];
+  PList movers;     // written by the tile kernel this step
+  PList spill_in;   // loose particles to push this step
+  PList spill_out;  // loose particles for the next step
+  float dtdx, dtdy; // dt/dx, dt/dy
+  int bcx, bcy;
+  double* ke_slots; // [kMaxSpecies][kEnergySlots]
+  int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
+};
+
+struct YeeParams {
+  GridDesc g;
+  const float* E0; const float* B0; const float* J;
+  float* E1; float* B1;
+  float dt, dtdx, dtdy, hdx, hdy;   // dt, dt/dx, dt/dy, (dt/2)/dx, (dt/2)/dy
+  int bcx, bcy;
+  double* fe_slots;
+  double fe_scale;  // dx dy / 2
+};
+
+struct InjectParams {
+  PStore ps;
+  int T, ntx, nx_global, y0, ny;
+  int px, py;
+  int col_lo, col_hi;   // filled global columns [col_lo, col_hi)
+  uint64_t key;         // mix64(mix64(seed) + species)
+  double ufl[3], uth[3];
+};
+
+enum ErrBits { ERR_OVERFLOW = 1, ERR_MIGRATION = 2 };
+
+}  // namespace zpic
+
+// The opaque ABI handle.
+struct zpic_ctx {
+  zpic::GridDesc g;
+  int nx_global, ny_global, y0;
+  double dx, dy, dt;
+  int bcx, bcy;
+  int nspecies;
+  zpic_species species[zpic::kMaxSpecies];
+  zpic::SpeciesConst sc[zpic::kMaxSpecies];
+  uint64_t seed;
+  zpic_options opt;
+  zpic_dist dist;
+  int T, ntx, nty, ntiles;
+  cudaStream_t stream;
+  bool own_stream;
+  // device buffers
+  float* E[2];
+  float* B[2];
+  float* J;        // assembled (and folded, filtered) current used by the field advance
+  float* Jpre;     // pre-filter copy (only with a filter)
+  float* Jt;       // per-tile blocks
+  zpic::PStore ps[zpic::kMaxSpecies];
+  zpic::PList movers, spill[2];
+  double* ke_slots;
+  double* fe_slots;
+  double* energy;  // [1 + kMaxSpecies] last finished step: FE, KE_s
+  int* err;
+  int* stats;      // [0] movers of last step, [1] spill count
+  int cur;         // index of the current E/B buffer
+  int64_t steps;
+  int64_t repacks;
+  std::vector<void*> allocations;
+  std::string last_error;
+  // profiling
+  bool prof;
+  std::vector<std::string> prof_names;
+  std::vector<cudaEvent_t> prof_ev;  // pairs
+  std::vector<double> prof_ms;
+  std::vector<int> prof_count;
+  std::vector<std::pair<int, int>> prof_pending;  // (kernel id, event pair index)
+};

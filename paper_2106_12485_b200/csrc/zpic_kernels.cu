@@ -1,0 +1,607 @@
+// zpic_kernels.cu — the sm_100a kernels of the B200 EM-PIC step.
+//   K1 k_push_tiles   fused gather + Boris + charge-conserving deposit + cell update + tile
+//                     compaction, one CTA per tile, fields and current in shared memory
+//   K3 k_insert       movers -> destination tile slack (or the loose list)
+//   K4 k_assemble_j   per-tile current blocks -> guard-extended J grid (plain stores, no atomics)
+//   K1L k_push_loose  the loose list: same physics, global-memory fields / current
+//   K4b k_guard_x/y   ghost-current reduction and guard refresh
+//   K5 k_yee          fused B half step, E step, B half step on a 32x32 tile
+//   K0 k_inject       counter-based lattice injection
+//   k_epilogue        energies, counters
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "zpic_kernels.cuh"
+
+namespace zpic {
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// warp-aggregated slot reservation on a global counter
+__device__ __forceinline__ int warp_reserve(int* counter, bool want) {
+  const unsigned m = __ballot_sync(0xffffffffu, want);
+  if (!m) return -1;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return want ? base + __popc(m & lanemask_lt()) : -1;
+}
+
+__device__ __forceinline__ void block_add_double(double v, double* slot) {
+  __shared__ double s_red[kBlock / 32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0) s_red[w] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < kBlock / 32; ++k) t += s_red[k];
+    if (t != 0.0) atomicAdd(slot, t);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ int pack_cell(int ix, int iy) { return (ix & 0xffff) | (iy << 16); }
+__device__ __forceinline__ int cell_ix(int c) { return c & 0xffff; }
+__device__ __forceinline__ int cell_iy(int c) { return c >> 16; }
+
+// Apply the particle boundary conditions to a new cell (a5).  Returns false if the particle
+// leaves the domain through an open / window edge (removed).
+__device__ __forceinline__ bool domain_bc(int& ix, int& iy, const GridDesc& g, int bcx, int bcy) {
+  if (ix < 0 || ix >= g.nx) {
+    if (bcx != ZPIC_BC_PERIODIC) return false;
+    ix += ix < 0 ? g.nx : -g.nx;
+  }
+  if (iy < 0 || iy >= g.ny) {
+    if (bcy != ZPIC_BC_PERIODIC) return false;
+    iy += iy < 0 ? g.ny : -g.ny;
+  }
+  return true;
+}
+
+__device__ __forceinline__ void list_put(const PList& L, int k, int cell, float x, float y, float ux, float uy, float uz,
+                                         uint32_t id, int s) {
+  L.cell[k] = cell; L.x[k] = x; L.y[k] = y; L.ux[k] = ux; L.uy[k] = uy; L.uz[k] = uz;
+  if (L.id) L.id[k] = id;
+  L.species[k] = s;
+}
+
+// Insert one particle into its tile's slack, else into the loose list.
+__device__ __forceinline__ void insert_particle(const PushParams& p, int s, int ix, int iy, float x, float y, float ux,
+                                                float uy, float uz, uint32_t id) {
+  const int t = (iy / p.T) * p.ntx + (ix / p.T);
+  const PStore& ps = p.ps[s];
+  const int slot = atomicAdd(ps.cnt + t, 1);
+  const int cell = pack_cell(ix, iy);
+  if (slot < ps.cap) {
+    const long k = (long)t * ps.cap + slot;
+    ps.cell[k] = cell; ps.x[k] = x; ps.y[k] = y; ps.ux[k] = ux; ps.uy[k] = uy; ps.uz[k] = uz;
+    if (ps.id) ps.id[k] = id;
+  } else {
+    atomicSub(ps.cnt + t, 1);
+    const int k = atomicAdd(p.spill_out.count, 1);
+    if (k < p.spill_out.cap) list_put(p.spill_out, k, cell, x, y, ux, uy, uz, id, s);
+    else atomicOr(p.err, ERR_OVERFLOW);
+  }
+}
+
+// =============================================================================================
+// K1: one CTA per tile.  Stage the tile's E, B (+1 guard cell each side) in shared memory, zero a
+// shared (T+3)^2 current block, push every particle of every species of the tile (one thread
+// per particle, chunks of kBlock), write the particles that stay back compacted in place, send
+// the others to the mover list, and finally store the current block to Jt (plain stores; K4
+// sums the overlapping blocks).
+template <int T>
+__global__ void __launch_bounds__(kBlock) k_push_tiles(PushParams p) {
+  constexpr int W = T + 2, WJ = T + 3;
+  __shared__ float2 s_eb1[W * W], s_eb2[W * W];
+  __shared__ float s_ez[W * W], s_bz[W * W];
+  __shared__ float s_j[3 * WJ * WJ];
+  __shared__ int s_wsum[2][kBlock / 32];
+
+  const int t = blockIdx.x;
+  const int tx = t % p.ntx, ty = t / p.ntx;
+  const int i0 = tx * T, j0 = ty * T;
+  const int tw = min(T, p.g.nx - i0), th = min(T, p.g.ny - j0);
+  const long pl = p.g.plane;
+
+  for (int k = threadIdx.x; k < W * W; k += kBlock) {
+    const int gi = i0 + k % W - 1, gj = j0 + k / W - 1;
+    float ex = 0.f, ey = 0.f, ez = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
+    if (gi <= p.g.nx + 1 && gj <= p.g.ny + 1) {
+      const long a = p.g.at(gi, gj);
+      ex = __ldg(p.E + a); ey = __ldg(p.E + pl + a); ez = __ldg(p.E + 2 * pl + a);
+      bx = __ldg(p.B + a); by = __ldg(p.B + pl + a); bz = __ldg(p.B + 2 * pl + a);
+    }
+    s_eb1[k] = make_float2(ex, by);
+    s_eb2[k] = make_float2(ey, bx);
+    s_ez[k] = ez;
+    s_bz[k] = bz;
+  }
+  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += kBlock) s_j[k] = 0.f;
+  __syncthreads();
+
+  const SmemFields F{s_eb1, s_eb2, s_ez, s_bz, W};
+  const SmemCurrent A{s_j, WJ};
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned ltmask = lanemask_lt();
+  int buf = 0;
+
+  for (int s = 0; s < p.nspecies; ++s) {
+    const PStore& ps = p.ps[s];
+    const SpeciesConst sc = p.sc[s];
+    const int n = ps.cnt[t];
+    const long base = (long)t * ps.cap;
+    int out = 0;
+    float ke = 0.f;
+    for (int c0 = 0; c0 < n; c0 += kBlock) {
+      const int i = c0 + threadIdx.x;
+      const bool valid = i < n;
+      int cell = 0;
+      float x = 0.f, y = 0.f, ux = 0.f, uy = 0.f, uz = 0.f;
+      uint32_t id = 0;
+      if (valid) {
+        const long k = base + i;
+        cell = __ldcs(ps.cell + k);
+        x = __ldcs(ps.x + k); y = __ldcs(ps.y + k);
+        ux = __ldcs(ps.ux + k); uy = __ldcs(ps.uy + k); uz = __ldcs(ps.uz + k);
+        if (ps.id) id = __ldcs(ps.id + k);
+      }
+      bool stay = false, move = false;
+      int ix = 0, iy = 0;
+      if (valid) {
+        ix = cell_ix(cell); iy = cell_iy(cell);
+        const int lx = ix - i0, ly = iy - j0;
+        float ex, ey, ez, bx, by, bz;
+        interpolate(F, lx, ly, x, y, ex, ey, ez, bx, by, bz);
+        ke += boris(ux, uy, uz, ex, ey, ez, bx, by, bz, sc.h);
+        const float rg = rsqrtf(1.0f + fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+        const float dxp = ux * rg * p.dtdx, dyp = uy * rg * p.dtdy;
+        if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(p.err, ERR_MIGRATION);
+        int di, dj;
+        advance_deposit(A, lx, ly, x, y, dxp, dyp, sc.jx, sc.jy, sc.q * uz * rg, di, dj);
+        ix += di; iy += dj;
+        if ((unsigned)(lx + di) < (unsigned)tw && (unsigned)(ly + dj) < (unsigned)th) {
+          stay = true;
+        } else {
+          move = domain_bc(ix, iy, p.g, p.bcx, p.bcy);
+        }
+      }
+      // block-wide exclusive scan of `stay` -> compacted in-place write
+      const unsigned bal = __ballot_sync(0xffffffffu, stay);
+      if (lane == 0) s_wsum[buf][warp] = __popc(bal);
+      __syncthreads();
+      int before = 0, tot = 0;
+#pragma unroll
+      for (int w = 0; w < kBlock / 32; ++w) {
+        const int v = s_wsum[buf][w];
+        before += (w < warp) ? v : 0;
+        tot += v;
+      }
+      buf ^= 1;
+      if (stay) {
+        const long k = base + out + before + __popc(bal & ltmask);
+        __stcs(ps.cell + k, pack_cell(ix, iy));
+        __stcs(ps.x + k, x); __stcs(ps.y + k, y);
+        __stcs(ps.ux + k, ux); __stcs(ps.uy + k, uy); __stcs(ps.uz + k, uz);
+        if (ps.id) __stcs(ps.id + k, id);
+      }
+      out += tot;
+      const int m = warp_reserve(p.movers.count, move);
+      if (move) {
+        if (m < p.movers.cap) list_put(p.movers, m, pack_cell(ix, iy), x, y, ux, uy, uz, id, s);
+        else atomicOr(p.err, ERR_OVERFLOW);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) ps.cnt[t] = out;
+    block_add_double((double)ke, p.ke_slots + s * kEnergySlots + (t & (kEnergySlots - 1)));
+  }
+  __syncthreads();
+  float* jt = p.Jt + (long)t * 3 * WJ * WJ;
+  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += kBlock) __stcg(jt + k, s_j[k]);
+}
+
+// =============================================================================================
+// K3: movers -> destination tiles (grid-stride over the device-side count).
+__global__ void __launch_bounds__(kBlock) k_insert(PushParams p) {
+  const int n = min(*p.movers.count, p.movers.cap);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int cell = p.movers.cell[k];
+    insert_particle(p, p.movers.species[k], cell_ix(cell), cell_iy(cell), p.movers.x[k], p.movers.y[k],
+                    p.movers.ux[k], p.movers.uy[k], p.movers.uz[k], p.movers.id ? p.movers.id[k] : 0u);
+  }
+}
+
+// =============================================================================================
+// K4: J grid node (i, j), -1 <= i <= nx+1, -1 <= j <= ny+1, = sum of the (at most 2 x 2) tile
+// blocks covering it.  No periodic wrap here: blocks at the domain edge land in the guards and
+// K4b folds them ("the reduction is only required for ghost cells").
+template <int T>
+__global__ void __launch_bounds__(kBlock) k_assemble_j(float* __restrict__ J, const float* __restrict__ Jt, GridDesc g,
+                                                       int ntx, int nty) {
+  constexpr int WJ = T + 3;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x - 1;
+  const int j = blockIdx.y - 1;
+  if (i > g.nx + 1) return;
+  int txs[2], lxs[2], nxs = 0, tys[2], lys[2], nys = 0;
+  {
+    const int th = (i + 1) / T, lh = i - th * T;
+    if (th < ntx) { txs[nxs] = th; lxs[nxs++] = lh; }
+    if (lh <= 1 && th >= 1) { txs[nxs] = th - 1; lxs[nxs++] = lh + T; }
+  }
+  {
+    const int th = (j + 1) / T, lh = j - th * T;
+    if (th < nty) { tys[nys] = th; lys[nys++] = lh; }
+    if (lh <= 1 && th >= 1) { tys[nys] = th - 1; lys[nys++] = lh + T; }
+  }
+  float v0 = 0.f, v1 = 0.f, v2 = 0.f;
+  for (int a = 0; a < nys; ++a)
+    for (int b = 0; b < nxs; ++b) {
+      const float* blk = Jt + ((long)tys[a] * ntx + txs[b]) * 3 * WJ * WJ + (lys[a] + 1) * WJ + (lxs[b] + 1);
+      v0 += __ldcg(blk);
+      v1 += __ldcg(blk + WJ * WJ);
+      v2 += __ldcg(blk + 2 * WJ * WJ);
+    }
+  const long o = g.at(i, j);
+  J[o] = v0;
+  J[g.plane + o] = v1;
+  J[2 * g.plane + o] = v2;
+}
+
+// =============================================================================================
+// K1L: loose particles (those that found no tile slack): global-memory gather, global atomics
+// into the assembled J grid (guard-extended, folded afterwards), then re-insertion.
+__global__ void __launch_bounds__(kBlock) k_push_loose(PushParams p) {
+  const int n = min(*p.spill_in.count, p.spill_in.cap);
+  const GlobalFields F{p.E, p.B, p.g};
+  const GlobalCurrent A{p.J, p.g};
+  float ke[kMaxSpecies] = {0.f, 0.f, 0.f, 0.f};
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int s = p.spill_in.species[k];
+    const SpeciesConst sc = p.sc[s];
+    const int cell = p.spill_in.cell[k];
+    int ix = cell_ix(cell), iy = cell_iy(cell);
+    float x = p.spill_in.x[k], y = p.spill_in.y[k];
+    float ux = p.spill_in.ux[k], uy = p.spill_in.uy[k], uz = p.spill_in.uz[k];
+    const uint32_t id = p.spill_in.id ? p.spill_in.id[k] : 0u;
+    float ex, ey, ez, bx, by, bz;
+    interpolate(F, ix, iy, x, y, ex, ey, ez, bx, by, bz);
+    const float kk = boris(ux, uy, uz, ex, ey, ez, bx, by, bz, sc.h);
+#pragma unroll
+    for (int q = 0; q < kMaxSpecies; ++q) ke[q] += (q == s) ? kk : 0.f;
+    const float rg = rsqrtf(1.0f + fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+    const float dxp = ux * rg * p.dtdx, dyp = uy * rg * p.dtdy;
+    if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(p.err, ERR_MIGRATION);
+    int di, dj;
+    advance_deposit(A, ix, iy, x, y, dxp, dyp, sc.jx, sc.jy, sc.q * uz * rg, di, dj);
+    ix += di; iy += dj;
+    if (domain_bc(ix, iy, p.g, p.bcx, p.bcy)) insert_particle(p, s, ix, iy, x, y, ux, uy, uz, id);
+  }
+  for (int s = 0; s < p.nspecies; ++s) block_add_double((double)ke[s], p.ke_slots + s * kEnergySlots + (blockIdx.x & (kEnergySlots - 1)));
+}
+
+// =============================================================================================
+// K4b: guard handling of a 3-component grid along x (one thread per row and component) or y
+// (one thread per column and component).
+//   mode 0: ghost-current reduction + periodic refresh (periodic axis)
+//   mode 1: periodic refresh (copies)
+//   mode 2: zero the guards (open / window axis: guard deposits discarded, fields outside = 0)
+//   mode 3: zero the guards but keep the first high guard node of components in keep_mask
+//           (Mur-updated tangential E on an open edge, R13)
+__global__ void k_guard_x(float* F, GridDesc g, int mode, int keep_mask) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int rows = g.ny + 3;
+  if (idx >= 3 * rows) return;
+  const int c = idx / rows, j = idx % rows - 1;
+  float* r = F + c * g.plane;
+  const int nx = g.nx;
+  if (mode == 0) {
+    r[g.at(nx - 1, j)] += r[g.at(-1, j)];
+    r[g.at(0, j)] += r[g.at(nx, j)];
+    r[g.at(1, j)] += r[g.at(nx + 1, j)];
+  }
+  if (mode <= 1) {
+    r[g.at(-1, j)] = r[g.at(nx - 1, j)];
+    r[g.at(nx, j)] = r[g.at(0, j)];
+    r[g.at(nx + 1, j)] = r[g.at(1, j)];
+  } else {
+    r[g.at(-1, j)] = 0.f;
+    if (!(mode == 3 && ((keep_mask >> c) & 1))) r[g.at(nx, j)] = 0.f;
+    r[g.at(nx + 1, j)] = 0.f;
+  }
+}
+
+__global__ void k_guard_y(float* F, GridDesc g, int mode, int keep_mask) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cols = g.nx + 3;
+  if (idx >= 3 * cols) return;
+  const int c = idx / cols, i = idx % cols - 1;
+  float* r = F + c * g.plane;
+  const int ny = g.ny;
+  if (mode == 0) {
+    r[g.at(i, ny - 1)] += r[g.at(i, -1)];
+    r[g.at(i, 0)] += r[g.at(i, ny)];
+    r[g.at(i, 1)] += r[g.at(i, ny + 1)];
+  }
+  if (mode <= 1) {
+    r[g.at(i, -1)] = r[g.at(i, ny - 1)];
+    r[g.at(i, ny)] = r[g.at(i, 0)];
+    r[g.at(i, ny + 1)] = r[g.at(i, 1)];
+  } else {
+    r[g.at(i, -1)] = 0.f;
+    if (!(mode == 3 && ((keep_mask >> c) & 1))) r[g.at(i, ny)] = 0.f;
+    r[g.at(i, ny + 1)] = 0.f;
+  }
+}
+
+// =============================================================================================
+// K5: Yee advance (R2) on a 32 x 32 output tile.  E^n is staged on local
+// [-1, T+2), B^n on [-1, T+1), J on [0, T+1).  B^{n+1/2} is computed on [-1, T], E^{n+1} on
+// [0, T] (the row/column T redundantly, so no second exchange is needed), B^{n+1} on [0, T).
+// Outputs go to the other buffer (E1, B1), interior plus periodic guard images, so no tile
+// reads a value another tile writes.  FE(n) of the inputs is reduced on the way.
+constexpr int kYeeT = 32;
+__global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
+  constexpr int T = kYeeT, WE = T + 3, WB = T + 2, WJ = T + 1;
+  __shared__ float sE[3][WE * WE];
+  __shared__ float sB[3][WB * WB];
+  __shared__ float sJ[3][WJ * WJ];
+  const GridDesc& g = p.g;
+  const int i0 = blockIdx.x * T, j0 = blockIdx.y * T;
+  const int tw = min(T, g.nx - i0), th = min(T, g.ny - j0);
+  const long pl = g.plane;
+
+  for (int k = threadIdx.x; k < WE * WE; k += kBlock) {
+    const int gi = i0 + k % WE - 1, gj = j0 + k / WE - 1;
+    const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
+    const long a = in ? g.at(gi, gj) : 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) sE[c][k] = in ? __ldg(p.E0 + c * pl + a) : 0.f;
+  }
+  for (int k = threadIdx.x; k < WB * WB; k += kBlock) {
+    const int gi = i0 + k % WB - 1, gj = j0 + k / WB - 1;
+    const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
+    const long a = in ? g.at(gi, gj) : 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) sB[c][k] = in ? __ldg(p.B0 + c * pl + a) : 0.f;
+  }
+  for (int k = threadIdx.x; k < WJ * WJ; k += kBlock) {
+    const int gi = i0 + k % WJ, gj = j0 + k / WJ;
+    const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
+    const long a = in ? g.at(gi, gj) : 0;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) sJ[c][k] = in ? __ldg(p.J + c * pl + a) : 0.f;
+  }
+  __syncthreads();
+
+  // FE(n) = 1/2 dx dy sum(E^2 + B^2) over this tile's interior cells
+  float fe = 0.f;
+  for (int k = threadIdx.x; k < T * T; k += kBlock) {
+    const int lx = k % T, ly = k / T;
+    if (lx < tw && ly < th) {
+      const int e = (ly + 1) * WE + lx + 1, b = (ly + 1) * WB + lx + 1;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) fe += sE[c][e] * sE[c][e] + sB[c][b] * sB[c][b];
+    }
+  }
+#define EI(lx, ly) (((ly) + 1) * WE + (lx) + 1)
+#define BI(lx, ly) (((ly) + 1) * WB + (lx) + 1)
+#define JI(lx, ly) ((ly) * WJ + (lx))
+  // B^{n+1/2} on [-1, T]^2
+  for (int k = threadIdx.x; k < WB * WB; k += kBlock) {
+    const int lx = k % WB - 1, ly = k / WB - 1;
+    const float ez = sE[2][EI(lx, ly)];
+    sB[0][k] -= p.hdy * (sE[2][EI(lx, ly + 1)] - ez);
+    sB[1][k] += p.hdx * (sE[2][EI(lx + 1, ly)] - ez);
+    sB[2][k] += p.hdy * (sE[0][EI(lx, ly + 1)] - sE[0][EI(lx, ly)]) - p.hdx * (sE[1][EI(lx + 1, ly)] - sE[1][EI(lx, ly)]);
+  }
+  __syncthreads();
+  // E^{n+1} on [0, T]^2
+  for (int k = threadIdx.x; k < WJ * WJ; k += kBlock) {
+    const int lx = k % WJ, ly = k / WJ;
+    const int e = EI(lx, ly), b = BI(lx, ly);
+    sE[0][e] += p.dtdy * (sB[2][b] - sB[2][BI(lx, ly - 1)]) - p.dt * sJ[0][k];
+    sE[1][e] -= p.dtdx * (sB[2][b] - sB[2][BI(lx - 1, ly)]) + p.dt * sJ[1][k];
+    sE[2][e] += p.dtdx * (sB[1][b] - sB[1][BI(lx - 1, ly)]) - p.dtdy * (sB[0][b] - sB[0][BI(lx, ly - 1)]) - p.dt * sJ[2][k];
+  }
+  __syncthreads();
+  // B^{n+1} on [0, T)^2 and the stores
+  for (int k = threadIdx.x; k < T * T; k += kBlock) {
+    const int lx = k % T, ly = k / T;
+    if (lx >= tw || ly >= th) continue;
+    const int e = EI(lx, ly), b = BI(lx, ly);
+    const float ez = sE[2][e];
+    const float bx = sB[0][b] - p.hdy * (sE[2][EI(lx, ly + 1)] - ez);
+    const float by = sB[1][b] + p.hdx * (sE[2][EI(lx + 1, ly)] - ez);
+    const float bz = sB[2][b] + p.hdy * (sE[0][EI(lx, ly + 1)] - sE[0][e]) - p.hdx * (sE[1][EI(lx + 1, ly)] - sE[1][e]);
+    const float vals[6] = {sE[0][e], sE[1][e], ez, bx, by, bz};
+    const int gi = i0 + lx, gj = j0 + ly;
+    int xs[3], ys[3], nxs = 1, nys = 1;
+    xs[0] = gi; ys[0] = gj;
+    if (p.bcx == ZPIC_BC_PERIODIC) {
+      if (gi <= 1) xs[nxs++] = gi + g.nx;
+      if (gi == g.nx - 1) xs[nxs++] = -1;
+    }
+    if (p.bcy == ZPIC_BC_PERIODIC) {
+      if (gj <= 1) ys[nys++] = gj + g.ny;
+      if (gj == g.ny - 1) ys[nys++] = -1;
+    }
+    for (int a = 0; a < nys; ++a)
+      for (int c2 = 0; c2 < nxs; ++c2) {
+        const long o = g.at(xs[c2], ys[a]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          p.E1[c * pl + o] = vals[c];
+          p.B1[c * pl + o] = vals[3 + c];
+        }
+      }
+  }
+#undef EI
+#undef BI
+#undef JI
+  block_add_double((double)fe * p.fe_scale, p.fe_slots + ((blockIdx.y * gridDim.x + blockIdx.x) & (kEnergySlots - 1)));
+}
+
+// =============================================================================================
+// Epilogue (1 CTA): reduce the energy slots of the step just taken, reset per-step counters.
+__global__ void k_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4,
+                           int* movers_count, int* spill_in_count, int* spill_out_count, int* stats) {
+  __shared__ double red[kBlock];
+  for (int q = 0; q <= nspecies; ++q) {
+    double* slots = q == 0 ? fe_slots : ke_slots + (q - 1) * kEnergySlots;
+    double v = 0.0;
+    for (int k = threadIdx.x; k < kEnergySlots; k += blockDim.x) { v += slots[k]; slots[k] = 0.0; }
+    red[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) energy[q] = q == 0 ? red[0] : red[0] * ke_scale4[q - 1];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    stats[0] = *movers_count;
+    *movers_count = 0;
+    *spill_in_count = 0;
+    stats[1] = *spill_out_count;
+  }
+}
+
+// =============================================================================================
+// K0: lattice injection with the counter-based generator (synth/generate.py
+// documents the same definition for the host side).  One CTA per tile; the filled cells are the
+// columns [c_lo, c_hi) of the tile; particle p of the tile goes to cell p % ncell (cell-strided,
+// so consecutive threads deposit into different cells) and sub-lattice point p / ncell.
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double uniform01(uint64_t key, uint64_t id, int j) {
+  const uint64_t r = mix64(key ^ mix64(id * 8ull + (uint64_t)j));
+  return __dmul_rn(__dadd_rn((double)(r >> 11), 0.5), 1.1102230246251565e-16);  // 2^-53
+}
+__device__ __forceinline__ float thermal(uint64_t key, uint64_t id, int k, double ufl, double uth) {
+  if (uth == 0.0) return (float)ufl;
+  const double u1 = uniform01(key, id, 2 * k), u2 = uniform01(key, id, 2 * k + 1);
+  const double nrm = __dmul_rn(sqrt(__dmul_rn(-2.0, log(u1))), cos(__dmul_rn(6.283185307179586, u2)));
+  return (float)__dadd_rn(ufl, __dmul_rn(uth, nrm));
+}
+
+__global__ void __launch_bounds__(kBlock) k_inject(InjectParams q) {
+  const int t = blockIdx.x;
+  const int tx = t % q.ntx, ty = t / q.ntx;
+  const int i0 = tx * q.T, j0 = ty * q.T;
+  const int c_lo = max(i0, q.col_lo), c_hi = min(min(i0 + q.T, q.nx_global), q.col_hi);
+  const int rows = min(q.T, q.ny - j0);
+  const int wc = max(0, c_hi - c_lo);
+  const int ncell = wc * rows;
+  const int ppc = q.px * q.py;
+  const int n = ncell * ppc;
+  const long base = (long)t * q.ps.cap;
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    const int ck = p % ncell, sub = p / ncell;
+    const int ix = c_lo + ck % wc, iy = j0 + ck / wc;
+    const int k = sub % q.px, l = sub / q.px;
+    const uint64_t id = (((uint64_t)(iy + q.y0) * q.nx_global + ix) * q.py + l) * q.px + k;
+    const long o = base + p;
+    q.ps.cell[o] = pack_cell(ix, iy);
+    q.ps.x[o] = (float)(((double)k + 0.5) / q.px);
+    q.ps.y[o] = (float)(((double)l + 0.5) / q.py);
+    q.ps.ux[o] = thermal(q.key, id, 0, q.ufl[0], q.uth[0]);
+    q.ps.uy[o] = thermal(q.key, id, 1, q.ufl[1], q.uth[1]);
+    q.ps.uz[o] = thermal(q.key, id, 2, q.ufl[2], q.uth[2]);
+    if (q.ps.id) q.ps.id[o] = (uint32_t)id;
+  }
+  if (threadIdx.x == 0) q.ps.cnt[t] = n;
+}
+
+// Bin host-uploaded particles (global iy -> slab-local) into tiles.
+__global__ void k_bin(PStore ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
+                      const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err) {
+  for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const int cx = ix[k], cy = iy[k] - y0;
+    const int t = (cy / T) * ntx + cx / T;
+    const int slot = atomicAdd(ps.cnt + t, 1);
+    if (slot >= ps.cap) { atomicOr(err, ERR_OVERFLOW); continue; }
+    const long o = (long)t * ps.cap + slot;
+    ps.cell[o] = pack_cell(cx, cy);
+    ps.x[o] = x[k]; ps.y[o] = y[k]; ps.ux[o] = ux[k]; ps.uy[o] = uy[k]; ps.uz[o] = uz[k];
+    if (ps.id) ps.id[o] = id ? id[k] : (uint32_t)k;
+  }
+}
+
+// Copy every tile segment of one species to a contiguous buffer (prefix[t] = output offset);
+// global ix, iy on the way out.
+__global__ void k_export(PStore ps, const int64_t* prefix, int y0, int32_t* ix, int32_t* iy, float* x, float* y,
+                         float* ux, float* uy, float* uz, uint32_t* id) {
+  const int t = blockIdx.x;
+  const int n = ps.cnt[t];
+  const long src = (long)t * ps.cap;
+  const int64_t dst = prefix[t];
+  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+    const int c = ps.cell[src + k];
+    ix[dst + k] = cell_ix(c);
+    iy[dst + k] = cell_iy(c) + y0;
+    x[dst + k] = ps.x[src + k]; y[dst + k] = ps.y[src + k];
+    ux[dst + k] = ps.ux[src + k]; uy[dst + k] = ps.uy[src + k]; uz[dst + k] = ps.uz[src + k];
+    if (id) id[dst + k] = ps.id ? ps.id[src + k] : 0u;
+  }
+}
+
+// ---- host-side launchers --------------------------------------------------------------------
+void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st) {
+  switch (p.T) {
+    case 8: k_push_tiles<8><<<ntiles, kBlock, 0, st>>>(p); break;
+    case 16: k_push_tiles<16><<<ntiles, kBlock, 0, st>>>(p); break;
+    case 32: k_push_tiles<32><<<ntiles, kBlock, 0, st>>>(p); break;
+  }
+}
+void launch_insert(const PushParams& p, int grid, cudaStream_t st) { k_insert<<<grid, kBlock, 0, st>>>(p); }
+void launch_loose(const PushParams& p, int grid, cudaStream_t st) { k_push_loose<<<grid, kBlock, 0, st>>>(p); }
+void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st) {
+  dim3 grid((g.nx + 3 + kBlock - 1) / kBlock, g.ny + 3);
+  switch (T) {
+    case 8: k_assemble_j<8><<<grid, kBlock, 0, st>>>(J, Jt, g, ntx, nty); break;
+    case 16: k_assemble_j<16><<<grid, kBlock, 0, st>>>(J, Jt, g, ntx, nty); break;
+    case 32: k_assemble_j<32><<<grid, kBlock, 0, st>>>(J, Jt, g, ntx, nty); break;
+  }
+}
+void launch_guard_x(float* F, const GridDesc& g, int mode, int keep, cudaStream_t st) {
+  const int n = 3 * (g.ny + 3);
+  k_guard_x<<<(n + 255) / 256, 256, 0, st>>>(F, g, mode, keep);
+}
+void launch_guard_y(float* F, const GridDesc& g, int mode, int keep, cudaStream_t st) {
+  const int n = 3 * (g.nx + 3);
+  k_guard_y<<<(n + 255) / 256, 256, 0, st>>>(F, g, mode, keep);
+}
+void launch_yee(const YeeParams& p, cudaStream_t st) {
+  dim3 grid((p.g.nx + kYeeT - 1) / kYeeT, (p.g.ny + kYeeT - 1) / kYeeT);
+  k_yee<<<grid, kBlock, 0, st>>>(p);
+}
+void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4,
+                     int* mc, int* sic, int* soc, int* stats, cudaStream_t st) {
+  k_epilogue<<<1, kBlock, 0, st>>>(ke_slots, fe_slots, energy, nspecies, ke_scale4, mc, sic, soc, stats);
+}
+void launch_inject(const InjectParams& q, int ntiles, cudaStream_t st) { k_inject<<<ntiles, kBlock, 0, st>>>(q); }
+void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
+                const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err,
+                cudaStream_t st) {
+  const int grid = (int)std::min<long>((n + kBlock - 1) / kBlock, 148L * 32);
+  if (grid > 0) k_bin<<<grid, kBlock, 0, st>>>(ps, T, ntx, y0, n, ix, iy, x, y, ux, uy, uz, id, err);
+}
+void launch_export(const PStore& ps, int ntiles, const int64_t* prefix, int y0, int32_t* ix, int32_t* iy, float* x,
+                   float* y, float* ux, float* uy, float* uz, uint32_t* id, cudaStream_t st) {
+  k_export<<<ntiles, kBlock, 0, st>>>(ps, prefix, y0, ix, iy, x, y, ux, uy, uz, id);
+}
+
+}  // namespace zpic

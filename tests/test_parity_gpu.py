@@ -1,0 +1,162 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the same seeded
+inputs (BASELINE.json north_star tolerances).  Needs a B200."""
+import numpy as np
+import pytest
+
+import synth
+from oracle.sim import from_config
+from parity_util import (CELL_FRAC, CONT_TOL, ENERGY_TOL, FIELD_TOL, MOM_TOL, POS_TOL, compare_particles,
+                         continuity_residual, energy_agreement, oracle_particles, rel_l2, rho_nodes)
+
+pytestmark = pytest.mark.gpu
+
+
+def _z():
+    import paper_2106_12485_b200 as z
+    return z
+
+
+def gpu_from_particles(cfg, parts, tile=16):
+    sim = _z().Simulation(cfg, inject=False, track_ids=True, tile=tile)
+    for s, p in enumerate(parts):
+        sim.set_particles(s, p)
+    return sim
+
+
+def _parity_run(cfg, steps, tile=16, check_every_step=True):
+    parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
+    g = gpu_from_particles(cfg, parts, tile)
+    o = from_config(cfg, particles=parts)
+    nx, ny, dx, dy, dt = cfg["nx"], cfg["ny"], cfg["dx"], cfg["dy"], cfg["dt"]
+    q = [o.species[s]["q"] for s in range(len(parts))]
+    fe_g, fe_o, ke_g, ke_o = [], [], [], []
+    prev = [g.particles(s, True) for s in range(len(parts))]
+    prev_n = -1
+    report = {}
+    for n in range(steps):
+        g.step(1)
+        o.step()
+        it, fe, ke = g.energy()
+        assert it == n
+        fe_g.append(fe); ke_g.append(ke)
+        fe_o.append(o.fe[-1]); ke_o.append(o.ke[-1])
+        if check_every_step or n in (0, 9, steps - 1):
+            cur = [g.particles(s, True) for s in range(len(parts))]
+            if n < 10 and prev_n == n - 1:
+                rho0 = sum(rho_nodes(nx, ny, q[s], prev[s]) for s in range(len(parts)))
+                rho1 = sum(rho_nodes(nx, ny, q[s], cur[s]) for s in range(len(parts)))
+                r = continuity_residual(nx, ny, dx, dy, dt, rho0, rho1, g.fields(3))
+                report.setdefault("continuity", []).append(r)
+                assert r <= CONT_TOL, (n, r)
+            if n == 0:
+                for s in range(len(parts)):
+                    c = compare_particles(cur[s], oracle_particles(o, s), nx, ny)
+                    report["step1_s%d" % s] = c
+                    assert c["pos_max"] <= POS_TOL, c
+                    assert c["mom_max"] <= MOM_TOL, c
+                    assert c["cell_exact_frac"] >= CELL_FRAC and c["cell_bad"] == 0, c
+            if n == 9:
+                eE, eB = rel_l2(g.fields(0), o.fields(0)), rel_l2(g.fields(1), o.fields(1))
+                report["fields10"] = (eE, eB)
+                assert eE <= FIELD_TOL and eB <= FIELD_TOL, (eE, eB)
+                for s in range(len(parts)):
+                    c = compare_particles(cur[s], oracle_particles(o, s), nx, ny)
+                    assert c["cell_exact_frac"] >= CELL_FRAC, c
+            prev, prev_n = cur, n
+    assert energy_agreement(fe_g, fe_o) <= ENERGY_TOL
+    for s in range(len(parts)):
+        assert energy_agreement([k[s] for k in ke_g], [k[s] for k in ke_o]) <= ENERGY_TOL
+    assert energy_agreement([f + sum(k) for f, k in zip(fe_g, ke_g)], [f + sum(k) for f, k in zip(fe_o, ke_o)]) <= ENERGY_TOL
+    cnt = g.counters()
+    assert cnt["particles"] == sum(len(p["ix"]) for p in parts)
+    g.close()
+    return report
+
+
+def test_c1_full_run():
+    """BASELINE.json configs[0] at full size: 1-step particles, 10-step fields, 100-step energies."""
+    cfg = synth.config("C1")
+    rep = _parity_run(cfg, cfg["steps"], check_every_step=False)
+    print(rep)
+
+
+def test_c2_weibel_reduced():
+    """configs[1] physics (two counter-streaming species) on a 64x64 grid, 12 steps."""
+    cfg = synth.config("C2", nx=64, ny=64)
+    _parity_run(cfg, 12)
+
+
+@pytest.mark.parametrize("tile", [8, 16, 32])
+def test_ragged_grid_tiles(tile):
+    """Grid sizes that are not multiples of the tile (partial tiles on both axes)."""
+    cfg = synth.config("C1", nx=50, ny=37)
+    cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)   # more crossings
+    _parity_run(cfg, 10, tile=tile)
+
+
+def test_device_injection_matches_generator():
+    """K0 (device counter-based injector) reproduces synth's particles: positions bit-exact,
+    momenta within 1 fp32 ulp (fp64 libm vs CUDA fp64 math)."""
+    for name, over in (("C1", {}), ("C2", dict(nx=48, ny=40))):
+        cfg = synth.config(name, **over)
+        sim = _z().Simulation(cfg, inject=True, track_ids=True)
+        for s in range(len(cfg["species"])):
+            g = sim.particles(s, True)
+            h = synth.species_particles(cfg, s)
+            o = np.argsort(g["id"])
+            g = {k: v[o] for k, v in g.items()}
+            assert np.array_equal(g["id"], h["id"])
+            for k in ("ix", "iy", "x", "y"):
+                assert np.array_equal(g[k], h[k]), k
+            for k in ("ux", "uy", "uz"):
+                assert np.all(np.abs(g[k] - h[k]) <= np.spacing(np.abs(h[k]))), k
+        sim.close()
+
+
+def test_slab_injection_counts():
+    cfg = synth.config("C3", nx=64, ny=32)
+    cfg["species"][0].update(x0=0.0, x1=3.2)
+    cfg["species"][1].update(x0=3.2, x1=6.4)
+    cfg["bc"] = (0, 0)
+    sim = _z().Simulation(cfg, inject=True, track_ids=True)
+    for s in range(2):
+        g = sim.particles(s, True)
+        h = synth.species_particles(cfg, s)
+        assert len(g["ix"]) == len(h["ix"]) == 32 * 32 * 8
+        assert np.array_equal(np.sort(g["id"]), np.sort(h["id"]))
+    sim.close()
+
+
+def test_empty_and_vacuum():
+    """No particles: fields stay exactly zero; a species with zero particles is allowed."""
+    cfg = synth.config("C1", nx=32, ny=32)
+    sim = _z().Simulation(cfg, inject=False, track_ids=True)
+    sim.set_particles(0, {k: np.zeros(0, dt) for k, dt in
+                          (("ix", np.int32), ("iy", np.int32), ("x", np.float32), ("y", np.float32),
+                           ("ux", np.float32), ("uy", np.float32), ("uz", np.float32))})
+    sim.step(5)
+    for w in range(3):
+        assert not np.any(sim.fields(w))
+    assert sim.energy()[0] == 4
+    sim.close()
+
+
+def test_vacuum_wave_matches_oracle():
+    """Pure field solve (K5 + guards): a random initial field, no particles, 50 steps."""
+    cfg = synth.config("C1", nx=40, ny=24)
+    rng = np.random.default_rng(3)
+    E = rng.normal(size=(3, 24, 40)).astype(np.float32)
+    B = rng.normal(size=(3, 24, 40)).astype(np.float32)
+    empty = {k: np.zeros(0, dt) for k, dt in (("ix", np.int32), ("iy", np.int32), ("x", np.float32),
+                                               ("y", np.float32), ("ux", np.float32), ("uy", np.float32),
+                                               ("uz", np.float32), ("id", np.uint32))}
+    g = gpu_from_particles(cfg, [empty])
+    g.set_fields(0, E)
+    g.set_fields(1, B)
+    o = from_config(cfg, particles=[empty], E=E, B=B)
+    for _ in range(50):
+        g.step(1)
+        o.step()
+    assert rel_l2(g.fields(0), o.fields(0)) < 1e-5
+    assert rel_l2(g.fields(1), o.fields(1)) < 1e-5
+    g.close()
