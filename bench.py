@@ -1,0 +1,277 @@
+"""Benchmark of the B200 EM-PIC hot path (BASELINE.json metric: particle pushes/s, % of the HBM
+roofline).  Contract: `python bench.py --gpus N --steps K --warmup W` prints ONE JSON line on
+rank 0.  Workload (N=1): BASELINE.json configs[4] "C5" (8192^2 cells, 4x4 ppc, 1.07e9
+particles, uth 0.1, periodic), the configuration the metric and the roofline target are quoted
+on.  `--impl reference` times the fp64 oracle (the reference arm of this tier) on the host.
+
+Timing: W untimed warm-up steps, then K steps bracketed by barrier + cuda synchronize, CUDA
+events on the library's stream (= torch's current stream), max over ranks.  The particle
+store (30 GB) is far larger than the 126 MB L2, so no L2 flush is needed between steps.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle pushes/s (push+deposit)"
+UNIT = "particles/s"
+# algorithmic bytes of the fused push+deposit kernel (K1) per launch:
+# 56 B per particle (read + write ix, iy, x, y, ux, uy, uz) + 36 B per cell (E, B read, J write).
+K1_BYTES_PER_PARTICLE = 56
+K1_BYTES_PER_CELL = 36
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + self.Q,
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                      stderr=subprocess.DEVNULL)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            if len(r) < 9:
+                continue
+            for k, nm in enumerate(names):
+                if "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def cpu_baseline(args):
+    """The oracle, as it stands, on a bounded sample of the same workload: the C5 physics on a
+    1024 x 1024-cell periodic patch (16 ppc, 16.8 M particles), `steps` steps, one host core."""
+    import synth
+    from oracle.sim import from_config
+    cfg = synth.config(args.config, nx=args.cpu_cells, ny=args.cpu_cells)
+    sim = from_config(cfg)
+    n = sum(len(s["ix"]) for s in sim.species)
+    t0 = time.perf_counter()
+    for _ in range(args.cpu_steps):
+        sim.step()
+    dt = time.perf_counter() - t0
+    return {"value": n * args.cpu_steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": "%s physics on a %dx%d-cell periodic patch (%d particles), %d steps, fp64 serial oracle"
+                      % (args.config, args.cpu_cells, args.cpu_cells, n, args.cpu_steps),
+            "seconds": dt}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the oracle (the reference arm of this tier) on the box's host cores."""
+    if rank != 0:
+        return
+    import synth
+    from oracle.sim import from_config
+    cfg = synth.config(args.config, nx=args.cpu_cells, ny=args.cpu_cells)
+    sim = from_config(cfg)
+    n = sum(len(s["ix"]) for s in sim.species)
+    for _ in range(args.warmup):
+        sim.step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        sim.step()
+    dt = time.perf_counter() - t0
+    v = n * args.steps / dt
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "%s physics, %dx%d-cell sample" % (args.config, args.cpu_cells, args.cpu_cells),
+                       "particles": n},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": "%dx%d-cell periodic patch of %s, %d particles, %d steps"
+                                       % (args.cpu_cells, args.cpu_cells, args.config, n, args.steps)},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def e2e_run(args, cfg, torch, z):
+    """End to end through the public API with HOST buffers: upload the initial particles from
+    pinned host memory (zpic_set_particles), K steps with the energies read back every step,
+    and the final E, B fields read back; all inside the timed region."""
+    import numpy as np
+    src = z.Simulation(cfg, inject=True)
+    host = []
+    for s in range(len(cfg["species"])):
+        p = src.particles(s)
+        pinned = {}
+        for k, v in p.items():
+            t = torch.empty(v.shape, dtype={np.int32: torch.int32, np.float32: torch.float32}[v.dtype.type],
+                            pin_memory=True)
+            t.numpy()[...] = v
+            pinned[k] = t
+        host.append(pinned)
+    src.close()
+    del p
+    sim = z.Simulation(cfg, inject=False)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    h2d = 0
+    for s, hp in enumerate(host):
+        sim.set_particles(s, {k: v.numpy() for k, v in hp.items()})
+        h2d += sum(v.numel() * v.element_size() for v in hp.values())
+    d2h = 0
+    for _ in range(args.steps):
+        sim.step(1)
+        sim.energy()
+        d2h += 8 * (1 + len(cfg["species"]))
+    for w in (0, 1):
+        f = sim.fields(w)
+        d2h += f.nbytes
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    n = sum(v["ix"].numel() for v in host)
+    sim.close()
+    return {"value": n * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
+            "d2h_bytes_per_step": int(d2h / args.steps), "seconds": dt,
+            "note": "initial particles uploaded from pinned host memory, energies read every step, E and B read at the end"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--tile", type=int, default=16)
+    ap.add_argument("--cpu-cells", type=int, default=1024)
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--nx", type=int, default=0, help="override the grid (profiling runs only)")
+    ap.add_argument("--ny", type=int, default=0)
+    args = ap.parse_args()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import synth
+    import paper_2106_12485_b200 as z
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = synth.config(args.config)
+    if args.nx:
+        cfg["nx"], cfg["ny"] = args.nx, args.ny or args.nx
+        cfg["name"] += "-resized-%dx%d" % (cfg["nx"], cfg["ny"])
+    sim = z.Simulation(cfg, inject=True, profile=True, tile=args.tile)
+    n_particles = sim.counters()["particles"]
+    n_cells = cfg["nx"] * cfg["ny"]
+    sim.step(args.warmup)
+    sim.sync()
+    sim.kernel_times()                 # reset the per-kernel accumulators
+    launches0 = sim.counters()["launches"]
+    clocks = ClockSampler(local)
+    clocks.start()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(sim.torch_stream)
+    sim.step(args.steps)
+    e1.record(sim.torch_stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    sim.sync()
+    kt = sim.kernel_times()
+    cnt = sim.counters()
+    launches = cnt["launches"] - launches0
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        npt = torch.tensor([n_particles], device="cuda", dtype=torch.int64)
+        torch.distributed.all_reduce(npt)
+        n_particles = int(npt.item())
+    sim.close()
+
+    k1_ms, k1_n = kt["k_push_tiles"]
+    k1_avg_s = k1_ms / max(k1_n, 1) * 1e-3
+    k1_bytes = K1_BYTES_PER_PARTICLE * cnt["particles"] + K1_BYTES_PER_CELL * n_cells // max(world, 1)
+    peak, peak_kind = measured_peaks()
+    achieved = k1_bytes / k1_avg_s / 1e9
+    value = n_particles * args.steps / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "%s (BASELINE.json configs[4]): %dx%d cells, 4x4 ppc, %d particles, uth 0.1, periodic"
+                               % (cfg["name"], cfg["nx"], cfg["ny"], n_particles),
+                   "tile": args.tile, "l2": "inputs larger than L2 (particle store ~30 GB)",
+                   "parallelism": "y-slabs x%d" % world},
+        "cell_updates_per_s": n_cells * args.steps / (ms * 1e-3),
+        "k1_pushes_per_s": cnt["particles"] / k1_avg_s,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None, "kernel": "k_push_tiles", "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg_s * 1e3},
+        "kernel_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in kt.items() if v[1]},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(args)
+    if rank == 0 and world == 1 and not args.no_e2e:
+        line["e2e"] = e2e_run(args, cfg, torch, z)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -28,6 +28,8 @@ void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t*
                 cudaStream_t st);
 void launch_export(const PStore& ps, int ntiles, const int64_t* prefix, int y0, int32_t* ix, int32_t* iy, float* x,
                    float* y, float* ux, float* uy, float* uz, uint32_t* id, cudaStream_t st);
+void launch_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
+                  const float* y, int* counts, int* err, cudaStream_t st);
 }  // namespace zpic
 
 using namespace zpic;
@@ -97,6 +99,17 @@ void alloc_store(zpic_ctx* c, int s, int cap) {
   ps.uz = alloc_n<float>(c, n);
   ps.id = c->opt.track_ids ? alloc_n<uint32_t>(c, n) : nullptr;
   ps.cnt = alloc_n<int32_t>(c, c->ntiles);
+}
+
+// The tile current is accumulated as exact fixed point whose low halves must stay below 2^31:
+// a node receives at most 3 contributions per particle of the tile (one per sub-segment), each
+// below 2^15, so all species together may hold at most 21845 particles per tile.
+void check_tile_capacity(zpic_ctx* c) {
+  long total = 0;
+  for (int s = 0; s < c->nspecies; ++s) total += c->ps[s].cap;
+  if (total > 21845)
+    throw Fail{ZPIC_E_INVALID, "tile capacity " + std::to_string(total) +
+                                   " > 21845 particles (fixed-point current range): use a smaller tile"};
 }
 
 void free_store(zpic_ctx* c, int s) {
@@ -313,6 +326,7 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       const int cap = std::max(32, round_up((int)std::ceil(maxcount * c->opt.capacity_slack), 32));
       if ((double)cap * c->ntiles > 2.0e9) throw Fail{ZPIC_E_INVALID, "particle store exceeds 2^31 slots"};
       alloc_store(c, s, cap);
+      check_tile_capacity(c);
       if (col_hi > col_lo) {
         InjectParams q{};
         q.ps = c->ps[s];
@@ -349,31 +363,18 @@ zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t*
     c->last_error = "set_particles: bad arguments"; return ZPIC_E_INVALID;
   }
   try {
-    std::vector<int> counts(c->ntiles, 0);
-    for (int64_t k = 0; k < n; ++k) {
-      const int cx = ix[k], cy = iy[k] - c->y0;
-      if (cx < 0 || cx >= c->g.nx || cy < 0 || cy >= c->g.ny || !(x[k] >= 0.f && x[k] < 1.f) || !(y[k] >= 0.f && y[k] < 1.f))
-        throw Fail{ZPIC_E_INVALID, "set_particles: particle " + std::to_string(k) + " outside the local slab or offset not in [0,1)"};
-      counts[(cy / c->T) * c->ntx + cx / c->T]++;
-    }
-    int maxc = 0;
-    for (int v : counts) maxc = std::max(maxc, v);
-    const int ppc = c->species[s].ppc[0] * c->species[s].ppc[1];
-    const int cap = std::max({32, round_up((int)std::ceil(maxc * c->opt.capacity_slack), 32),
-                              round_up((int)std::ceil(c->T * c->T * ppc * c->opt.capacity_slack), 32)});
-    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
-    free_store(c, s);
-    alloc_store(c, s, cap);
+    // upload, then validate + count per tile on the device
+    char* tmp = (char*)dev_alloc(c, (size_t)std::max<int64_t>(n, 1) * (7 * 4 + 4));
+    int32_t* dix = (int32_t*)tmp;
+    int32_t* diy = dix + n;
+    float* dx_ = (float*)(diy + n);
+    float* dy_ = dx_ + n;
+    float* dux = dy_ + n;
+    float* duy = dux + n;
+    float* duz = duy + n;
+    uint32_t* did = (uint32_t*)(duz + n);
+    int* dcounts = alloc_n<int>(c, c->ntiles + 1);
     if (n > 0) {
-      char* tmp = (char*)dev_alloc(c, (size_t)n * (7 * 4 + 4));
-      int32_t* dix = (int32_t*)tmp;
-      int32_t* diy = dix + n;
-      float* dx_ = (float*)(diy + n);
-      float* dy_ = dx_ + n;
-      float* dux = dy_ + n;
-      float* duy = dux + n;
-      float* duz = duy + n;
-      uint32_t* did = (uint32_t*)(duz + n);
       CUDA_OR_THROW(cudaMemcpyAsync(dix, ix, n * 4, cudaMemcpyHostToDevice, c->stream));
       CUDA_OR_THROW(cudaMemcpyAsync(diy, iy, n * 4, cudaMemcpyHostToDevice, c->stream));
       CUDA_OR_THROW(cudaMemcpyAsync(dx_, x, n * 4, cudaMemcpyHostToDevice, c->stream));
@@ -382,12 +383,33 @@ zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t*
       CUDA_OR_THROW(cudaMemcpyAsync(duy, uy, n * 4, cudaMemcpyHostToDevice, c->stream));
       CUDA_OR_THROW(cudaMemcpyAsync(duz, uz, n * 4, cudaMemcpyHostToDevice, c->stream));
       if (id) CUDA_OR_THROW(cudaMemcpyAsync(did, id, n * 4, cudaMemcpyHostToDevice, c->stream));
+      launch_count(c->T, c->ntx, c->g.nx, c->g.ny, c->y0, (long)n, dix, diy, dx_, dy_, dcounts, dcounts + c->ntiles,
+                   c->stream);
+      CUDA_OR_THROW(cudaGetLastError());
+    }
+    std::vector<int> counts(c->ntiles + 1, 0);
+    CUDA_OR_THROW(cudaMemcpyAsync(counts.data(), dcounts, (c->ntiles + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+    dev_free(c, dcounts);
+    if (counts[c->ntiles]) {
+      dev_free(c, tmp);
+      throw Fail{ZPIC_E_INVALID, "set_particles: a particle is outside the local slab or its offset is not in [0,1)"};
+    }
+    int maxc = 0;
+    for (int t = 0; t < c->ntiles; ++t) maxc = std::max(maxc, counts[t]);
+    const int ppc = c->species[s].ppc[0] * c->species[s].ppc[1];
+    const int cap = std::max({32, round_up((int)std::ceil(maxc * c->opt.capacity_slack), 32),
+                              round_up((int)std::ceil(c->T * c->T * ppc * c->opt.capacity_slack), 32)});
+    free_store(c, s);
+    alloc_store(c, s, cap);
+    check_tile_capacity(c);
+    if (n > 0) {
       launch_bin(c->ps[s], c->T, c->ntx, c->y0, (long)n, dix, diy, dx_, dy_, dux, duy, duz, id ? did : nullptr, c->err,
                  c->stream);
       CUDA_OR_THROW(cudaGetLastError());
-      CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
-      dev_free(c, tmp);
     }
+    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+    dev_free(c, tmp);
     // movers / loose lists sized for the new population
     int64_t total = 0;
     for (int q = 0; q < c->nspecies; ++q) {
@@ -460,6 +482,7 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
     }
     c->cur ^= 1;
     c->steps += 1;
+    c->launches += 8;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { c->last_error = std::string("launch: ") + cudaGetErrorString(e); return ZPIC_E_CUDA; }
@@ -602,8 +625,8 @@ zpic_status zpic_counters(zpic_ctx* c, int64_t* out, int32_t n) {
   }
   int nl = 0;
   cudaMemcpy(&nl, c->spill[c->steps & 1].count, 4, cudaMemcpyDeviceToHost);
-  const int64_t v[6] = {total + nl, stats[0], maxfill, c->repacks, c->steps, c->ntiles};
-  for (int k = 0; k < n && k < 6; ++k) out[k] = v[k];
+  const int64_t v[7] = {total + nl, stats[0], maxfill, c->repacks, c->steps, c->ntiles, c->launches};
+  for (int k = 0; k < n && k < 7; ++k) out[k] = v[k];
   return ZPIC_OK;
 }
 

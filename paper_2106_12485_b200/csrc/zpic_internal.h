@@ -128,6 +128,7 @@ struct zpic_ctx {
   int cur;         // index of the current E/B buffer
   int64_t steps;
   int64_t repacks;
+  int64_t launches;  // kernels enqueued by zpic_step so far
   std::vector<void*> allocations;
   std::string last_error;
   // profiling

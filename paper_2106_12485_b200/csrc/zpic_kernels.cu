@@ -11,202 +11,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
-#include "zpic_kernels.cuh"
+#include "zpic_device.cuh"
 
 namespace zpic {
-
-__device__ __forceinline__ unsigned lanemask_lt() {
-  unsigned m;
-  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
-  return m;
-}
-
-// warp-aggregated slot reservation on a global counter
-__device__ __forceinline__ int warp_reserve(int* counter, bool want) {
-  const unsigned m = __ballot_sync(0xffffffffu, want);
-  if (!m) return -1;
-  const int lane = threadIdx.x & 31;
-  const int leader = __ffs(m) - 1;
-  int base = 0;
-  if (lane == leader) base = atomicAdd(counter, __popc(m));
-  base = __shfl_sync(0xffffffffu, base, leader);
-  return want ? base + __popc(m & lanemask_lt()) : -1;
-}
-
-__device__ __forceinline__ void block_add_double(double v, double* slot) {
-  __shared__ double s_red[kBlock / 32];
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  const int w = threadIdx.x >> 5;
-  if ((threadIdx.x & 31) == 0) s_red[w] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int k = 0; k < kBlock / 32; ++k) t += s_red[k];
-    if (t != 0.0) atomicAdd(slot, t);
-  }
-  __syncthreads();
-}
-
-__device__ __forceinline__ int pack_cell(int ix, int iy) { return (ix & 0xffff) | (iy << 16); }
-__device__ __forceinline__ int cell_ix(int c) { return c & 0xffff; }
-__device__ __forceinline__ int cell_iy(int c) { return c >> 16; }
-
-// Apply the particle boundary conditions to a new cell (a5).  Returns false if the particle
-// leaves the domain through an open / window edge (removed).
-__device__ __forceinline__ bool domain_bc(int& ix, int& iy, const GridDesc& g, int bcx, int bcy) {
-  if (ix < 0 || ix >= g.nx) {
-    if (bcx != ZPIC_BC_PERIODIC) return false;
-    ix += ix < 0 ? g.nx : -g.nx;
-  }
-  if (iy < 0 || iy >= g.ny) {
-    if (bcy != ZPIC_BC_PERIODIC) return false;
-    iy += iy < 0 ? g.ny : -g.ny;
-  }
-  return true;
-}
-
-__device__ __forceinline__ void list_put(const PList& L, int k, int cell, float x, float y, float ux, float uy, float uz,
-                                         uint32_t id, int s) {
-  L.cell[k] = cell; L.x[k] = x; L.y[k] = y; L.ux[k] = ux; L.uy[k] = uy; L.uz[k] = uz;
-  if (L.id) L.id[k] = id;
-  L.species[k] = s;
-}
-
-// Insert one particle into its tile's slack, else into the loose list.
-__device__ __forceinline__ void insert_particle(const PushParams& p, int s, int ix, int iy, float x, float y, float ux,
-                                                float uy, float uz, uint32_t id) {
-  const int t = (iy / p.T) * p.ntx + (ix / p.T);
-  const PStore& ps = p.ps[s];
-  const int slot = atomicAdd(ps.cnt + t, 1);
-  const int cell = pack_cell(ix, iy);
-  if (slot < ps.cap) {
-    const long k = (long)t * ps.cap + slot;
-    ps.cell[k] = cell; ps.x[k] = x; ps.y[k] = y; ps.ux[k] = ux; ps.uy[k] = uy; ps.uz[k] = uz;
-    if (ps.id) ps.id[k] = id;
-  } else {
-    atomicSub(ps.cnt + t, 1);
-    const int k = atomicAdd(p.spill_out.count, 1);
-    if (k < p.spill_out.cap) list_put(p.spill_out, k, cell, x, y, ux, uy, uz, id, s);
-    else atomicOr(p.err, ERR_OVERFLOW);
-  }
-}
-
-// =============================================================================================
-// K1: one CTA per tile.  Stage the tile's E, B (+1 guard cell each side) in shared memory, zero a
-// shared (T+3)^2 current block, push every particle of every species of the tile (one thread
-// per particle, chunks of kBlock), write the particles that stay back compacted in place, send
-// the others to the mover list, and finally store the current block to Jt (plain stores; K4
-// sums the overlapping blocks).
-template <int T>
-__global__ void __launch_bounds__(kBlock) k_push_tiles(PushParams p) {
-  constexpr int W = T + 2, WJ = T + 3;
-  __shared__ float2 s_eb1[W * W], s_eb2[W * W];
-  __shared__ float s_ez[W * W], s_bz[W * W];
-  __shared__ float s_j[3 * WJ * WJ];
-  __shared__ int s_wsum[2][kBlock / 32];
-
-  const int t = blockIdx.x;
-  const int tx = t % p.ntx, ty = t / p.ntx;
-  const int i0 = tx * T, j0 = ty * T;
-  const int tw = min(T, p.g.nx - i0), th = min(T, p.g.ny - j0);
-  const long pl = p.g.plane;
-
-  for (int k = threadIdx.x; k < W * W; k += kBlock) {
-    const int gi = i0 + k % W - 1, gj = j0 + k / W - 1;
-    float ex = 0.f, ey = 0.f, ez = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
-    if (gi <= p.g.nx + 1 && gj <= p.g.ny + 1) {
-      const long a = p.g.at(gi, gj);
-      ex = __ldg(p.E + a); ey = __ldg(p.E + pl + a); ez = __ldg(p.E + 2 * pl + a);
-      bx = __ldg(p.B + a); by = __ldg(p.B + pl + a); bz = __ldg(p.B + 2 * pl + a);
-    }
-    s_eb1[k] = make_float2(ex, by);
-    s_eb2[k] = make_float2(ey, bx);
-    s_ez[k] = ez;
-    s_bz[k] = bz;
-  }
-  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += kBlock) s_j[k] = 0.f;
-  __syncthreads();
-
-  const SmemFields F{s_eb1, s_eb2, s_ez, s_bz, W};
-  const SmemCurrent A{s_j, WJ};
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned ltmask = lanemask_lt();
-  int buf = 0;
-
-  for (int s = 0; s < p.nspecies; ++s) {
-    const PStore& ps = p.ps[s];
-    const SpeciesConst sc = p.sc[s];
-    const int n = ps.cnt[t];
-    const long base = (long)t * ps.cap;
-    int out = 0;
-    float ke = 0.f;
-    for (int c0 = 0; c0 < n; c0 += kBlock) {
-      const int i = c0 + threadIdx.x;
-      const bool valid = i < n;
-      int cell = 0;
-      float x = 0.f, y = 0.f, ux = 0.f, uy = 0.f, uz = 0.f;
-      uint32_t id = 0;
-      if (valid) {
-        const long k = base + i;
-        cell = __ldcs(ps.cell + k);
-        x = __ldcs(ps.x + k); y = __ldcs(ps.y + k);
-        ux = __ldcs(ps.ux + k); uy = __ldcs(ps.uy + k); uz = __ldcs(ps.uz + k);
-        if (ps.id) id = __ldcs(ps.id + k);
-      }
-      bool stay = false, move = false;
-      int ix = 0, iy = 0;
-      if (valid) {
-        ix = cell_ix(cell); iy = cell_iy(cell);
-        const int lx = ix - i0, ly = iy - j0;
-        float ex, ey, ez, bx, by, bz;
-        interpolate(F, lx, ly, x, y, ex, ey, ez, bx, by, bz);
-        ke += boris(ux, uy, uz, ex, ey, ez, bx, by, bz, sc.h);
-        const float rg = rsqrtf(1.0f + fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
-        const float dxp = ux * rg * p.dtdx, dyp = uy * rg * p.dtdy;
-        if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(p.err, ERR_MIGRATION);
-        int di, dj;
-        advance_deposit(A, lx, ly, x, y, dxp, dyp, sc.jx, sc.jy, sc.q * uz * rg, di, dj);
-        ix += di; iy += dj;
-        if ((unsigned)(lx + di) < (unsigned)tw && (unsigned)(ly + dj) < (unsigned)th) {
-          stay = true;
-        } else {
-          move = domain_bc(ix, iy, p.g, p.bcx, p.bcy);
-        }
-      }
-      // block-wide exclusive scan of `stay` -> compacted in-place write
-      const unsigned bal = __ballot_sync(0xffffffffu, stay);
-      if (lane == 0) s_wsum[buf][warp] = __popc(bal);
-      __syncthreads();
-      int before = 0, tot = 0;
-#pragma unroll
-      for (int w = 0; w < kBlock / 32; ++w) {
-        const int v = s_wsum[buf][w];
-        before += (w < warp) ? v : 0;
-        tot += v;
-      }
-      buf ^= 1;
-      if (stay) {
-        const long k = base + out + before + __popc(bal & ltmask);
-        __stcs(ps.cell + k, pack_cell(ix, iy));
-        __stcs(ps.x + k, x); __stcs(ps.y + k, y);
-        __stcs(ps.ux + k, ux); __stcs(ps.uy + k, uy); __stcs(ps.uz + k, uz);
-        if (ps.id) __stcs(ps.id + k, id);
-      }
-      out += tot;
-      const int m = warp_reserve(p.movers.count, move);
-      if (move) {
-        if (m < p.movers.cap) list_put(p.movers, m, pack_cell(ix, iy), x, y, ux, uy, uz, id, s);
-        else atomicOr(p.err, ERR_OVERFLOW);
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) ps.cnt[t] = out;
-    block_add_double((double)ke, p.ke_slots + s * kEnergySlots + (t & (kEnergySlots - 1)));
-  }
-  __syncthreads();
-  float* jt = p.Jt + (long)t * 3 * WJ * WJ;
-  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += kBlock) __stcg(jt + k, s_j[k]);
-}
 
 // =============================================================================================
 // K3: movers -> destination tiles (grid-stride over the device-side count).
@@ -280,7 +87,9 @@ __global__ void __launch_bounds__(kBlock) k_push_loose(PushParams p) {
     const float dxp = ux * rg * p.dtdx, dyp = uy * rg * p.dtdy;
     if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(p.err, ERR_MIGRATION);
     int di, dj;
-    advance_deposit(A, ix, iy, x, y, dxp, dyp, sc.jx, sc.jy, sc.q * uz * rg, di, dj);
+    Seg seg[3];
+    const int nseg = split_path(ix, iy, x, y, dxp, dyp, sc.q * uz * rg, seg, di, dj);
+    for (int q = 0; q < nseg; ++q) deposit_seg(A, seg[q], sc.jx, sc.jy);
     ix += di; iy += dj;
     if (domain_bc(ix, iy, p.g, p.bcx, p.bcy)) insert_particle(p, s, ix, iy, x, y, ux, uy, uz, id);
   }
@@ -525,6 +334,20 @@ __global__ void __launch_bounds__(kBlock) k_inject(InjectParams q) {
   if (threadIdx.x == 0) q.ps.cnt[t] = n;
 }
 
+// Validate host-uploaded particles and count them per tile (err bit 4 = out of the slab).
+__global__ void k_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy,
+                        const float* x, const float* y, int* counts, int* err) {
+  for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const int cx = ix[k], cy = iy[k] - y0;
+    const float px = x[k], py = y[k];
+    if (cx < 0 || cx >= nx || cy < 0 || cy >= ny || !(px >= 0.f && px < 1.f) || !(py >= 0.f && py < 1.f)) {
+      atomicOr(err, 4);
+      continue;
+    }
+    atomicAdd(counts + (cy / T) * ntx + cx / T, 1);
+  }
+}
+
 // Bin host-uploaded particles (global iy -> slab-local) into tiles.
 __global__ void k_bin(PStore ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
                       const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err) {
@@ -559,13 +382,6 @@ __global__ void k_export(PStore ps, const int64_t* prefix, int y0, int32_t* ix, 
 }
 
 // ---- host-side launchers --------------------------------------------------------------------
-void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st) {
-  switch (p.T) {
-    case 8: k_push_tiles<8><<<ntiles, kBlock, 0, st>>>(p); break;
-    case 16: k_push_tiles<16><<<ntiles, kBlock, 0, st>>>(p); break;
-    case 32: k_push_tiles<32><<<ntiles, kBlock, 0, st>>>(p); break;
-  }
-}
 void launch_insert(const PushParams& p, int grid, cudaStream_t st) { k_insert<<<grid, kBlock, 0, st>>>(p); }
 void launch_loose(const PushParams& p, int grid, cudaStream_t st) { k_push_loose<<<grid, kBlock, 0, st>>>(p); }
 void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st) {
@@ -598,6 +414,11 @@ void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t*
                 cudaStream_t st) {
   const int grid = (int)std::min<long>((n + kBlock - 1) / kBlock, 148L * 32);
   if (grid > 0) k_bin<<<grid, kBlock, 0, st>>>(ps, T, ntx, y0, n, ix, iy, x, y, ux, uy, uz, id, err);
+}
+void launch_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
+                  const float* y, int* counts, int* err, cudaStream_t st) {
+  const int grid = (int)std::min<long>((n + kBlock - 1) / kBlock, 148L * 32);
+  if (grid > 0) k_count<<<grid, kBlock, 0, st>>>(T, ntx, nx, ny, y0, n, ix, iy, x, y, counts, err);
 }
 void launch_export(const PStore& ps, int ntiles, const int64_t* prefix, int y0, int32_t* ix, int32_t* iy, float* x,
                    float* y, float* ux, float* uy, float* uz, uint32_t* id, cudaStream_t st) {

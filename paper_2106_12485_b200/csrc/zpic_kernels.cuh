@@ -63,12 +63,26 @@ struct GlobalFields {
 };
 
 // ---- current accumulators ----------------------------------------------------------------
-// Shared-memory tile current: 3 planes covering local nodes [-1, T+2), row width WJ = T + 3.
-struct SmemCurrent {
-  float* j;
+// Shared-memory tile current as exact fixed point: every contribution v (already scaled by
+// kFxScale = 2^32, a power of two, so the scaling is exact) is rounded once to an int64
+// V = rint(v), split V = hi * 2^15 + lo with 0 <= lo < 2^15, and both halves are added with
+// native 32-bit shared-memory integer atomics (sm_100a has no native fp32 shared atomic add: it
+// compiles to a CAS loop).  Integer sums are exact and order-independent, so the tile current
+// is bit-reproducible; the only error is the 2^-33 rounding of each contribution.  Ranges:
+// |sum v| < 2^14 per node; lo sums stay below 2^31 for < 21845 contributions per node (the tile
+// capacity is capped accordingly, zpic_api.cu).  3 planes x 2 halves cover local nodes
+// [-1, T+2), row width WJ = T + 3.
+constexpr float kFxScale = 4294967296.0f;  // 2^32
+constexpr double kFxInv = 2.3283064365386963e-10;  // 2^-32
+struct SmemCurrentFx {
+  int* hi;
+  int* lo;
   int WJ;
   __device__ __forceinline__ void add(int c, int i, int k, float v) const {
-    atomicAdd(j + c * WJ * WJ + (k + 1) * WJ + (i + 1), v);
+    const long long V = __float2ll_rn(v);
+    const int o = c * WJ * WJ + (k + 1) * WJ + (i + 1);
+    atomicAdd(hi + o, (int)(V >> 15));
+    atomicAdd(lo + o, (int)(V & 0x7fff));
   }
 };
 struct GlobalCurrent {
@@ -113,72 +127,79 @@ __device__ __forceinline__ float boris(float& ux, float& uy, float& uz, float ex
   return ke;
 }
 
-// ---- (3) charge-conserving deposit of one straight sub-segment, PAPER.md:146 ------------------
-// Segment in local cell (cx, cy) from (a0, b0) to (a1, b1) (cell offsets), covering fraction f
-// of the step.  Jx, Jy: the charge flux through the dual-cell faces (Villasenor-Buneman);
-// Jz: q vz f times the exact path average of the bilinear weight,
-//   W_ij = Sbar_x,i Sbar_y,j + dS_x,i dS_y,j / 12   (Sbar = mid-point weight, dS = +-(end-start)).
-template <class A>
-__device__ __forceinline__ void deposit_segment(const A& acc, int cx, int cy, float a0, float b0, float a1, float b1,
-                                                float f, float jxs, float jys, float qvz) {
-  const float da = a1 - a0, db = b1 - b0;
-  const float xm = 0.5f * (a0 + a1), ym = 0.5f * (b0 + b1);
-  const float wx = jxs * da, wy = jys * db;
-  acc.add(0, cx, cy, wx * (1.0f - ym));
-  acc.add(0, cx, cy + 1, wx * ym);
-  acc.add(1, cx, cy, wy * (1.0f - xm));
-  acc.add(1, cx + 1, cy, wy * xm);
-  const float w = qvz * f, c = da * db * (1.0f / 12.0f);
-  acc.add(2, cx, cy, w * fmaf(1.0f - xm, 1.0f - ym, c));
-  acc.add(2, cx + 1, cy, w * fmaf(xm, 1.0f - ym, -c));
-  acc.add(2, cx, cy + 1, w * fmaf(1.0f - xm, ym, -c));
-  acc.add(2, cx + 1, cy + 1, w * fmaf(xm, ym, c));
-}
+// ---- (3) charge-conserving deposit, PAPER.md:146 ---------------------------------------------
+// One straight sub-segment of a particle path: local cell (cx, cy), offsets (a0,b0)->(a1,b1),
+// and wz = q vz f (the z-current weight of the piece).
+struct Seg {
+  int cx, cy;
+  float a0, b0, a1, b1, wz;
+};
 
-// Position advance by (dxp, dyp) cells from local cell (lx, ly), offset (x, y): split the
-// straight path at the cell edges it crosses (at most one per axis), deposit
-// every piece, and return the new offset and the cell steps (di, dj) with the R6 rounding
-// rule (an offset that rounds to 1 after renormalisation becomes 0 in the next cell).
-template <class A>
-__device__ __forceinline__ void advance_deposit(const A& acc, int lx, int ly, float& x, float& y, float dxp, float dyp,
-                                                float jxs, float jys, float qvz, int& di, int& dj) {
+// Villasenor-Buneman split of the path (x, y) -> (x + dxp, y + dyp) from local cell (lx, ly)
+// into 1-3 straight pieces at the cell edges it crosses (at most one per axis),
+// in time order; returns the piece count, the cell steps (di, dj) and the renormalised offset
+// with the R6 rounding rule.  Pieces beyond the count are left untouched.
+__device__ __forceinline__ int split_path(int lx, int ly, float& x, float& y, float dxp, float dyp, float qvz, Seg* s,
+                                          int& di, int& dj) {
   const float x1 = x + dxp, y1 = y + dyp;
   di = (x1 >= 1.0f) - (x1 < 0.0f);
   dj = (y1 >= 1.0f) - (y1 < 0.0f);
+  int n;
   if ((di | dj) == 0) {
-    deposit_segment(acc, lx, ly, x, y, x1, y1, 1.0f, jxs, jys, qvz);
+    s[0] = Seg{lx, ly, x, y, x1, y1, qvz};
+    n = 1;
   } else if (dj == 0) {
     const float xb = di > 0 ? 1.0f : 0.0f;
     const float t = (xb - x) / dxp;
     const float yb = fmaf(t, dyp, y);
-    deposit_segment(acc, lx, ly, x, y, xb, yb, t, jxs, jys, qvz);
-    deposit_segment(acc, lx + di, ly, xb - di, yb, x1 - di, y1, 1.0f - t, jxs, jys, qvz);
+    s[0] = Seg{lx, ly, x, y, xb, yb, qvz * t};
+    s[1] = Seg{lx + di, ly, xb - di, yb, x1 - di, y1, qvz * (1.0f - t)};
+    n = 2;
   } else if (di == 0) {
     const float yb = dj > 0 ? 1.0f : 0.0f;
     const float t = (yb - y) / dyp;
     const float xb = fmaf(t, dxp, x);
-    deposit_segment(acc, lx, ly, x, y, xb, yb, t, jxs, jys, qvz);
-    deposit_segment(acc, lx, ly + dj, xb, yb - dj, x1, y1 - dj, 1.0f - t, jxs, jys, qvz);
+    s[0] = Seg{lx, ly, x, y, xb, yb, qvz * t};
+    s[1] = Seg{lx, ly + dj, xb, yb - dj, x1, y1 - dj, qvz * (1.0f - t)};
+    n = 2;
   } else {
     const float xb = di > 0 ? 1.0f : 0.0f, yb = dj > 0 ? 1.0f : 0.0f;
     const float tx = (xb - x) / dxp, ty = (yb - y) / dyp;
     if (tx <= ty) {  // x edge first
       const float yx = fmaf(tx, dyp, y), xy = fmaf(ty, dxp, x);
-      deposit_segment(acc, lx, ly, x, y, xb, yx, tx, jxs, jys, qvz);
-      deposit_segment(acc, lx + di, ly, xb - di, yx, xy - di, yb, ty - tx, jxs, jys, qvz);
-      deposit_segment(acc, lx + di, ly + dj, xy - di, yb - dj, x1 - di, y1 - dj, 1.0f - ty, jxs, jys, qvz);
+      s[0] = Seg{lx, ly, x, y, xb, yx, qvz * tx};
+      s[1] = Seg{lx + di, ly, xb - di, yx, xy - di, yb, qvz * (ty - tx)};
+      s[2] = Seg{lx + di, ly + dj, xy - di, yb - dj, x1 - di, y1 - dj, qvz * (1.0f - ty)};
     } else {         // y edge first
       const float xy = fmaf(ty, dxp, x), yx = fmaf(tx, dyp, y);
-      deposit_segment(acc, lx, ly, x, y, xy, yb, ty, jxs, jys, qvz);
-      deposit_segment(acc, lx, ly + dj, xy, yb - dj, xb, yx - dj, tx - ty, jxs, jys, qvz);
-      deposit_segment(acc, lx + di, ly + dj, xb - di, yx - dj, x1 - di, y1 - dj, 1.0f - tx, jxs, jys, qvz);
+      s[0] = Seg{lx, ly, x, y, xy, yb, qvz * ty};
+      s[1] = Seg{lx, ly + dj, xy, yb - dj, xb, yx - dj, qvz * (tx - ty)};
+      s[2] = Seg{lx + di, ly + dj, xb - di, yx - dj, x1 - di, y1 - dj, qvz * (1.0f - tx)};
     }
+    n = 3;
   }
   float xn = x1 - di, yn = y1 - dj;
   if (xn >= 1.0f) { xn = 0.0f; di += 1; }   // R6: only reachable when x1 < 0 rounds to 1
   if (yn >= 1.0f) { yn = 0.0f; dj += 1; }
   x = xn;
   y = yn;
+  return n;
+}
+
+template <class A>
+__device__ __forceinline__ void deposit_seg(const A& acc, const Seg& s, float jxs, float jys) {
+  const float da = s.a1 - s.a0, db = s.b1 - s.b0;
+  const float xm = 0.5f * (s.a0 + s.a1), ym = 0.5f * (s.b0 + s.b1);
+  const float wx = jxs * da, wy = jys * db;
+  acc.add(0, s.cx, s.cy, wx * (1.0f - ym));
+  acc.add(0, s.cx, s.cy + 1, wx * ym);
+  acc.add(1, s.cx, s.cy, wy * (1.0f - xm));
+  acc.add(1, s.cx + 1, s.cy, wy * xm);
+  const float c = da * db * (1.0f / 12.0f);
+  acc.add(2, s.cx, s.cy, s.wz * fmaf(1.0f - xm, 1.0f - ym, c));
+  acc.add(2, s.cx + 1, s.cy, s.wz * fmaf(xm, 1.0f - ym, -c));
+  acc.add(2, s.cx, s.cy + 1, s.wz * fmaf(1.0f - xm, ym, -c));
+  acc.add(2, s.cx + 1, s.cy + 1, s.wz * fmaf(xm, ym, c));
 }
 
 }  // namespace zpic

@@ -1,0 +1,273 @@
+// zpic_push.cu — K1, the fused particle kernel of the B200 EM-PIC step.
+//
+// One CTA per tile of T x T cells.  It stages the tile's E and B (+1 guard cell each side) in
+// shared memory, pushes every particle of every species of the tile — interpolation
+// (PAPER.md:144), relativistic Boris, charge-conserving deposit
+// — and accumulates the tile's current exactly in shared memory (fixed point,
+// native integer atomics).  Then it stores the (T+3)^2 current block for K4 and fixes up the
+// tile's particle segment.
+//
+// Divergence control: every lane deposits the first straight piece of its path in lock-step;
+// the extra pieces of cell-crossing paths go to a per-warp shared-memory queue that is drained
+// 32 at a time with all lanes active.
+// Re-sort: particles that stay in the tile are written back in place; leavers leave a hole
+// (cell = -1) and go to the mover list (K3 inserts them into their new tile).  Once per tile
+// and species, the holes below the new count are filled from the tail — no block barrier per
+// chunk, and only O(#leavers) particle moves.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "zpic_device.cuh"
+
+namespace zpic {
+
+constexpr int kQCap = 96;   // per-warp queue of extra path pieces (<= 31 + 2 * 32 after a chunk)
+constexpr int kHCap = 256;  // holes recorded per tile and species (else the sentinel fallback)
+constexpr int kHole = -1;   // cell value of a vacated slot
+
+// Per-warp queue of path pieces in shared memory (structure of arrays: conflict-free lanes).
+struct SegQueue {
+  int* c;     // packed (cx + 8) | (cy + 8) << 16
+  float *a0, *b0, *a1, *b1, *wz;
+  __device__ __forceinline__ void put(int k, const Seg& s) const {
+    c[k] = (s.cx + 8) | ((s.cy + 8) << 16);
+    a0[k] = s.a0; b0[k] = s.b0; a1[k] = s.a1; b1[k] = s.b1; wz[k] = s.wz;
+  }
+  __device__ __forceinline__ Seg get(int k) const {
+    const int v = c[k];
+    return Seg{(v & 0xffff) - 8, (v >> 16) - 8, a0[k], b0[k], a1[k], b1[k], wz[k]};
+  }
+};
+
+template <int T>
+__global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
+  constexpr int W = T + 2, WJ = T + 3, NW = kBlock / 32;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* s_eb1 = reinterpret_cast<float2*>(smem_raw);
+  float2* s_eb2 = s_eb1 + W * W;
+  float* s_ez = reinterpret_cast<float*>(s_eb2 + W * W);
+  float* s_bz = s_ez + W * W;
+  int* s_jhi = reinterpret_cast<int*>(s_bz + W * W);
+  int* s_jlo = s_jhi + 3 * WJ * WJ;
+  int* s_q = s_jlo + 3 * WJ * WJ;  // 6 arrays of NW * kQCap words
+  __shared__ int s_holes[kHCap], s_hb[kHCap], s_sa[kHCap];
+  __shared__ unsigned s_bits[kHCap / 32];
+  __shared__ int s_cnt[4];  // holes, holes below, stayers above, hole-list overflow
+  __shared__ int s_wsum[2][NW];
+
+  const int t = blockIdx.x;
+  const int tx = t % p.ntx, ty = t / p.ntx;
+  const int i0 = tx * T, j0 = ty * T;
+  const int tw = min(T, p.g.nx - i0), th = min(T, p.g.ny - j0);
+  const long pl = p.g.plane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned ltmask = lanemask_lt();
+
+  for (int k = threadIdx.x; k < W * W; k += kBlock) {
+    const int gi = i0 + k % W - 1, gj = j0 + k / W - 1;
+    float ex = 0.f, ey = 0.f, ez = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
+    if (gi <= p.g.nx + 1 && gj <= p.g.ny + 1) {
+      const long a = p.g.at(gi, gj);
+      ex = __ldg(p.E + a); ey = __ldg(p.E + pl + a); ez = __ldg(p.E + 2 * pl + a);
+      bx = __ldg(p.B + a); by = __ldg(p.B + pl + a); bz = __ldg(p.B + 2 * pl + a);
+    }
+    s_eb1[k] = make_float2(ex, by);
+    s_eb2[k] = make_float2(ey, bx);
+    s_ez[k] = ez;
+    s_bz[k] = bz;
+  }
+  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += kBlock) { s_jhi[k] = 0; s_jlo[k] = 0; }
+
+  const SmemFields F{s_eb1, s_eb2, s_ez, s_bz, W};
+  const SmemCurrentFx A{s_jhi, s_jlo, WJ};
+  const int qo = warp * kQCap;
+  const SegQueue Q{s_q + qo, reinterpret_cast<float*>(s_q + NW * kQCap + qo),
+                   reinterpret_cast<float*>(s_q + 2 * NW * kQCap + qo), reinterpret_cast<float*>(s_q + 3 * NW * kQCap + qo),
+                   reinterpret_cast<float*>(s_q + 4 * NW * kQCap + qo), reinterpret_cast<float*>(s_q + 5 * NW * kQCap + qo)};
+
+  for (int s = 0; s < p.nspecies; ++s) {
+    const PStore ps = p.ps[s];
+    const SpeciesConst sc = p.sc[s];
+    const float jxs = sc.jx * kFxScale, jys = sc.jy * kFxScale, qs = sc.q * kFxScale;
+    const int n = ps.cnt[t];
+    const long base = (long)t * ps.cap;
+    if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    __syncthreads();
+    float ke = 0.f;
+    int qn = 0;  // warp-uniform queue fill
+    // software pipeline: the next chunk's particle is loaded while this one is pushed
+    int ncell = 0;
+    float nxo = 0.f, nyo = 0.f, nux = 0.f, nuy = 0.f, nuz = 0.f;
+    uint32_t nid = 0;
+    if ((int)threadIdx.x < n) {
+      const long k = base + threadIdx.x;
+      ncell = __ldcs(ps.cell + k);
+      nxo = __ldcs(ps.x + k); nyo = __ldcs(ps.y + k);
+      nux = __ldcs(ps.ux + k); nuy = __ldcs(ps.uy + k); nuz = __ldcs(ps.uz + k);
+      if (ps.id) nid = __ldcs(ps.id + k);
+    }
+    for (int c0 = 0; c0 < n; c0 += kBlock) {
+      const int i = c0 + threadIdx.x;
+      const bool valid = i < n;
+      const int cell = ncell;
+      float x = nxo, y = nyo, ux = nux, uy = nuy, uz = nuz;
+      const uint32_t id = nid;
+      if (i + kBlock < n) {
+        const long k = base + i + kBlock;
+        ncell = __ldcs(ps.cell + k);
+        nxo = __ldcs(ps.x + k); nyo = __ldcs(ps.y + k);
+        nux = __ldcs(ps.ux + k); nuy = __ldcs(ps.uy + k); nuz = __ldcs(ps.uz + k);
+        if (ps.id) nid = __ldcs(ps.id + k);
+      }
+      Seg seg[3];
+      int nseg = 0, ix = 0, iy = 0;
+      bool stay = false, move = false;
+      if (valid) {
+        ix = cell_ix(cell); iy = cell_iy(cell);
+        const int lx = ix - i0, ly = iy - j0;
+        float ex, ey, ez, bx, by, bz;
+        interpolate(F, lx, ly, x, y, ex, ey, ez, bx, by, bz);
+        ke += boris(ux, uy, uz, ex, ey, ez, bx, by, bz, sc.h);
+        const float rg = rsqrtf(1.0f + fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
+        const float dxp = ux * rg * p.dtdx, dyp = uy * rg * p.dtdy;
+        if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(p.err, ERR_MIGRATION);
+        int di, dj;
+        nseg = split_path(lx, ly, x, y, dxp, dyp, qs * uz * rg, seg, di, dj);
+        deposit_seg(A, seg[0], jxs, jys);
+        ix += di; iy += dj;
+        if ((unsigned)(lx + di) < (unsigned)tw && (unsigned)(ly + dj) < (unsigned)th) stay = true;
+        else move = domain_bc(ix, iy, p.g, p.bcx, p.bcy);
+      }
+      // extra pieces -> this warp's queue; drain full batches of 32 with every lane active
+#pragma unroll
+      for (int k = 1; k < 3; ++k) {
+        const bool has = nseg > k;
+        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        if (has) Q.put(qn + __popc(bal & ltmask), seg[k]);
+        qn += __popc(bal);
+      }
+      __syncwarp();
+      while (qn >= 32) {
+        deposit_seg(A, Q.get(lane), jxs, jys);
+        __syncwarp();
+        const bool m1 = lane + 32 < qn, m2 = lane + 64 < qn;
+        Seg s1, s2;
+        if (m1) s1 = Q.get(lane + 32);
+        if (m2) s2 = Q.get(lane + 64);
+        __syncwarp();
+        if (m1) Q.put(lane, s1);
+        if (m2) Q.put(lane + 32, s2);
+        qn -= 32;
+        __syncwarp();
+      }
+      if (valid) {
+        const long k = base + i;
+        if (stay) {
+          __stcs(ps.cell + k, pack_cell(ix, iy));
+          __stcs(ps.x + k, x); __stcs(ps.y + k, y);
+          __stcs(ps.ux + k, ux); __stcs(ps.uy + k, uy); __stcs(ps.uz + k, uz);
+        } else {
+          ps.cell[k] = kHole;
+          const int h = atomicAdd(&s_cnt[0], 1);
+          if (h < kHCap) s_holes[h] = i;
+          else s_cnt[3] = 1;
+        }
+      }
+      const int m = warp_reserve(p.movers.count, move);
+      if (move) {
+        if (m < p.movers.cap) list_put(p.movers, m, pack_cell(ix, iy), x, y, ux, uy, uz, id, s);
+        else atomicOr(p.err, ERR_OVERFLOW);
+      }
+    }
+    if (lane < qn) deposit_seg(A, Q.get(lane), jxs, jys);
+    block_add_double((double)ke, p.ke_slots + s * kEnergySlots + (t & (kEnergySlots - 1)));  // has barriers
+
+    // ---- re-sort: fill the holes below the new count from the tail --------------------------
+    const int nh = s_cnt[0], n2 = n - nh;
+    if (nh > 0 && s_cnt[3] == 0) {
+      for (int k = threadIdx.x; k < (nh + 31) / 32; k += kBlock) s_bits[k] = 0u;
+      __syncthreads();
+      for (int k = threadIdx.x; k < nh; k += kBlock) {
+        const int pos = s_holes[k];
+        if (pos >= n2) atomicOr(&s_bits[(pos - n2) >> 5], 1u << ((pos - n2) & 31));
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < nh; k += kBlock) {
+        const int pos = s_holes[k];
+        if (pos < n2) s_hb[atomicAdd(&s_cnt[1], 1)] = pos;
+        const int q = n2 + k;   // the tail [n2, n) has exactly nh slots
+        if (!((s_bits[k >> 5] >> (k & 31)) & 1u)) s_sa[atomicAdd(&s_cnt[2], 1)] = q;
+      }
+      __syncthreads();
+      const int nmove = s_cnt[1];
+      for (int k = threadIdx.x; k < nmove; k += kBlock) {
+        const long d = base + s_hb[k], sidx = base + s_sa[k];
+        ps.cell[d] = ps.cell[sidx];
+        ps.x[d] = ps.x[sidx]; ps.y[d] = ps.y[sidx];
+        ps.ux[d] = ps.ux[sidx]; ps.uy[d] = ps.uy[sidx]; ps.uz[d] = ps.uz[sidx];
+        if (ps.id) ps.id[d] = ps.id[sidx];
+      }
+    } else if (nh > 0) {
+      // more holes than the list holds: stable compaction of the whole segment by the sentinel
+      __syncthreads();
+      int out = 0, buf = 0;
+      for (int c0 = 0; c0 < n; c0 += kBlock) {
+        const int i = c0 + threadIdx.x;
+        int cell = kHole;
+        float x = 0.f, y = 0.f, ux = 0.f, uy = 0.f, uz = 0.f;
+        uint32_t id = 0;
+        if (i < n) {
+          const long k = base + i;
+          cell = ps.cell[k];
+          x = ps.x[k]; y = ps.y[k]; ux = ps.ux[k]; uy = ps.uy[k]; uz = ps.uz[k];
+          if (ps.id) id = ps.id[k];
+        }
+        const bool keep = cell != kHole;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_wsum[buf][warp] = __popc(bal);
+        __syncthreads();
+        int before = 0, tot = 0;
+        for (int w = 0; w < NW; ++w) {
+          const int v = s_wsum[buf][w];
+          before += (w < warp) ? v : 0;
+          tot += v;
+        }
+        buf ^= 1;
+        if (keep) {
+          const long k = base + out + before + __popc(bal & ltmask);
+          ps.cell[k] = cell; ps.x[k] = x; ps.y[k] = y; ps.ux[k] = ux; ps.uy[k] = uy; ps.uz[k] = uz;
+          if (ps.id) ps.id[k] = id;
+        }
+        out += tot;
+      }
+    }
+    if (threadIdx.x == 0) ps.cnt[t] = n2;
+    __syncthreads();
+  }
+  float* jt = p.Jt + (long)t * 3 * WJ * WJ;
+  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += kBlock)
+    __stcg(jt + k, (float)(fma((double)s_jhi[k], 32768.0, (double)s_jlo[k]) * kFxInv));
+}
+
+template <int T>
+static void launch_push_T(const PushParams& p, int ntiles, cudaStream_t st) {
+  constexpr int W = T + 2, WJ = T + 3;
+  constexpr size_t smem = (size_t)W * W * (2 * sizeof(float2) + 2 * sizeof(float)) + (size_t)6 * WJ * WJ * sizeof(int) +
+                          (size_t)6 * (kBlock / 32) * kQCap * sizeof(int);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_push_tiles<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = true;
+  }
+  k_push_tiles<T><<<ntiles, kBlock, smem, st>>>(p);
+}
+
+void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st) {
+  switch (p.T) {
+    case 8: launch_push_T<8>(p, ntiles, st); break;
+    case 16: launch_push_T<16>(p, ntiles, st); break;
+    case 32: launch_push_T<32>(p, ntiles, st); break;
+  }
+}
+
+}  // namespace zpic

@@ -182,9 +182,9 @@ def zpic_energy(ctx, nspecies):
 
 
 def zpic_counters(ctx):
-    out = (ctypes.c_int64 * 6)()
-    _check(_lib.zpic_counters(ctx, out, 6), ctx)
-    keys = ("particles", "movers", "max_fill_permille", "repacks", "steps", "tiles")
+    out = (ctypes.c_int64 * 7)()
+    _check(_lib.zpic_counters(ctx, out, 7), ctx)
+    keys = ("particles", "movers", "max_fill_permille", "repacks", "steps", "tiles", "launches")
     return dict(zip(keys, list(out)))
 
 
@@ -242,6 +242,8 @@ class Simulation:
             import torch
             dev = torch.cuda.current_device()
             st = stream if stream is not None else torch.cuda.current_stream()
+            if st.cuda_stream == 0:      # the legacy NULL stream: give the library a real one
+                st = torch.cuda.Stream()
             opt.stream = st.cuda_stream
             self.torch_stream = st
 

@@ -16,16 +16,16 @@ def _z():
     return z
 
 
-def gpu_from_particles(cfg, parts, tile=16):
-    sim = _z().Simulation(cfg, inject=False, track_ids=True, tile=tile)
+def gpu_from_particles(cfg, parts, tile=16, slack=1.25):
+    sim = _z().Simulation(cfg, inject=False, track_ids=True, tile=tile, capacity_slack=slack)
     for s, p in enumerate(parts):
         sim.set_particles(s, p)
     return sim
 
 
-def _parity_run(cfg, steps, tile=16, check_every_step=True):
+def _parity_run(cfg, steps, tile=16, check_every_step=True, slack=1.25):
     parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
-    g = gpu_from_particles(cfg, parts, tile)
+    g = gpu_from_particles(cfg, parts, tile, slack)
     o = from_config(cfg, particles=parts)
     nx, ny, dx, dy, dt = cfg["nx"], cfg["ny"], cfg["dx"], cfg["dy"], cfg["dt"]
     q = [o.species[s]["q"] for s in range(len(parts))]
@@ -92,6 +92,23 @@ def test_ragged_grid_tiles(tile):
     cfg = synth.config("C1", nx=50, ny=37)
     cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)   # more crossings
     _parity_run(cfg, 10, tile=tile)
+
+
+def test_tile_overflow_loose_path():
+    """Capacity slack 1.0: thermal fluctuations overflow tiles every step, so particles go
+    through the loose list (global-memory push + re-insertion); results are unchanged."""
+    cfg = synth.config("C1", nx=48, ny=48)
+    cfg["species"][0]["uth"] = (0.4, 0.4, 0.4)
+    _parity_run(cfg, 10, slack=1.0)
+
+
+def test_hole_list_overflow_fallback():
+    """A fast diagonal drift with 32x32 tiles makes > 256 particles leave a tile in one step,
+    which exercises the sentinel compaction path of K1."""
+    cfg = synth.config("C1", nx=64, ny=64)
+    cfg["species"][0]["ufl"] = (2.0, 2.0, 0.0)
+    cfg["species"][0]["uth"] = (0.05, 0.05, 0.05)
+    _parity_run(cfg, 10, tile=32)
 
 
 def test_device_injection_matches_generator():
