@@ -8,7 +8,11 @@ CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libzpic_b200.so")
 SOURCES = ["zpic_api.cu", "zpic_kernels.cu", "zpic_push.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+# -ftz=true: fp32 denormals flush to zero (no guard code around rsqrt / rcp); -prec-div=false:
+# approximate fp32 division (2 ulp) for the cell-crossing fractions.  The fp64 paths (injector RNG,
+# energy sums) are unaffected.
+FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17", "-ftz=true",
+         "-prec-div=false", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 

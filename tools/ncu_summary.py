@@ -22,7 +22,12 @@ src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-so
                      text=True).stdout
 rows = list(csv.reader(src.splitlines()))
 hh = rows[1]
-data = rows[2:]
+data = []
+for r in rows[2:]:
+    if r and r[0] == "Kernel Name":
+        break                      # only the first kernel's source page
+    if len(r) == len(hh):
+        data.append(r)
 iS, iE, iW, iT = (hh.index(k) for k in ("Source", "Instructions Executed", "Warp Stall Sampling (All Samples)",
                                          "Avg. Threads Executed"))
 tot = sum(int(r[iE]) for r in data if r[iE].isdigit())
