@@ -240,7 +240,6 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
   }
   if (bc->y == ZPIC_BC_MOVING_WINDOW) { g_init_error = "moving window is x only"; return ZPIC_E_INVALID; }
   if (bc->x == ZPIC_BC_MOVING_WINDOW) { g_init_error = "moving window not supported yet"; return ZPIC_E_INVALID; }
-  if (bc->x == ZPIC_BC_OPEN || bc->y == ZPIC_BC_OPEN) { g_init_error = "open boundaries not supported yet"; return ZPIC_E_INVALID; }
   int world = 1, rank = 0;
   if (dist && dist->world > 1) {
     g_init_error = "multi-GPU slabs not supported yet"; return ZPIC_E_DECOMP;
@@ -470,6 +469,8 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
       y.dt = (float)c->dt;
       y.dtdx = (float)(c->dt / c->dx); y.dtdy = (float)(c->dt / c->dy);
       y.hdx = (float)(0.5 * c->dt / c->dx); y.hdy = (float)(0.5 * c->dt / c->dy);
+      y.murx = (float)((c->dt - c->dx) / (c->dt + c->dx));
+      y.mury = (float)((c->dt - c->dy) / (c->dt + c->dy));
       y.bcx = c->bcx; y.bcy = c->bcy;
       y.fe_slots = c->fe_slots;
       y.fe_scale = 0.5 * c->dx * c->dy;

@@ -79,6 +79,7 @@ struct YeeParams {
   const float* E0; const float* B0; const float* J;
   float* E1; float* B1;
   float dt, dtdx, dtdy, hdx, hdy;   // dt, dt/dx, dt/dy, (dt/2)/dx, (dt/2)/dy
+  float murx, mury;                 // Mur-1 coefficients (dt - dx)/(dt + dx), (dt - dy)/(dt + dy)
   int bcx, bcy;
   double* fe_slots;
   double fe_scale;  // dx dy / 2

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   __shared__ float sE[3][WE * WE];
   __shared__ float sB[3][WB * WB];
   __shared__ float sJ[3][WJ * WJ];
+  __shared__ float s_mur[4][2][2][T + 1];  // E^n on Mur node lines: [edge][component][b, b'][index]
   const GridDesc& g = p.g;
   const int i0 = blockIdx.x * T, j0 = blockIdx.y * T;
   const int tw = min(T, g.nx - i0), th = min(T, g.ny - j0);
@@ -211,6 +212,20 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
     sB[1][k] += p.hdx * (sE[2][EI(lx + 1, ly)] - ez);
     sB[2][k] += p.hdy * (sE[0][EI(lx, ly + 1)] - sE[0][EI(lx, ly)]) - p.hdx * (sE[1][EI(lx + 1, ly)] - sE[1][EI(lx, ly)]);
   }
+  if (p.bcx == ZPIC_BC_OPEN || p.bcy == ZPIC_BC_OPEN) {   // save E^n on the Mur node lines
+    for (int k = threadIdx.x; k < 4 * 2 * 2 * (T + 1); k += kBlock) {
+      const int idx = k % (T + 1), node = (k / (T + 1)) % 2, comp = (k / (2 * (T + 1))) % 2, edge = k / (4 * (T + 1));
+      float v = 0.f;
+      if (edge < 2 && p.bcx == ZPIC_BC_OPEN && idx <= th) {
+        const int bn = edge ? tw : 0, bp = edge ? tw - 1 : 1;
+        v = sE[comp ? 2 : 1][EI(node ? bp : bn, idx)];
+      } else if (edge >= 2 && p.bcy == ZPIC_BC_OPEN && idx <= tw) {
+        const int bn = edge == 3 ? th : 0, bp = edge == 3 ? th - 1 : 1;
+        v = sE[comp ? 2 : 0][EI(idx, node ? bp : bn)];
+      }
+      s_mur[edge][comp][node][idx] = v;
+    }
+  }
   __syncthreads();
   // E^{n+1} on [0, T]^2
   for (int k = threadIdx.x; k < WJ * WJ; k += kBlock) {
@@ -219,6 +234,43 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
     sE[0][e] += p.dtdy * (sB[2][b] - sB[2][BI(lx, ly - 1)]) - p.dt * sJ[0][k];
     sE[1][e] -= p.dtdx * (sB[2][b] - sB[2][BI(lx - 1, ly)]) + p.dt * sJ[1][k];
     sE[2][e] += p.dtdx * (sB[1][b] - sB[1][BI(lx - 1, ly)]) - p.dtdy * (sB[0][b] - sB[0][BI(lx, ly - 1)]) - p.dt * sJ[2][k];
+  }
+  __syncthreads();
+  // Non-periodic edges (R13, R14).  The node line on a domain edge holds: Mur-1 values for the
+  // tangential E on an open edge, E^{n+1}_b = E^n_b' + k (E^{n+1}_b' - E^n_b); zero (a guard) for
+  // everything else outside the box.  x edges first, then y edges (the oracle's order).
+  const bool xlo = i0 == 0, xhi = i0 + tw == g.nx, ylo = j0 == 0, yhi = j0 + th == g.ny;
+  if (p.bcx != ZPIC_BC_PERIODIC && (xlo || xhi)) {
+    for (int k = threadIdx.x; k < 2 * (th + 1); k += kBlock) {
+      const int ly = k % (th + 1), hiE = k / (th + 1);
+      if (!(hiE ? xhi : xlo)) continue;
+      const int gj = j0 + ly, bn = hiE ? tw : 0, bp = hiE ? tw - 1 : 1;
+      const bool row_out = p.bcy != ZPIC_BC_PERIODIC && gj == g.ny;   // guard row of an open y axis
+      if (p.bcx == ZPIC_BC_OPEN && !row_out) {
+        sE[1][EI(bn, ly)] = s_mur[hiE][0][1][ly] + p.murx * (sE[1][EI(bp, ly)] - s_mur[hiE][0][0][ly]);
+        if (!(p.bcy == ZPIC_BC_OPEN && gj == 0))
+          sE[2][EI(bn, ly)] = s_mur[hiE][1][1][ly] + p.murx * (sE[2][EI(bp, ly)] - s_mur[hiE][1][0][ly]);
+        else if (hiE)
+          sE[2][EI(bn, ly)] = 0.f;   // corner node (nx, 0) of two open edges: never Mur-updated
+        if (hiE) sE[0][EI(bn, ly)] = 0.f;
+      } else if (hiE) {
+        sE[0][EI(bn, ly)] = 0.f; sE[1][EI(bn, ly)] = 0.f; sE[2][EI(bn, ly)] = 0.f;
+      }
+    }
+  }
+  __syncthreads();
+  if (p.bcy != ZPIC_BC_PERIODIC && (ylo || yhi)) {
+    for (int k = threadIdx.x; k < 2 * (tw + 1); k += kBlock) {
+      const int lx = k % (tw + 1), hiE = k / (tw + 1);
+      if (!(hiE ? yhi : ylo)) continue;
+      const int gi = i0 + lx, bn = hiE ? th : 0, bp = hiE ? th - 1 : 1;
+      if (p.bcx != ZPIC_BC_PERIODIC && gi == g.nx) continue;   // corner column: set by the x pass
+      if (p.bcy == ZPIC_BC_OPEN) {
+        sE[0][EI(lx, bn)] = s_mur[2 + hiE][0][1][lx] + p.mury * (sE[0][EI(lx, bp)] - s_mur[2 + hiE][0][0][lx]);
+        sE[2][EI(lx, bn)] = s_mur[2 + hiE][1][1][lx] + p.mury * (sE[2][EI(lx, bp)] - s_mur[2 + hiE][1][0][lx]);
+        if (hiE) sE[1][EI(lx, bn)] = 0.f;
+      }
+    }
   }
   __syncthreads();
   // B^{n+1} on [0, T)^2 and the stores
@@ -251,6 +303,39 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
           p.B1[c * pl + o] = vals[3 + c];
         }
       }
+  }
+  // Mur nodes on the high edges sit in the first high guard (node nx / ny)
+  if (p.bcx == ZPIC_BC_OPEN && xhi) {
+    for (int ly = threadIdx.x; ly < th; ly += kBlock) {
+      const int gj = j0 + ly;
+      int ys[3], nys = 1;
+      ys[0] = gj;
+      if (p.bcy == ZPIC_BC_PERIODIC) {
+        if (gj <= 1) ys[nys++] = gj + g.ny;
+        if (gj == g.ny - 1) ys[nys++] = -1;
+      }
+      for (int a = 0; a < nys; ++a) {
+        const long o = g.at(g.nx, ys[a]);
+        p.E1[pl + o] = sE[1][EI(tw, ly)];
+        p.E1[2 * pl + o] = sE[2][EI(tw, ly)];
+      }
+    }
+  }
+  if (p.bcy == ZPIC_BC_OPEN && yhi) {
+    for (int lx = threadIdx.x; lx < tw; lx += kBlock) {
+      const int gi = i0 + lx;
+      int xs[3], nxs = 1;
+      xs[0] = gi;
+      if (p.bcx == ZPIC_BC_PERIODIC) {
+        if (gi <= 1) xs[nxs++] = gi + g.nx;
+        if (gi == g.nx - 1) xs[nxs++] = -1;
+      }
+      for (int a = 0; a < nxs; ++a) {
+        const long o = g.at(xs[a], g.ny);
+        p.E1[o] = sE[0][EI(lx, th)];
+        p.E1[2 * pl + o] = sE[2][EI(lx, th)];
+      }
+    }
   }
 #undef EI
 #undef BI

@@ -65,11 +65,18 @@ def rho_nodes(nx, ny, q, p):
     return r
 
 
-def continuity_residual(nx, ny, dx, dy, dt, rho0, rho1, J):
+def continuity_residual(nx, ny, dx, dy, dt, rho0, rho1, J, bc=(0, 0)):
+    """max |rho1 - rho0 + dt div J| over nodes; cells within 2 of a non-periodic edge are
+    excluded (R21: charge leaves there)."""
     Jx = J[0].astype(np.float64)
     Jy = J[1].astype(np.float64)
     div = (Jx - np.roll(Jx, 1, axis=1)) / dx + (Jy - np.roll(Jy, 1, axis=0)) / dy
-    return float(np.max(np.abs(rho1 - rho0 + dt * div)))
+    r = np.abs(rho1 - rho0 + dt * div)
+    if bc[0] != 0:
+        r = r[:, 2:-2]
+    if bc[1] != 0:
+        r = r[2:-2, :]
+    return float(np.max(r))
 
 
 def energy_agreement(hist_g, hist_o):
