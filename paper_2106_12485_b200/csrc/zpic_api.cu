@@ -30,6 +30,10 @@ void launch_export(const PStore& ps, int ntiles, const int64_t* prefix, int y0, 
                    float* y, float* ux, float* uy, float* uz, uint32_t* id, cudaStream_t st);
 void launch_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
                   const float* y, int* counts, int* err, cudaStream_t st);
+void launch_inject_column(const PushParams& p, int s, int px, int py, int n_move, int ny_global, int y0, uint64_t key,
+                          const double* ufl, const double* uth, cudaStream_t st);
+void launch_filter_x(const float* Jin, float* Jout, const GridDesc& g, int npass, int compensated, int periodic,
+                     cudaStream_t st);
 }  // namespace zpic
 
 using namespace zpic;
@@ -145,9 +149,9 @@ void refresh_field_guards(zpic_ctx* c, float* F, bool is_E) {
 }
 
 // ---- profiling ---------------------------------------------------------------------------
-enum KId { K_PUSH = 0, K_INSERT, K_ASSEMBLE, K_LOOSE, K_FOLD, K_YEE, K_EPI, K_COUNT };
-const char* kNames[K_COUNT] = {"k_push_tiles", "k_insert", "k_assemble_j", "k_push_loose", "k_guard_fold", "k_yee",
-                               "k_epilogue"};
+enum KId { K_PUSH = 0, K_INSERT, K_ASSEMBLE, K_LOOSE, K_FOLD, K_FILTER, K_YEE, K_WINDOW, K_EPI, K_COUNT };
+const char* kNames[K_COUNT] = {"k_push_tiles", "k_insert", "k_assemble_j", "k_push_loose", "k_guard_fold",
+                               "k_filter_x", "k_yee", "k_inject_column", "k_epilogue"};
 
 struct ProfScope {
   zpic_ctx* c;
@@ -239,7 +243,6 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       if (sp.uth[k] < 0) { g_init_error = "species " + std::to_string(s) + ": uth >= 0"; return ZPIC_E_INVALID; }
   }
   if (bc->y == ZPIC_BC_MOVING_WINDOW) { g_init_error = "moving window is x only"; return ZPIC_E_INVALID; }
-  if (bc->x == ZPIC_BC_MOVING_WINDOW) { g_init_error = "moving window not supported yet"; return ZPIC_E_INVALID; }
   int world = 1, rank = 0;
   if (dist && dist->world > 1) {
     g_init_error = "multi-GPU slabs not supported yet"; return ZPIC_E_DECOMP;
@@ -295,7 +298,8 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     // fields
     for (int b = 0; b < 2; ++b) { c->E[b] = alloc_n<float>(c, 3 * g.plane); c->B[b] = alloc_n<float>(c, 3 * g.plane); }
     c->J = alloc_n<float>(c, 3 * g.plane);
-    c->Jpre = nullptr;
+    c->Jf = c->opt.filter_passes > 0 ? alloc_n<float>(c, 3 * g.plane) : nullptr;
+    if (c->opt.filter_passes < 0 || c->opt.filter_passes > 64) throw Fail{ZPIC_E_INVALID, "filter_passes must be in [0, 64]"};
     const int WJ = c->T + 3;
     c->Jt = alloc_n<float>(c, (size_t)c->ntiles * 3 * WJ * WJ);
     c->ke_slots = alloc_n<double>(c, kMaxSpecies * kEnergySlots);
@@ -451,20 +455,35 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
   const int grid_small = 148 * 4;
   for (int k = 0; k < n; ++k) {
     PushParams p = push_params(c);
-    { ProfScope ps(c, K_PUSH); launch_push_tiles(p, c->ntiles, c->stream); }
-    { ProfScope ps(c, K_INSERT); launch_insert(p, grid_small, c->stream); }
-    { ProfScope ps(c, K_ASSEMBLE); launch_assemble(c->J, c->Jt, c->g, c->T, c->ntx, c->nty, c->stream); }
-    { ProfScope ps(c, K_LOOSE); launch_loose(p, grid_small, c->stream); }
+    // moving window: the host knows in advance that the window shifts at the end of
+    // this step, when (n+1) dt > dx (n_move + 1) — the oracle's test, in the same fp64 arithmetic
+    const int shift = (c->bcx == ZPIC_BC_MOVING_WINDOW && (double)(c->steps + 1) * c->dt > c->dx * (double)(c->n_move + 1)) ? 1 : 0;
+    p.shift = shift;
+    int launches = 0;
+    { ProfScope ps(c, K_PUSH); launch_push_tiles(p, c->ntiles, c->stream); ++launches; }
+    { ProfScope ps(c, K_INSERT); launch_insert(p, grid_small, c->stream); ++launches; }
+    { ProfScope ps(c, K_ASSEMBLE); launch_assemble(c->J, c->Jt, c->g, c->T, c->ntx, c->nty, c->stream); ++launches; }
+    { ProfScope ps(c, K_LOOSE); launch_loose(p, grid_small, c->stream); ++launches; }
     {
       ProfScope ps(c, K_FOLD);
       launch_guard_x(c->J, c->g, c->bcx == ZPIC_BC_PERIODIC ? 0 : 2, 0, c->stream);
       launch_guard_y(c->J, c->g, c->bcy == ZPIC_BC_PERIODIC ? 0 : 2, 0, c->stream);
+      launches += 2;
+    }
+    const float* Jyee = c->J;
+    if (c->opt.filter_passes > 0) {
+      ProfScope ps(c, K_FILTER);
+      launch_filter_x(c->J, c->Jf, c->g, c->opt.filter_passes, c->opt.filter_compensated, c->bcx == ZPIC_BC_PERIODIC,
+                      c->stream);
+      launch_guard_y(c->Jf, c->g, c->bcy == ZPIC_BC_PERIODIC ? 1 : 2, 0, c->stream);
+      launches += 2;
+      Jyee = c->Jf;
     }
     {
       ProfScope ps(c, K_YEE);
       YeeParams y{};
       y.g = c->g;
-      y.E0 = c->E[c->cur]; y.B0 = c->B[c->cur]; y.J = c->J;
+      y.E0 = c->E[c->cur]; y.B0 = c->B[c->cur]; y.J = Jyee;
       y.E1 = c->E[c->cur ^ 1]; y.B1 = c->B[c->cur ^ 1];
       y.dt = (float)c->dt;
       y.dtdx = (float)(c->dt / c->dx); y.dtdy = (float)(c->dt / c->dy);
@@ -472,18 +491,33 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
       y.murx = (float)((c->dt - c->dx) / (c->dt + c->dx));
       y.mury = (float)((c->dt - c->dy) / (c->dt + c->dy));
       y.bcx = c->bcx; y.bcy = c->bcy;
+      y.shift = shift;
       y.fe_slots = c->fe_slots;
       y.fe_scale = 0.5 * c->dx * c->dy;
       launch_yee(y, c->stream);
+      ++launches;
+    }
+    if (shift) {
+      ProfScope ps(c, K_WINDOW);
+      for (int s = 0; s < c->nspecies; ++s) {
+        const zpic_species& sp = c->species[s];
+        if (!(sp.n > 0)) continue;
+        const uint64_t key = host_mix64(host_mix64(c->seed) + (uint64_t)s);
+        launch_inject_column(p, s, sp.ppc[0], sp.ppc[1], (int)c->n_move, c->ny_global, c->y0, key, sp.ufl, sp.uth,
+                             c->stream);
+        ++launches;
+      }
+      c->n_move += 1;
     }
     {
       ProfScope ps(c, K_EPI);
       launch_epilogue(c->ke_slots, c->fe_slots, c->energy, c->nspecies, c->energy + 1 + kMaxSpecies, c->movers.count,
                       p.spill_in.count, p.spill_out.count, c->stats, c->stream);
+      ++launches;
     }
     c->cur ^= 1;
     c->steps += 1;
-    c->launches += 8;
+    c->launches += launches;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { c->last_error = std::string("launch: ") + cudaGetErrorString(e); return ZPIC_E_CUDA; }
@@ -501,7 +535,7 @@ zpic_status zpic_get_fields(zpic_ctx* c, int32_t which, float* out, size_t out_l
   if (st != ZPIC_OK) return st;
   const GridDesc& g = c->g;
   if (out_len < (size_t)3 * g.nx * g.ny) { c->last_error = "get_fields: buffer too small"; return ZPIC_E_BUFSIZE; }
-  const float* F = which == 0 ? c->E[c->cur] : which == 1 ? c->B[c->cur] : (which == 3 && c->Jpre) ? c->Jpre : c->J;
+  const float* F = which == 0 ? c->E[c->cur] : which == 1 ? c->B[c->cur] : (which == 2 && c->Jf) ? c->Jf : c->J;
   for (int k = 0; k < 3; ++k) {
     cudaError_t e = cudaMemcpy2DAsync(out + (size_t)k * g.nx * g.ny, g.nx * 4, F + k * g.plane + g.at(0, 0), g.pitch * 4,
                                       g.nx * 4, g.ny, cudaMemcpyDeviceToHost, c->stream);

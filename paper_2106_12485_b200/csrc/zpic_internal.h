@@ -70,6 +70,7 @@ struct PushParams {
   PList spill_out;  // loose particles for the next step
   float dtdx, dtdy; // dt/dx, dt/dy
   int bcx, bcy;
+  int shift;        // 1 when the moving window shifts at the end of this step (ix -= 1)
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
   int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
 };
@@ -81,6 +82,7 @@ struct YeeParams {
   float dt, dtdx, dtdy, hdx, hdy;   // dt, dt/dx, dt/dy, (dt/2)/dx, (dt/2)/dy
   float murx, mury;                 // Mur-1 coefficients (dt - dx)/(dt + dx), (dt - dy)/(dt + dy)
   int bcx, bcy;
+  int shift;                        // 1: store the result one column toward -x (window shift)
   double* fe_slots;
   double fe_scale;  // dx dy / 2
 };
@@ -117,7 +119,7 @@ struct zpic_ctx {
   float* E[2];
   float* B[2];
   float* J;        // assembled (and folded, filtered) current used by the field advance
-  float* Jpre;     // pre-filter copy (only with a filter)
+  float* Jf;       // filtered current (only with a filter; J keeps the pre-filter values)
   float* Jt;       // per-tile blocks
   zpic::PStore ps[zpic::kMaxSpecies];
   zpic::PList movers, spill[2];
@@ -130,6 +132,7 @@ struct zpic_ctx {
   int64_t steps;
   int64_t repacks;
   int64_t launches;  // kernels enqueued by zpic_step so far
+  int64_t n_move;    // moving-window shifts so far
   std::vector<void*> allocations;
   std::string last_error;
   // profiling

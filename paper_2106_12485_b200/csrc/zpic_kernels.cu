@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kBlock) k_push_loose(PushParams p) {
     Seg seg[3];
     const int nseg = split_path(ix, iy, x, y, dxp, dyp, sc.q * uz * rg, seg, di, dj);
     for (int q = 0; q < nseg; ++q) deposit_seg(A, seg[q], sc.jx, sc.jy);
-    ix += di; iy += dj;
+    ix += di - p.shift; iy += dj;
     if (domain_bc(ix, iy, p.g, p.bcx, p.bcy)) insert_particle(p, s, ix, iy, x, y, ux, uy, uz, id);
   }
   for (int s = 0; s < p.nspecies; ++s) block_add_double((double)ke[s], p.ke_slots + s * kEnergySlots + (blockIdx.x & (kEnergySlots - 1)));
@@ -207,6 +207,9 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   // B^{n+1/2} on [-1, T]^2
   for (int k = threadIdx.x; k < WB * WB; k += kBlock) {
     const int lx = k % WB - 1, ly = k / WB - 1;
+    const int gi = i0 + lx, gj = j0 + ly;
+    if ((p.bcx != ZPIC_BC_PERIODIC && (gi < 0 || gi >= g.nx)) || (p.bcy != ZPIC_BC_PERIODIC && (gj < 0 || gj >= g.ny)))
+      continue;   // B guards of a non-periodic axis stay 0 (only the interior is advanced)
     const float ez = sE[2][EI(lx, ly)];
     sB[0][k] -= p.hdy * (sE[2][EI(lx, ly + 1)] - ez);
     sB[1][k] += p.hdx * (sE[2][EI(lx + 1, ly)] - ez);
@@ -283,7 +286,8 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
     const float by = sB[1][b] + p.hdx * (sE[2][EI(lx + 1, ly)] - ez);
     const float bz = sB[2][b] + p.hdy * (sE[0][EI(lx, ly + 1)] - sE[0][e]) - p.hdx * (sE[1][EI(lx + 1, ly)] - sE[1][e]);
     const float vals[6] = {sE[0][e], sE[1][e], ez, bx, by, bz};
-    const int gi = i0 + lx, gj = j0 + ly;
+    const int gi = i0 + lx - p.shift, gj = j0 + ly;   // window shift: column i is stored at i - 1
+    if (gi < 0) continue;
     int xs[3], ys[3], nxs = 1, nys = 1;
     xs[0] = gi; ys[0] = gj;
     if (p.bcx == ZPIC_BC_PERIODIC) {
@@ -321,9 +325,30 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
       }
     }
   }
+  if (p.shift && xhi) {   // the column entering the window is empty (R14)
+    for (int ly = threadIdx.x; ly <= th; ly += kBlock) {
+      const int gj = j0 + ly;
+      if (ly == th && !(p.bcy == ZPIC_BC_OPEN && yhi)) continue;   // row ny only holds Mur nodes
+      int ys[3], nys = 1;
+      ys[0] = gj;
+      if (p.bcy == ZPIC_BC_PERIODIC) {
+        if (gj <= 1) ys[nys++] = gj + g.ny;
+        if (gj == g.ny - 1) ys[nys++] = -1;
+      }
+      for (int a = 0; a < nys; ++a) {
+        const long o = g.at(g.nx - 1, ys[a]);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          p.E1[c * pl + o] = 0.f;
+          if (ly < th) p.B1[c * pl + o] = 0.f;
+        }
+      }
+    }
+  }
   if (p.bcy == ZPIC_BC_OPEN && yhi) {
     for (int lx = threadIdx.x; lx < tw; lx += kBlock) {
-      const int gi = i0 + lx;
+      const int gi = i0 + lx - p.shift;
+      if (gi < 0 || (p.shift && gi == g.nx - 1)) continue;
       int xs[3], nxs = 1;
       xs[0] = gi;
       if (p.bcx == ZPIC_BC_PERIODIC) {
@@ -419,6 +444,58 @@ __global__ void __launch_bounds__(kBlock) k_inject(InjectParams q) {
   if (threadIdx.x == 0) q.ps.cnt[t] = n;
 }
 
+// Moving window (R15): fresh plasma in the column entering the window, ix = nx-1:
+// the ppc sub-lattice at the species density, u = ufl + uth N with the counter-based generator,
+// ids 2^31 + (n_move ny + iy) ppc + l ppc_x + k.  Inserted straight into the tiles.
+__global__ void k_inject_column(PushParams p, int s, int px, int py, int n_move, int ny_global, int y0, uint64_t key,
+                                double ufl0, double ufl1, double ufl2, double uth0, double uth1, double uth2) {
+  const int ppc = px * py;
+  const int n = p.g.ny * ppc;
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    const int iy = k / ppc, sub = k % ppc, l = sub / px, kk = sub % px;
+    const uint64_t id = 2147483648ull + ((uint64_t)n_move * ny_global + (iy + y0)) * ppc + (uint64_t)l * px + kk;
+    const float x = (float)(((double)kk + 0.5) / px), y = (float)(((double)l + 0.5) / py);
+    insert_particle(p, s, p.g.nx - 1, iy, x, y, thermal(key, id, 0, ufl0, uth0), thermal(key, id, 1, ufl1, uth1),
+                    thermal(key, id, 2, ufl2, uth2), (uint32_t)id);
+  }
+}
+
+// Digital current filter along x (R12), all passes fused: one CTA per
+// (interior row, component) keeps the row in shared memory, applies n passes of (1/4, 1/2, 1/4)
+// and, if compensated, one pass of (-n/4, 1 + n/2, -n/4), refreshing the two guard values before
+// every pass (periodic copy, or zero on a non-periodic x axis), and writes the row and its x
+// guards once.
+__global__ void k_filter_x(const float* __restrict__ Jin, float* __restrict__ Jout, GridDesc g, int npass,
+                           int compensated, int periodic) {
+  extern __shared__ float srow[];
+  float* a = srow;
+  float* b = srow + g.nx + 2;
+  const int j = blockIdx.x % g.ny, c = blockIdx.x / g.ny;
+  const float* in = Jin + c * g.plane;
+  float* out = Jout + c * g.plane;
+  for (int i = threadIdx.x; i < g.nx; i += blockDim.x) a[i + 1] = in[g.at(i, j)];
+  const int total = npass + (compensated && npass > 0 ? 1 : 0);
+  for (int pass = 0; pass < total; ++pass) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      a[0] = periodic ? a[g.nx] : 0.f;
+      a[g.nx + 1] = periodic ? a[1] : 0.f;
+    }
+    __syncthreads();
+    const bool comp = pass == npass;
+    const float side = comp ? -0.25f * npass : 0.25f, centre = comp ? 1.0f + 0.5f * npass : 0.5f;
+    for (int i = threadIdx.x; i < g.nx; i += blockDim.x) b[i + 1] = side * a[i] + centre * a[i + 1] + side * a[i + 2];
+    float* t = a; a = b; b = t;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < g.nx; i += blockDim.x) out[g.at(i, j)] = a[i + 1];
+  if (threadIdx.x == 0) {
+    out[g.at(-1, j)] = periodic ? a[g.nx] : 0.f;
+    out[g.at(g.nx, j)] = periodic ? a[1] : 0.f;
+    out[g.at(g.nx + 1, j)] = periodic ? a[2] : 0.f;
+  }
+}
+
 // Validate host-uploaded particles and count them per tile (err bit 4 = out of the slab).
 __global__ void k_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy,
                         const float* x, const float* y, int* counts, int* err) {
@@ -499,6 +576,22 @@ void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t*
                 cudaStream_t st) {
   const int grid = (int)std::min<long>((n + kBlock - 1) / kBlock, 148L * 32);
   if (grid > 0) k_bin<<<grid, kBlock, 0, st>>>(ps, T, ntx, y0, n, ix, iy, x, y, ux, uy, uz, id, err);
+}
+void launch_inject_column(const PushParams& p, int s, int px, int py, int n_move, int ny_global, int y0, uint64_t key,
+                          const double* ufl, const double* uth, cudaStream_t st) {
+  const int n = p.g.ny * px * py;
+  k_inject_column<<<(n + kBlock - 1) / kBlock, kBlock, 0, st>>>(p, s, px, py, n_move, ny_global, y0, key, ufl[0], ufl[1],
+                                                                ufl[2], uth[0], uth[1], uth[2]);
+}
+void launch_filter_x(const float* Jin, float* Jout, const GridDesc& g, int npass, int compensated, int periodic,
+                     cudaStream_t st) {
+  const size_t smem = 2 * (size_t)(g.nx + 2) * sizeof(float);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(k_filter_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  k_filter_x<<<3 * g.ny, kBlock, smem, st>>>(Jin, Jout, g, npass, compensated, periodic);
 }
 void launch_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
                   const float* y, int* counts, int* err, cudaStream_t st) {

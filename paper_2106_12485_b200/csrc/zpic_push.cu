@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
         int di, dj;
         nseg = split_path(lx, ly, x, y, dxp, dyp, qs * uz * rg, seg, di, dj);
         deposit_seg(A, seg[0], jxs, jys);
+        di -= p.shift;   // moving window: the cell index follows the shift at the end of the step
         ix += di; iy += dj;
         if ((unsigned)(lx + di) < (unsigned)tw && (unsigned)(ly + dj) < (unsigned)th) stay = true;
         else move = domain_bc(ix, iy, p.g, p.bcx, p.bcy);

@@ -122,7 +122,10 @@ def ramp_species(cfg, s):
     X = np.concatenate([Xr, Xu])            # one x sub-row of particles (physical x)
     gx = X / dx
     ixr = np.floor(gx).astype(np.int64)
-    xr = gx - ixr
+    xr = (gx - ixr).astype(np.float32)
+    up = xr >= np.float32(1.0)          # an offset that rounds to 1 in fp32 starts the next cell (R6)
+    ixr[up] += 1
+    xr[up] = 0.0
     n_row = len(X)
     rows = np.arange(ny * py, dtype=np.int64)          # y sub-rows: iy = r // py, l = r % py
     iy = np.repeat(rows // py, n_row)

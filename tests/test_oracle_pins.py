@@ -504,6 +504,30 @@ def test_mur_absorbs_normal_pulse():
 
 
 # ---------------------------------------------------------------------------------------
+# P11 moving window
+def test_window_shift_composition_injection_and_exit():
+    nx, ny = 12, 5
+    rng = np.random.default_rng(16)
+    A = rng.normal(size=(3, ny, nx))
+    sp = [dict(m_q=-1.0, n=1.0, ppc=(2, 2), ufl=(0, 0, 0), uth=(0, 0, 0), ix=np.array([0, 5], np.int32),
+               iy=np.array([1, 2], np.int32), x=np.array([0.5, 0.5]), y=np.array([0.5, 0.5]), ux=np.zeros(2),
+               uy=np.zeros(2), uz=np.zeros(2), id=np.array([0, 1]))]
+    sim = OracleSim(nx, ny, 0.1, 0.1, 0.05, sp, bc=(2, 1), E=A, B=A)
+    sim._shift_window()
+    sim._shift_window()
+    # two single shifts == one double shift: F'[i] = F[i+2], two fresh zero columns
+    want = np.concatenate([A[:, :, 2:], np.zeros((3, ny, 2))], axis=2)
+    assert np.array_equal(sim.fields(0), want) and np.array_equal(sim.fields(1), want)
+    s = sim.species[0]
+    for_ = [k for k in range(len(s["id"])) if s["id"][k] >= 2 ** 31]
+    assert len(for_) == 2 * ny * 4                    # ppc * ny per shift
+    assert len(set(s["id"][for_].tolist())) == len(for_)
+    sim._particle_bc(s, window_now=True)             # the particle at ix = 0 left (ix = -2)
+    assert 0 not in s["id"] and 1 in s["id"]
+    assert s["ix"][list(s["id"]).index(1)] == 3
+
+
+# ---------------------------------------------------------------------------------------
 # P13 init (shared synth inputs) and energy conventions
 def test_injection_counts_cold_and_determinism():
     import synth

@@ -105,10 +105,79 @@ def test_c3_open_x_clouds_reduced():
     print(rep)
 
 
+def c4_reduced(nx=400, ny=64):
+    """configs[3] physics on a smaller box: same dx, dy, dt, ppc, a0, omega0, fwhm, W0, filter and
+    boundaries; the ramp starts at x = 2.0 (20 cells) and the laser's leading edge is Lx - 2."""
+    cfg = synth.config("C4", nx=nx, ny=ny)
+    cfg["species"][0].update(x0=2.0, x1=2.0 + 20 * cfg["dx"])
+    cfg["laser"] = dict(cfg["laser"], start=nx * cfg["dx"] - 2.0)
+    return cfg
+
+
+def _gpu_c4(cfg, parts):
+    g = gpu_from_particles(cfg, parts)
+    E, B = synth.laser_fields(cfg)
+    g.set_fields(0, E)
+    g.set_fields(1, B)
+    return g
+
+
+def test_c4_lwfa_window_filter_reduced():
+    """Moving window (shift + injection), compensated 4-pass filter, laser initial fields, density
+    ramp and absorbing y edges, against the oracle: particles after 1 and 10 steps, fields after
+    10 steps, energies over 30 steps (the window shifts on 28 of them)."""
+    cfg = c4_reduced()
+    parts = [synth.species_particles(cfg, 0)]
+    g = _gpu_c4(cfg, parts)
+    o = from_config(cfg, particles=parts)
+    nx, ny = cfg["nx"], cfg["ny"]
+    fe_g, fe_o, ke_g, ke_o = [], [], [], []
+    for n in range(30):
+        g.step(1)
+        o.step()
+        it, fe, ke = g.energy()
+        fe_g.append(fe); ke_g.append(ke[0])
+        fe_o.append(o.fe[-1]); ke_o.append(o.ke[-1][0])
+        if n in (0, 9, 29):
+            c = compare_particles(g.particles(0, True), oracle_particles(o, 0), nx, ny, (False, False))
+            if n == 0:
+                assert c["pos_max"] <= POS_TOL and c["mom_max"] <= MOM_TOL, c
+            assert c["cell_exact_frac"] >= CELL_FRAC, c
+        if n == 9:
+            for w in (0, 1):
+                assert rel_l2(g.fields(w), o.fields(w)) <= FIELD_TOL, (w, rel_l2(g.fields(w), o.fields(w)))
+            assert rel_l2(g.fields(3), o.fields(3)) <= 1e-3
+            assert rel_l2(g.fields(2), o.fields(2)) <= 1e-3
+    assert o.n_move == 28
+    assert energy_agreement(fe_g, fe_o) <= ENERGY_TOL
+    assert energy_agreement(ke_g, ke_o) <= ENERGY_TOL
+    assert g.counters()["particles"] == len(o.species[0]["ix"])
+    g.close()
+
+
+def test_window_injection_ids_and_counts():
+    """Each shift injects ppc * ny particles per species at ix = nx - 1 with
+    the oracle's ids; particles leaving x < 0 are removed."""
+    cfg = c4_reduced(nx=160, ny=16)
+    cfg["laser"] = dict(cfg["laser"], a0=0.0)
+    parts = [synth.species_particles(cfg, 0)]
+    g = _gpu_c4(cfg, parts)
+    o = from_config(cfg, particles=parts)
+    for n in range(12):
+        g.step(1)
+        o.step()
+    gp = g.particles(0, True)
+    assert len(gp["ix"]) == len(o.species[0]["ix"])
+    assert np.array_equal(np.sort(gp["id"].astype(np.int64)), np.sort(o.species[0]["id"]))
+    inj = gp["id"] >= 2 ** 31
+    assert np.count_nonzero(inj) == o.n_move * 16 * 4
+    g.close()
+
+
 def test_mur_vacuum_matches_oracle():
     """Open x and open y edges with an initial random field and a pulse: the GPU's Mur-1
     boundary nodes follow the oracle (R13)."""
-    for bc in ((1, 0), (0, 1), (1, 1)):
+    for bc in ((1, 0), (0, 1), (1, 1), (2, 1), (2, 0)):
         cfg = synth.config("C1", nx=48, ny=40)
         cfg["bc"] = bc
         rng = np.random.default_rng(5)
