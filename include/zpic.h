@@ -106,11 +106,23 @@ typedef struct {
   void* alloc_user;
 } zpic_options;
 
-/* Multi-GPU y-slab decomposition (nullable = 1 GPU). */
+/* y-slab decomposition (the paper's row-band regions).
+ * Rank r owns rows [r*ny/world, (r+1)*ny/world) with all nx columns; ny % world == 0 and at
+ * least 2 rows per slab.  Every step exchanges, with the y neighbours only: (1) raw current
+ * guard rows + migrating particles, (2) E/B ghost rows.  Transports:
+ *   ZPIC_TRANSPORT_NCCL: one process per GPU; nccl_comm is an ncclComm_t (e.g. torch's
+ *     ProcessGroupNCCL._comm_ptr()), or NULL with nccl_id = the 128-byte ncclUniqueId from
+ *     zpic_nccl_unique_id() on rank 0, broadcast by the caller (the library then owns a comm);
+ *   ZPIC_TRANSPORT_LOOPBACK: `world` contexts in one process on one device and one stream,
+ *     stepped together with zpic_step_group (validation of the slab logic on one GPU).
+ * Pass NULL for the unsplit single-GPU domain. */
+typedef enum { ZPIC_TRANSPORT_NCCL = 0, ZPIC_TRANSPORT_LOOPBACK = 1 } zpic_transport;
 typedef struct {
   int32_t rank, world;
-  void* nccl_comm; /* ncclComm_t shared with torch's ProcessGroupNCCL */
+  void* nccl_comm;
   int32_t device;
+  const void* nccl_id;      /* 128 bytes, used when nccl_comm == NULL */
+  zpic_transport transport;
 } zpic_dist;
 
 typedef struct zpic_ctx zpic_ctx;
@@ -130,8 +142,16 @@ zpic_status zpic_set_particles(zpic_ctx* ctx, int32_t species, int64_t n, const 
 /* Overwrite E (which=0) or B (which=1) interior values from host [comp][y][x] (laser init). */
 zpic_status zpic_set_fields(zpic_ctx* ctx, int32_t which, const float* in, size_t in_len);
 
-/* Enqueue n time steps (asynchronous w.r.t. the host). */
+/* Enqueue n time steps (asynchronous w.r.t. the host).  With NCCL slabs every rank must call it
+ * with the same n (the halo exchanges are collective between neighbours). */
 zpic_status zpic_step(zpic_ctx* ctx, int32_t n);
+
+/* Step `count` loopback slab contexts (ranks 0..count-1 of one decomposition, same device and
+ * stream) together for n steps.  ZPIC_E_STATE if they are not one complete loopback group. */
+zpic_status zpic_step_group(zpic_ctx** ctxs, int32_t count, int32_t n);
+
+/* Write a fresh ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128 bytes) to out (out_len >= 128). */
+zpic_status zpic_nccl_unique_id(void* out, size_t out_len);
 
 /* Block until all enqueued work is done; surface sticky device errors. */
 zpic_status zpic_sync(zpic_ctx* ctx);
@@ -148,7 +168,8 @@ zpic_status zpic_get_particles(zpic_ctx* ctx, int32_t species, int64_t* count_in
 
 /* Energies of the input state of the last step taken (time level iter = steps-1):
  * field = 1/2 dx dy sum(E^2 + B^2), kinetic[s] = q_s m_q,s dx dy sum(gamma - 1) (R8).
- * Before any step: iter = -1 and zeros. */
+ * Before any step: iter = -1 and zeros.  NCCL slabs: summed over all ranks (collective: every
+ * rank must call it); loopback slabs: this slab only. */
 zpic_status zpic_energy(zpic_ctx* ctx, int64_t* iter, double* field, double* kinetic);
 
 /* Local slab rows [y0, y0 + ny_local). */

@@ -16,6 +16,18 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-O2", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
 
 
+def _nccl_dirs():
+    """torch's bundled NCCL (the library must share the communicator type and the loaded .so)."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia.nccl") or importlib.util.find_spec("nvidia")
+    roots = list(spec.submodule_search_locations or []) if spec else []
+    for r in roots:
+        base = r if r.endswith("nccl") else os.path.join(r, "nccl")
+        if os.path.exists(os.path.join(base, "include", "nccl.h")):
+            return os.path.join(base, "include"), os.path.join(base, "lib")
+    raise RuntimeError("nccl.h not found (expected torch's nvidia/nccl package)")
+
+
 def _stale():
     if not os.path.exists(SO):
         return True
@@ -27,10 +39,11 @@ def _stale():
 def build(force=False, verbose=False):
     if not force and not _stale():
         return SO
+    nccl_inc, nccl_lib = _nccl_dirs()
     objs = []
     for src in SOURCES:
         obj = os.path.join(CSRC, src.replace(".cu", ".o"))
-        cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC] + FLAGS + ["-I", nccl_inc, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or r.returncode:
             sys.stderr.write(r.stdout + r.stderr)
@@ -38,7 +51,8 @@ def build(force=False, verbose=False):
             raise RuntimeError("nvcc failed for " + src)
         objs.append(obj)
     tmp = SO + ".tmp%d" % os.getpid()
-    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs + ["-lcudart"]
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs + [
+        "-lcudart", "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + nccl_lib]
     subprocess.check_call(cmd)
     os.replace(tmp, SO)
     for o in objs:

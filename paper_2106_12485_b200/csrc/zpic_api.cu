@@ -2,6 +2,7 @@
 // sequence, exports, energies, profiling.  No compute happens on the host:
 // every stage of the step is one of the kernels in zpic_kernels.cu.
 #include <cuda_runtime.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -34,6 +35,11 @@ void launch_inject_column(const PushParams& p, int s, int px, int py, int n_move
                           const double* ufl, const double* uth, cudaStream_t st);
 void launch_filter_x(const float* Jin, float* Jout, const GridDesc& g, int npass, int compensated, int periodic,
                      cudaStream_t st);
+void launch_apply_j_halo(float* J, const GridDesc& g, const float* rup, const float* rdn, int has_lo, int has_hi,
+                         cudaStream_t st);
+size_t particle_msg_bytes(int cap);
+PList particle_msg_list(void* buf, int cap);
+void launch_recv_insert(const PushParams& p, const PList& lo, const PList& hi, cudaStream_t st);
 }  // namespace zpic
 
 using namespace zpic;
@@ -145,13 +151,21 @@ void refresh_field_guards(zpic_ctx* c, float* F, bool is_E) {
   const int kx = (is_E && c->bcx == ZPIC_BC_OPEN) ? 0b110 : 0;  // Ey, Ez keep node nx
   const int ky = (is_E && c->bcy == ZPIC_BC_OPEN) ? 0b101 : 0;  // Ex, Ez keep node ny
   launch_guard_x(F, c->g, kx ? 3 : field_guard_mode(c->bcx), kx, c->stream);
-  launch_guard_y(F, c->g, ky ? 3 : field_guard_mode(c->bcy), ky, c->stream);
+  if (c->slab) {
+    // slab interfaces get their guard rows from the neighbours before the next step
+    if (c->bcy != ZPIC_BC_PERIODIC) launch_guard_y(F, c->g, ky ? 3 : 2, ky, c->stream);
+    c->halo_dirty = true;
+  } else {
+    launch_guard_y(F, c->g, ky ? 3 : field_guard_mode(c->bcy), ky, c->stream);
+  }
 }
 
 // ---- profiling ---------------------------------------------------------------------------
-enum KId { K_PUSH = 0, K_INSERT, K_ASSEMBLE, K_LOOSE, K_FOLD, K_FILTER, K_YEE, K_WINDOW, K_EPI, K_COUNT };
-const char* kNames[K_COUNT] = {"k_push_tiles", "k_insert", "k_assemble_j", "k_push_loose", "k_guard_fold",
-                               "k_filter_x", "k_yee", "k_inject_column", "k_epilogue"};
+enum KId { K_PUSH = 0, K_INSERT, K_ASSEMBLE, K_LOOSE, K_FOLD, K_HALO, K_FILTER, K_YEE, K_WINDOW, K_EPI, K_EXCHANGE,
+           K_COUNT };
+const char* kNames[K_COUNT] = {"k_push_tiles", "k_insert",        "k_assemble_j", "k_push_loose",
+                               "k_guard_fold", "k_apply_halo",    "k_filter_x",   "k_yee",
+                               "k_inject_column", "k_epilogue",   "halo_exchange"};
 
 struct ProfScope {
   zpic_ctx* c;
@@ -203,7 +217,111 @@ PushParams push_params(zpic_ctx* c) {
   p.bcx = c->bcx; p.bcy = c->bcy;
   p.ke_slots = c->ke_slots;
   p.err = c->err;
+  p.slab = c->slab;
+  p.has_lo = c->has_lo;
+  p.has_hi = c->has_hi;
+  if (c->slab) {
+    p.send[0] = particle_msg_list(c->pmsg_send[0], c->pcap);
+    p.send[1] = particle_msg_list(c->pmsg_send[1], c->pcap);
+  }
   return p;
+}
+
+// ---- y-slab halo exchange (§8(e)) ----------------------------------------------------------
+// Message order per neighbour pair is fixed so that ring sizes 1 and 2 (where the lower and
+// the upper neighbour are the same rank) match sends with receives: first everything that
+// travels up (+y), then everything that travels down (-y).
+float* jrow(zpic_ctx* c, int comp, int row) { return c->J + comp * c->g.plane + (long)(row + 1) * c->g.pitch; }
+float* frow(float* F, const GridDesc& g, int comp, int row) { return F + comp * g.plane + (long)(row + 1) * g.pitch; }
+
+ncclResult_t nccl_exchange_round1(zpic_ctx* c) {
+  ncclComm_t comm = (ncclComm_t)c->comm;
+  const size_t rows2 = 2 * (size_t)c->g.pitch;
+  const size_t mb = particle_msg_bytes(c->pcap);
+  ncclResult_t r = ncclGroupStart();
+  if (c->has_hi) {   // up: my raw J rows ny, ny+1 and my up-going particles
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(jrow(c, k, c->g.ny), rows2, ncclFloat, c->upper, comm, c->stream);
+    if (r == ncclSuccess) r = ncclSend(c->pmsg_send[1], mb, ncclChar, c->upper, comm, c->stream);
+  }
+  if (c->has_lo && r == ncclSuccess) {   // from below: the lower's rows ny, ny+1 and its up-going particles
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(c->jrdn + k * rows2, rows2, ncclFloat, c->lower, comm, c->stream);
+    if (r == ncclSuccess) r = ncclRecv(c->pmsg_recv[0], mb, ncclChar, c->lower, comm, c->stream);
+  }
+  if (c->has_lo && r == ncclSuccess) {   // down: my raw J rows -1, 0 and my down-going particles
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(jrow(c, k, -1), rows2, ncclFloat, c->lower, comm, c->stream);
+    if (r == ncclSuccess) r = ncclSend(c->pmsg_send[0], mb, ncclChar, c->lower, comm, c->stream);
+  }
+  if (c->has_hi && r == ncclSuccess) {   // from above: the upper's rows -1, 0 and its down-going particles
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(c->jrup + k * rows2, rows2, ncclFloat, c->upper, comm, c->stream);
+    if (r == ncclSuccess) r = ncclRecv(c->pmsg_recv[1], mb, ncclChar, c->upper, comm, c->stream);
+  }
+  ncclResult_t e = ncclGroupEnd();
+  return r != ncclSuccess ? r : e;
+}
+
+// Round 2: E, B ghost rows of buffer `b`: my row ny-1 -> the upper's guard row -1 (up); my rows
+// 0, 1 -> the lower's guard rows ny, ny+1 (down).
+ncclResult_t nccl_exchange_round2(zpic_ctx* c, int b) {
+  ncclComm_t comm = (ncclComm_t)c->comm;
+  const GridDesc& g = c->g;
+  const size_t row = g.pitch;
+  float* F[2] = {c->E[b], c->B[b]};
+  ncclResult_t r = ncclGroupStart();
+  for (int f = 0; f < 2 && c->has_hi && r == ncclSuccess; ++f)
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(frow(F[f], g, k, g.ny - 1), row, ncclFloat, c->upper, comm, c->stream);
+  for (int f = 0; f < 2 && c->has_lo && r == ncclSuccess; ++f)
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(frow(F[f], g, k, -1), row, ncclFloat, c->lower, comm, c->stream);
+  for (int f = 0; f < 2 && c->has_lo && r == ncclSuccess; ++f)
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(frow(F[f], g, k, 0), 2 * row, ncclFloat, c->lower, comm, c->stream);
+  for (int f = 0; f < 2 && c->has_hi && r == ncclSuccess; ++f)
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(frow(F[f], g, k, g.ny), 2 * row, ncclFloat, c->upper, comm, c->stream);
+  ncclResult_t e = ncclGroupEnd();
+  return r != ncclSuccess ? r : e;
+}
+
+// Loopback versions (all contexts of a group share one device and one stream).
+void loop_exchange_round1(zpic_ctx** cs, int n) {
+  for (int r = 0; r < n; ++r) {
+    zpic_ctx* c = cs[r];
+    const size_t rows2b = 2 * (size_t)c->g.pitch * sizeof(float);
+    const size_t mb = particle_msg_bytes(c->pcap);
+    if (c->has_lo) {
+      zpic_ctx* lo = cs[c->lower];
+      CUDA_OR_THROW(cudaMemcpy2DAsync(c->jrdn, rows2b, jrow(lo, 0, lo->g.ny), lo->g.plane * sizeof(float), rows2b, 3,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(c->pmsg_recv[0], lo->pmsg_send[1], mb, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    if (c->has_hi) {
+      zpic_ctx* up = cs[c->upper];
+      CUDA_OR_THROW(cudaMemcpy2DAsync(c->jrup, rows2b, jrow(up, 0, -1), up->g.plane * sizeof(float), rows2b, 3,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(c->pmsg_recv[1], up->pmsg_send[0], mb, cudaMemcpyDeviceToDevice, c->stream));
+    }
+  }
+}
+
+void loop_exchange_round2(zpic_ctx** cs, int n, int b) {
+  for (int r = 0; r < n; ++r) {
+    zpic_ctx* c = cs[r];
+    const GridDesc& g = c->g;
+    const size_t rowb = (size_t)g.pitch * sizeof(float);
+    for (int f = 0; f < 2; ++f) {
+      if (c->has_lo) {
+        zpic_ctx* lo = cs[c->lower];
+        float* src = f ? lo->B[b] : lo->E[b];
+        float* dst = f ? c->B[b] : c->E[b];
+        CUDA_OR_THROW(cudaMemcpy2DAsync(frow(dst, g, 0, -1), g.plane * sizeof(float), frow(src, g, 0, g.ny - 1),
+                                        g.plane * sizeof(float), rowb, 3, cudaMemcpyDeviceToDevice, c->stream));
+      }
+      if (c->has_hi) {
+        zpic_ctx* up = cs[c->upper];
+        float* src = f ? up->B[b] : up->E[b];
+        float* dst = f ? c->B[b] : c->E[b];
+        CUDA_OR_THROW(cudaMemcpy2DAsync(frow(dst, g, 0, g.ny), g.plane * sizeof(float), frow(src, g, 0, 0),
+                                        g.plane * sizeof(float), 2 * rowb, 3, cudaMemcpyDeviceToDevice, c->stream));
+      }
+    }
+  }
 }
 
 zpic_status check_sticky(zpic_ctx* c) {
@@ -243,11 +361,15 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       if (sp.uth[k] < 0) { g_init_error = "species " + std::to_string(s) + ": uth >= 0"; return ZPIC_E_INVALID; }
   }
   if (bc->y == ZPIC_BC_MOVING_WINDOW) { g_init_error = "moving window is x only"; return ZPIC_E_INVALID; }
-  int world = 1, rank = 0;
-  if (dist && dist->world > 1) {
-    g_init_error = "multi-GPU slabs not supported yet"; return ZPIC_E_DECOMP;
+  if (dist) {
+    if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world) { g_init_error = "bad rank / world"; return ZPIC_E_DECOMP; }
+    if (grid->ny % dist->world != 0 || grid->ny / dist->world < 2) {
+      g_init_error = "ny must be a multiple of world with >= 2 rows per slab"; return ZPIC_E_DECOMP;
+    }
+    if (dist->transport == ZPIC_TRANSPORT_NCCL && !dist->nccl_comm && !dist->nccl_id) {
+      g_init_error = "NCCL transport needs nccl_comm or nccl_id"; return ZPIC_E_DECOMP;
+    }
   }
-  (void)rank; (void)world;
 
   zpic_ctx* c = new zpic_ctx();
   try {
@@ -268,15 +390,24 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     c->prof = c->opt.profile != 0;
     c->prof_ms.assign(K_COUNT, 0.0);
     c->prof_count.assign(K_COUNT, 0);
-    if (dist) c->dist = *dist; else c->dist = zpic_dist{0, 1, nullptr, 0};
-    c->nx_global = grid->nx; c->ny_global = grid->ny; c->y0 = 0;
+    if (dist) c->dist = *dist; else c->dist = zpic_dist{0, 1, nullptr, 0, nullptr, ZPIC_TRANSPORT_NCCL};
+    c->nx_global = grid->nx; c->ny_global = grid->ny;
+    c->slab = dist != nullptr;
+    c->rank = c->dist.rank; c->world = c->dist.world;
+    c->transport = c->dist.transport;
+    c->lower = (c->rank + c->world - 1) % c->world;
+    c->upper = (c->rank + 1) % c->world;
+    c->has_lo = bc->y == ZPIC_BC_PERIODIC || c->rank > 0;
+    c->has_hi = bc->y == ZPIC_BC_PERIODIC || c->rank < c->world - 1;
+    const int ny_local = grid->ny / c->world;
+    c->y0 = c->rank * ny_local;
     c->dx = grid->dx; c->dy = grid->dy; c->dt = dt;
     c->bcx = bc->x; c->bcy = bc->y;
     c->nspecies = n_species;
     c->seed = seed;
     for (int s = 0; s < n_species; ++s) c->species[s] = species[s];
     GridDesc& g = c->g;
-    g.nx = grid->nx; g.ny = grid->ny;
+    g.nx = grid->nx; g.ny = ny_local;
     g.pitch = round_up(g.nx + kXOff + 2, 32);
     g.rows = g.ny + 3;
     g.plane = (long)g.rows * g.pitch;
@@ -348,6 +479,33 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     c->spill[1] = alloc_list(c, (int)mcap);
     c->cur = 0;
     c->steps = 0;
+    if (c->slab) {
+      // halo buffers: raw J rows from both neighbours; particle messages sized for two rows of
+      // cells at 2x the densest species sum (a particle crosses at most one row per step)
+      c->jrup = alloc_n<float>(c, (size_t)3 * 2 * g.pitch);
+      c->jrdn = alloc_n<float>(c, (size_t)3 * 2 * g.pitch);
+      int ppc_sum = 0;
+      for (int s = 0; s < n_species; ++s) ppc_sum += species[s].ppc[0] * species[s].ppc[1];
+      c->pcap = std::max(4096, round_up(4 * g.nx * std::max(ppc_sum, 1), 32));
+      for (int d = 0; d < 2; ++d) {
+        c->pmsg_send[d] = alloc_n<char>(c, particle_msg_bytes(c->pcap));
+        c->pmsg_recv[d] = alloc_n<char>(c, particle_msg_bytes(c->pcap));
+      }
+      if (c->transport == ZPIC_TRANSPORT_NCCL) {
+        if (c->dist.nccl_comm) {
+          c->comm = c->dist.nccl_comm;
+          c->own_comm = false;
+        } else {
+          ncclUniqueId id;
+          std::memcpy(&id, c->dist.nccl_id, sizeof(id));
+          ncclComm_t comm;
+          ncclResult_t r = ncclCommInitRank(&comm, c->world, id, c->rank);
+          if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)};
+          c->comm = comm;
+          c->own_comm = true;
+        }
+      }
+    }
     CUDA_OR_THROW(cudaGetLastError());
     CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
   } catch (const Fail& f) {
@@ -450,37 +608,67 @@ zpic_status zpic_set_fields(zpic_ctx* c, int32_t which, const float* in, size_t 
   return check_sticky(c);
 }
 
-zpic_status zpic_step(zpic_ctx* c, int32_t n) {
-  if (!c || n < 0) return ZPIC_E_INVALID;
+// ---- the step, in phases --------------------------------------------------
+// phase A: particles (K1, K3, K4, K1L) and the x ghost-current fold (+ the y fold on one slab)
+// [exchange round 1: raw J rows + migrating particles]
+// phase B: slab J halo + received particles, filter, Yee
+// [exchange round 2: E, B ghost rows]
+// phase C: window injection, energies, bookkeeping
+struct StepState {
+  PushParams p;
+  int shift;
+  int launches;
+};
+
+StepState step_phase_a(zpic_ctx* c) {
+  StepState s{};
+  s.p = push_params(c);
+  // moving window: the host knows in advance that the window shifts at the end of
+  // this step, when (n+1) dt > dx (n_move + 1) — the oracle's test, in the same fp64 arithmetic
+  s.shift = (c->bcx == ZPIC_BC_MOVING_WINDOW && (double)(c->steps + 1) * c->dt > c->dx * (double)(c->n_move + 1)) ? 1 : 0;
+  s.p.shift = s.shift;
   const int grid_small = 148 * 4;
-  for (int k = 0; k < n; ++k) {
-    PushParams p = push_params(c);
-    // moving window: the host knows in advance that the window shifts at the end of
-    // this step, when (n+1) dt > dx (n_move + 1) — the oracle's test, in the same fp64 arithmetic
-    const int shift = (c->bcx == ZPIC_BC_MOVING_WINDOW && (double)(c->steps + 1) * c->dt > c->dx * (double)(c->n_move + 1)) ? 1 : 0;
-    p.shift = shift;
-    int launches = 0;
-    { ProfScope ps(c, K_PUSH); launch_push_tiles(p, c->ntiles, c->stream); ++launches; }
-    { ProfScope ps(c, K_INSERT); launch_insert(p, grid_small, c->stream); ++launches; }
-    { ProfScope ps(c, K_ASSEMBLE); launch_assemble(c->J, c->Jt, c->g, c->T, c->ntx, c->nty, c->stream); ++launches; }
-    { ProfScope ps(c, K_LOOSE); launch_loose(p, grid_small, c->stream); ++launches; }
-    {
-      ProfScope ps(c, K_FOLD);
-      launch_guard_x(c->J, c->g, c->bcx == ZPIC_BC_PERIODIC ? 0 : 2, 0, c->stream);
+  const PushParams& p = s.p;
+  { ProfScope ps(c, K_PUSH); launch_push_tiles(p, c->ntiles, c->stream); ++s.launches; }
+  { ProfScope ps(c, K_INSERT); launch_insert(p, grid_small, c->stream); ++s.launches; }
+  { ProfScope ps(c, K_ASSEMBLE); launch_assemble(c->J, c->Jt, c->g, c->T, c->ntx, c->nty, c->stream); ++s.launches; }
+  { ProfScope ps(c, K_LOOSE); launch_loose(p, grid_small, c->stream); ++s.launches; }
+  {
+    ProfScope ps(c, K_FOLD);
+    launch_guard_x(c->J, c->g, c->bcx == ZPIC_BC_PERIODIC ? 0 : 2, 0, c->stream);
+    ++s.launches;
+    if (!c->slab) {
       launch_guard_y(c->J, c->g, c->bcy == ZPIC_BC_PERIODIC ? 0 : 2, 0, c->stream);
-      launches += 2;
+      ++s.launches;
     }
-    const float* Jyee = c->J;
-    if (c->opt.filter_passes > 0) {
-      ProfScope ps(c, K_FILTER);
-      launch_filter_x(c->J, c->Jf, c->g, c->opt.filter_passes, c->opt.filter_compensated, c->bcx == ZPIC_BC_PERIODIC,
-                      c->stream);
+  }
+  return s;
+}
+
+void step_phase_b(zpic_ctx* c, StepState& s) {
+  if (c->slab) {
+    ProfScope ps(c, K_HALO);
+    launch_apply_j_halo(c->J, c->g, c->jrup, c->jrdn, c->has_lo, c->has_hi, c->stream);
+    launch_recv_insert(s.p, particle_msg_list(c->pmsg_recv[0], c->pcap), particle_msg_list(c->pmsg_recv[1], c->pcap),
+                       c->stream);
+    s.launches += 2;
+  }
+  const float* Jyee = c->J;
+  if (c->opt.filter_passes > 0) {
+    ProfScope ps(c, K_FILTER);
+    GridDesc gf = c->g;
+    if (c->slab) gf.ny += 1;   // also the guard row ny (the neighbour's final row 0), used by the Yee kernel
+    launch_filter_x(c->J, c->Jf, gf, c->opt.filter_passes, c->opt.filter_compensated, c->bcx == ZPIC_BC_PERIODIC,
+                    c->stream);
+    ++s.launches;
+    if (!c->slab) {
       launch_guard_y(c->Jf, c->g, c->bcy == ZPIC_BC_PERIODIC ? 1 : 2, 0, c->stream);
-      launches += 2;
-      Jyee = c->Jf;
+      ++s.launches;
     }
-    {
-      ProfScope ps(c, K_YEE);
+    Jyee = c->Jf;
+  }
+  {
+    ProfScope ps(c, K_YEE);
       YeeParams y{};
       y.g = c->g;
       y.E0 = c->E[c->cur]; y.B0 = c->B[c->cur]; y.J = Jyee;
@@ -491,36 +679,120 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
       y.murx = (float)((c->dt - c->dx) / (c->dt + c->dx));
       y.mury = (float)((c->dt - c->dy) / (c->dt + c->dy));
       y.bcx = c->bcx; y.bcy = c->bcy;
-      y.shift = shift;
+      y.shift = s.shift;
+      y.y_images = !c->slab && c->bcy == ZPIC_BC_PERIODIC;
+      y.ylo_edge = !c->slab || !c->has_lo;
+      y.yhi_edge = !c->slab || !c->has_hi;
       y.fe_slots = c->fe_slots;
       y.fe_scale = 0.5 * c->dx * c->dy;
       launch_yee(y, c->stream);
-      ++launches;
-    }
-    if (shift) {
-      ProfScope ps(c, K_WINDOW);
-      for (int s = 0; s < c->nspecies; ++s) {
-        const zpic_species& sp = c->species[s];
-        if (!(sp.n > 0)) continue;
-        const uint64_t key = host_mix64(host_mix64(c->seed) + (uint64_t)s);
-        launch_inject_column(p, s, sp.ppc[0], sp.ppc[1], (int)c->n_move, c->ny_global, c->y0, key, sp.ufl, sp.uth,
-                             c->stream);
-        ++launches;
-      }
-      c->n_move += 1;
-    }
-    {
-      ProfScope ps(c, K_EPI);
-      launch_epilogue(c->ke_slots, c->fe_slots, c->energy, c->nspecies, c->energy + 1 + kMaxSpecies, c->movers.count,
-                      p.spill_in.count, p.spill_out.count, c->stats, c->stream);
-      ++launches;
-    }
-    c->cur ^= 1;
-    c->steps += 1;
-    c->launches += launches;
+      ++s.launches;
   }
+}
+
+void step_phase_c(zpic_ctx* c, StepState& s) {
+  if (s.shift) {
+    ProfScope ps(c, K_WINDOW);
+    for (int q = 0; q < c->nspecies; ++q) {
+      const zpic_species& sp = c->species[q];
+      if (!(sp.n > 0)) continue;
+      const uint64_t key = host_mix64(host_mix64(c->seed) + (uint64_t)q);
+      launch_inject_column(s.p, q, sp.ppc[0], sp.ppc[1], (int)c->n_move, c->ny_global, c->y0, key, sp.ufl, sp.uth,
+                           c->stream);
+      ++s.launches;
+    }
+    c->n_move += 1;
+  }
+  {
+    ProfScope ps(c, K_EPI);
+    launch_epilogue(c->ke_slots, c->fe_slots, c->energy, c->nspecies, c->energy + 1 + kMaxSpecies, c->movers.count,
+                    s.p.spill_in.count, s.p.spill_out.count, c->stats, c->stream);
+    ++s.launches;
+    if (c->slab) {
+      for (int d = 0; d < 2; ++d) CUDA_OR_THROW(cudaMemsetAsync(c->pmsg_send[d], 0, 4, c->stream));
+    }
+  }
+  c->cur ^= 1;
+  c->steps += 1;
+  c->launches += s.launches;
+}
+
+zpic_status step_error(zpic_ctx* c) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) { c->last_error = std::string("launch: ") + cudaGetErrorString(e); return ZPIC_E_CUDA; }
+  return ZPIC_OK;
+}
+
+zpic_status zpic_step(zpic_ctx* c, int32_t n) {
+  if (!c || n < 0) return ZPIC_E_INVALID;
+  if (c->slab && c->transport != ZPIC_TRANSPORT_NCCL) {
+    c->last_error = "loopback slabs are stepped with zpic_step_group";
+    return ZPIC_E_STATE;
+  }
+  try {
+    if (c->slab && c->halo_dirty) {
+      ncclResult_t r = nccl_exchange_round2(c, c->cur);
+      if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL halo: ") + ncclGetErrorString(r)};
+      c->halo_dirty = false;
+    }
+    for (int k = 0; k < n; ++k) {
+      StepState s = step_phase_a(c);
+      if (c->slab) {
+        ProfScope ps(c, K_EXCHANGE);
+        ncclResult_t r = nccl_exchange_round1(c);
+        if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 1: ") + ncclGetErrorString(r)};
+      }
+      step_phase_b(c, s);
+      if (c->slab) {
+        ProfScope ps(c, K_EXCHANGE);
+        ncclResult_t r = nccl_exchange_round2(c, c->cur ^ 1);
+        if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 2: ") + ncclGetErrorString(r)};
+      }
+      step_phase_c(c, s);
+    }
+  } catch (const Fail& f) {
+    c->last_error = f.msg;
+    return f.st;
+  }
+  return step_error(c);
+}
+
+zpic_status zpic_step_group(zpic_ctx** cs, int32_t count, int32_t n) {
+  if (!cs || count < 1 || n < 0) return ZPIC_E_INVALID;
+  for (int r = 0; r < count; ++r) {
+    zpic_ctx* c = cs[r];
+    if (!c || !c->slab || c->transport != ZPIC_TRANSPORT_LOOPBACK || c->world != count || c->rank != r ||
+        c->stream != cs[0]->stream) {
+      if (c) c->last_error = "zpic_step_group: not one complete loopback group on one stream (ranks in order)";
+      return ZPIC_E_STATE;
+    }
+  }
+  try {
+    if (cs[0]->halo_dirty) {
+      loop_exchange_round2(cs, count, cs[0]->cur);
+      for (int r = 0; r < count; ++r) cs[r]->halo_dirty = false;
+    }
+    for (int k = 0; k < n; ++k) {
+      std::vector<StepState> st(count);
+      for (int r = 0; r < count; ++r) st[r] = step_phase_a(cs[r]);
+      loop_exchange_round1(cs, count);
+      for (int r = 0; r < count; ++r) step_phase_b(cs[r], st[r]);
+      loop_exchange_round2(cs, count, cs[0]->cur ^ 1);
+      for (int r = 0; r < count; ++r) step_phase_c(cs[r], st[r]);
+    }
+  } catch (const Fail& f) {
+    cs[0]->last_error = f.msg;
+    return f.st;
+  }
+  return step_error(cs[0]);
+}
+
+zpic_status zpic_nccl_unique_id(void* out, size_t out_len) {
+  if (!out || out_len < sizeof(ncclUniqueId)) return ZPIC_E_BUFSIZE;
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) { g_init_error = std::string("ncclGetUniqueId: ") + ncclGetErrorString(r); return ZPIC_E_NCCL; }
+  std::memcpy(out, &id, sizeof(id));
   return ZPIC_OK;
 }
 
@@ -630,7 +902,19 @@ zpic_status zpic_energy(zpic_ctx* c, int64_t* iter, double* field, double* kinet
   zpic_status st = check_sticky(c);
   if (st != ZPIC_OK) return st;
   double e[1 + kMaxSpecies] = {0, 0, 0, 0, 0};
-  if (c->steps > 0) cudaMemcpy(e, c->energy, sizeof(e), cudaMemcpyDeviceToHost);
+  if (c->slab && c->transport == ZPIC_TRANSPORT_NCCL) {
+    // global sums over the slabs (collective over all ranks)
+    double* red = nullptr;
+    try { red = alloc_n<double>(c, 1 + kMaxSpecies); } catch (const Fail& f) { c->last_error = f.msg; return f.st; }
+    ncclResult_t r = ncclAllReduce(c->energy, red, 1 + kMaxSpecies, ncclDouble, ncclSum, (ncclComm_t)c->comm, c->stream);
+    if (r != ncclSuccess) { c->last_error = ncclGetErrorString(r); dev_free(c, red); return ZPIC_E_NCCL; }
+    cudaMemcpyAsync(e, red, sizeof(e), cudaMemcpyDeviceToHost, c->stream);
+    cudaStreamSynchronize(c->stream);
+    dev_free(c, red);
+    if (c->steps == 0) for (double& v : e) v = 0.0;
+  } else if (c->steps > 0) {
+    cudaMemcpy(e, c->energy, sizeof(e), cudaMemcpyDeviceToHost);
+  }
   if (iter) *iter = c->steps - 1;
   if (field) *field = e[0];
   if (kinetic)
@@ -684,6 +968,7 @@ zpic_status zpic_kernel_times(zpic_ctx* c, const char** names, double* ms, int32
 void zpic_free(zpic_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->own_comm && c->comm) ncclCommDestroy((ncclComm_t)c->comm);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   for (void* p : c->allocations) {
     if (c->opt.free) c->opt.free(p, c->opt.alloc_user);

@@ -43,14 +43,18 @@ __device__ __forceinline__ int cell_ix(int c) { return c & 0xffff; }
 __device__ __forceinline__ int cell_iy(int c) { return c >> 16; }
 
 // Apply the particle boundary conditions to a new cell (a5).  Returns false if the particle
-// leaves the domain through an open / window edge (removed).
-__device__ __forceinline__ bool domain_bc(int& ix, int& iy, const GridDesc& g, int bcx, int bcy) {
+// leaves the domain through an open / window edge (removed).  x: periodic wrap or removal.
+// y, one slab: periodic wrap or removal; y, slab decomposition: a particle crossing to an
+// existing neighbour keeps its out-of-slab iy (-1 or ny) and is routed by insert_particle.
+__device__ __forceinline__ bool domain_bc(int& ix, int& iy, const PushParams& p) {
+  const GridDesc& g = p.g;
   if (ix < 0 || ix >= g.nx) {
-    if (bcx != ZPIC_BC_PERIODIC) return false;
+    if (p.bcx != ZPIC_BC_PERIODIC) return false;
     ix += ix < 0 ? g.nx : -g.nx;
   }
   if (iy < 0 || iy >= g.ny) {
-    if (bcy != ZPIC_BC_PERIODIC) return false;
+    if (p.slab) return iy < 0 ? p.has_lo : p.has_hi;
+    if (p.bcy != ZPIC_BC_PERIODIC) return false;
     iy += iy < 0 ? g.ny : -g.ny;
   }
   return true;
@@ -63,9 +67,20 @@ __device__ __forceinline__ void list_put(const PList& L, int k, int cell, float 
   L.species[k] = s;
 }
 
-// Insert one particle into its tile's slack, else into the loose list.
+__device__ __forceinline__ void list_append(const PList& L, int* err, int cell, float x, float y, float ux, float uy,
+                                            float uz, uint32_t id, int s) {
+  const int k = atomicAdd(L.count, 1);
+  if (k < L.cap) list_put(L, k, cell, x, y, ux, uy, uz, id, s);
+  else atomicOr(err, ERR_OVERFLOW);
+}
+
+// Insert one particle into its tile's slack, else into the loose list; a particle outside the
+// slab (iy = -1 or ny, slab decomposition only) goes to the send list of that neighbour with iy
+// already in the neighbour's local rows (equal slabs).
 __device__ __forceinline__ void insert_particle(const PushParams& p, int s, int ix, int iy, float x, float y, float ux,
                                                 float uy, float uz, uint32_t id) {
+  if (iy < 0) { list_append(p.send[0], p.err, pack_cell(ix, iy + p.g.ny), x, y, ux, uy, uz, id, s); return; }
+  if (iy >= p.g.ny) { list_append(p.send[1], p.err, pack_cell(ix, iy - p.g.ny), x, y, ux, uy, uz, id, s); return; }
   const int t = (iy / p.T) * p.ntx + (ix / p.T);
   const PStore& ps = p.ps[s];
   const int slot = atomicAdd(ps.cnt + t, 1);
@@ -76,9 +91,7 @@ __device__ __forceinline__ void insert_particle(const PushParams& p, int s, int 
     if (ps.id) ps.id[k] = id;
   } else {
     atomicSub(ps.cnt + t, 1);
-    const int k = atomicAdd(p.spill_out.count, 1);
-    if (k < p.spill_out.cap) list_put(p.spill_out, k, cell, x, y, ux, uy, uz, id, s);
-    else atomicOr(p.err, ERR_OVERFLOW);
+    list_append(p.spill_out, p.err, cell, x, y, ux, uy, uz, id, s);
   }
 }
 

@@ -71,6 +71,11 @@ struct PushParams {
   float dtdx, dtdy; // dt/dx, dt/dy
   int bcx, bcy;
   int shift;        // 1 when the moving window shifts at the end of this step (ix -= 1)
+  // y-slab decomposition (§8(e)): slab = 1 when the y neighbours are other slabs; has_lo /
+  // has_hi = a neighbour exists below / above (else a domain edge).  Particles leaving the
+  // slab go to send[0] (down, iy += ny) or send[1] (up, iy -= ny).
+  int slab, has_lo, has_hi;
+  PList send[2];
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
   int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
 };
@@ -83,6 +88,8 @@ struct YeeParams {
   float murx, mury;                 // Mur-1 coefficients (dt - dx)/(dt + dx), (dt - dy)/(dt + dy)
   int bcx, bcy;
   int shift;                        // 1: store the result one column toward -x (window shift)
+  int y_images;                     // write periodic y guard images (1 GPU, periodic y)
+  int ylo_edge, yhi_edge;           // the slab's low / high y boundary is a domain edge
   double* fe_slots;
   double fe_scale;  // dx dy / 2
 };
@@ -133,6 +140,18 @@ struct zpic_ctx {
   int64_t repacks;
   int64_t launches;  // kernels enqueued by zpic_step so far
   int64_t n_move;    // moving-window shifts so far
+  // y-slab decomposition (§8(e)); slab == false: the whole domain, no exchanges
+  bool slab;
+  int rank, world, lower, upper, has_lo, has_hi;
+  int transport;
+  void* comm;        // ncclComm_t
+  bool own_comm;
+  float* jrup;       // [3][2][pitch]: the upper neighbour's raw J rows -1, 0
+  float* jrdn;       // [3][2][pitch]: the lower neighbour's raw J rows ny, ny+1
+  void* pmsg_send[2];  // particle messages to the lower [0] / upper [1] neighbour
+  void* pmsg_recv[2];  // from the lower [0] / upper [1] neighbour
+  int pcap;
+  bool halo_dirty;   // E/B guard rows of the current buffer must be exchanged before the next step
   std::vector<void*> allocations;
   std::string last_error;
   // profiling

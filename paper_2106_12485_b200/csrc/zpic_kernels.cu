@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kBlock) k_push_loose(PushParams p) {
     const int nseg = split_path(ix, iy, x, y, dxp, dyp, sc.q * uz * rg, seg, di, dj);
     for (int q = 0; q < nseg; ++q) deposit_seg(A, seg[q], sc.jx, sc.jy);
     ix += di - p.shift; iy += dj;
-    if (domain_bc(ix, iy, p.g, p.bcx, p.bcy)) insert_particle(p, s, ix, iy, x, y, ux, uy, uz, id);
+    if (domain_bc(ix, iy, p)) insert_particle(p, s, ix, iy, x, y, ux, uy, uz, id);
   }
   for (int s = 0; s < p.nspecies; ++s) block_add_double((double)ke[s], p.ke_slots + s * kEnergySlots + (blockIdx.x & (kEnergySlots - 1)));
 }
@@ -167,6 +167,9 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   const int i0 = blockIdx.x * T, j0 = blockIdx.y * T;
   const int tw = min(T, g.nx - i0), th = min(T, g.ny - j0);
   const long pl = g.plane;
+  // y edges of this slab that are domain edges (with a slab decomposition the others are
+  // interfaces whose guards come from the neighbour)
+  const bool ylo_dom = p.bcy != ZPIC_BC_PERIODIC && p.ylo_edge, yhi_dom = p.bcy != ZPIC_BC_PERIODIC && p.yhi_edge;
 
   for (int k = threadIdx.x; k < WE * WE; k += kBlock) {
     const int gi = i0 + k % WE - 1, gj = j0 + k / WE - 1;
@@ -208,7 +211,7 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   for (int k = threadIdx.x; k < WB * WB; k += kBlock) {
     const int lx = k % WB - 1, ly = k / WB - 1;
     const int gi = i0 + lx, gj = j0 + ly;
-    if ((p.bcx != ZPIC_BC_PERIODIC && (gi < 0 || gi >= g.nx)) || (p.bcy != ZPIC_BC_PERIODIC && (gj < 0 || gj >= g.ny)))
+    if ((p.bcx != ZPIC_BC_PERIODIC && (gi < 0 || gi >= g.nx)) || (gj < 0 && ylo_dom) || (gj >= g.ny && yhi_dom))
       continue;   // B guards of a non-periodic axis stay 0 (only the interior is advanced)
     const float ez = sE[2][EI(lx, ly)];
     sB[0][k] -= p.hdy * (sE[2][EI(lx, ly + 1)] - ez);
@@ -242,16 +245,16 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   // Non-periodic edges (R13, R14).  The node line on a domain edge holds: Mur-1 values for the
   // tangential E on an open edge, E^{n+1}_b = E^n_b' + k (E^{n+1}_b' - E^n_b); zero (a guard) for
   // everything else outside the box.  x edges first, then y edges (the oracle's order).
-  const bool xlo = i0 == 0, xhi = i0 + tw == g.nx, ylo = j0 == 0, yhi = j0 + th == g.ny;
+  const bool xlo = i0 == 0, xhi = i0 + tw == g.nx, ylo = j0 == 0 && ylo_dom, yhi = j0 + th == g.ny && yhi_dom;
   if (p.bcx != ZPIC_BC_PERIODIC && (xlo || xhi)) {
     for (int k = threadIdx.x; k < 2 * (th + 1); k += kBlock) {
       const int ly = k % (th + 1), hiE = k / (th + 1);
       if (!(hiE ? xhi : xlo)) continue;
       const int gj = j0 + ly, bn = hiE ? tw : 0, bp = hiE ? tw - 1 : 1;
-      const bool row_out = p.bcy != ZPIC_BC_PERIODIC && gj == g.ny;   // guard row of an open y axis
+      const bool row_out = yhi && gj == g.ny;   // guard row of an open y axis
       if (p.bcx == ZPIC_BC_OPEN && !row_out) {
         sE[1][EI(bn, ly)] = s_mur[hiE][0][1][ly] + p.murx * (sE[1][EI(bp, ly)] - s_mur[hiE][0][0][ly]);
-        if (!(p.bcy == ZPIC_BC_OPEN && gj == 0))
+        if (!(ylo && p.bcy == ZPIC_BC_OPEN && gj == 0))
           sE[2][EI(bn, ly)] = s_mur[hiE][1][1][ly] + p.murx * (sE[2][EI(bp, ly)] - s_mur[hiE][1][0][ly]);
         else if (hiE)
           sE[2][EI(bn, ly)] = 0.f;   // corner node (nx, 0) of two open edges: never Mur-updated
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
       if (gi <= 1) xs[nxs++] = gi + g.nx;
       if (gi == g.nx - 1) xs[nxs++] = -1;
     }
-    if (p.bcy == ZPIC_BC_PERIODIC) {
+    if (p.y_images) {
       if (gj <= 1) ys[nys++] = gj + g.ny;
       if (gj == g.ny - 1) ys[nys++] = -1;
     }
@@ -314,7 +317,7 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
       const int gj = j0 + ly;
       int ys[3], nys = 1;
       ys[0] = gj;
-      if (p.bcy == ZPIC_BC_PERIODIC) {
+      if (p.y_images) {
         if (gj <= 1) ys[nys++] = gj + g.ny;
         if (gj == g.ny - 1) ys[nys++] = -1;
       }
@@ -331,7 +334,7 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
       if (ly == th && !(p.bcy == ZPIC_BC_OPEN && yhi)) continue;   // row ny only holds Mur nodes
       int ys[3], nys = 1;
       ys[0] = gj;
-      if (p.bcy == ZPIC_BC_PERIODIC) {
+      if (p.y_images) {
         if (gj <= 1) ys[nys++] = gj + g.ny;
         if (gj == g.ny - 1) ys[nys++] = -1;
       }
@@ -496,6 +499,66 @@ __global__ void k_filter_x(const float* __restrict__ Jin, float* __restrict__ Jo
   }
 }
 
+// ---- y-slab decomposition (§8(e)) -----------------------------------------------------------
+// Round 1, current: the rows arrive raw (x-folded, not y-folded).  From the upper neighbour:
+// its raw rows -1, 0 (rup[c][0..1]); from the lower neighbour: its raw rows ny, ny+1
+// (rdn[c][0..1]).  Then ("the reduction is only required for ghost cells"):
+//   row ny-1 += upper's row -1;   guard row ny = upper's row 0 + my guard row ny  (= the upper's
+//   final row 0, which the redundant E^{n+1} row of the Yee kernel needs);
+//   row 0 += lower's row ny;      row 1 += lower's row ny+1.
+// At a domain edge (no neighbour) the guard deposits are discarded.  One thread per column of
+// the padded row and component (guard columns included: the rows are already x-refreshed).
+__global__ void k_apply_j_halo(float* J, GridDesc g, const float* rup, const float* rdn, int has_lo, int has_hi) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= 3 * g.pitch) return;
+  const int c = idx / g.pitch, col = idx % g.pitch;
+  float* F = J + c * g.plane + col;
+  const long P = g.pitch;
+  if (has_hi) {
+    F[(long)g.ny * P] += rup[(2 * c) * P + col];                       // row ny-1
+    F[(long)(g.ny + 1) * P] += rup[(2 * c + 1) * P + col];             // guard row ny
+  } else {
+    F[(long)(g.ny + 1) * P] = 0.f;
+    F[(long)(g.ny + 2) * P] = 0.f;
+  }
+  if (has_lo) {
+    F[1 * P] += rdn[(2 * c) * P + col];                                // row 0
+    F[2 * P] += rdn[(2 * c + 1) * P + col];                            // row 1
+  } else {
+    F[0] = 0.f;                                                        // guard row -1
+  }
+}
+
+// Particle message: [count, pad x3][cell][x][y][ux][uy][uz][id][species], each `cap` long.
+__host__ __device__ inline size_t msg_bytes(int cap) { return 16 + (size_t)cap * 32; }
+__host__ __device__ inline PList msg_list(void* buf, int cap) {
+  char* b = (char*)buf;
+  PList L;
+  L.count = (int32_t*)b;
+  L.cell = (int32_t*)(b + 16);
+  L.x = (float*)(L.cell + cap);
+  L.y = L.x + cap;
+  L.ux = L.y + cap;
+  L.uy = L.ux + cap;
+  L.uz = L.uy + cap;
+  L.id = (uint32_t*)(L.uz + cap);
+  L.species = (int32_t*)(L.id + cap);
+  L.cap = cap;
+  return L;
+}
+
+// Round 1, particles: insert the particles received from both neighbours (already pushed this
+// step; iy already in this slab's rows).
+__global__ void k_recv_insert(PushParams p, PList from_lo, PList from_hi) {
+  const int n_lo = min(*from_lo.count, from_lo.cap), n_hi = min(*from_hi.count, from_hi.cap);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n_lo + n_hi; k += gridDim.x * blockDim.x) {
+    const PList& L = k < n_lo ? from_lo : from_hi;
+    const int q = k < n_lo ? k : k - n_lo;
+    const int cell = L.cell[q];
+    insert_particle(p, L.species[q], cell_ix(cell), cell_iy(cell), L.x[q], L.y[q], L.ux[q], L.uy[q], L.uz[q], L.id[q]);
+  }
+}
+
 // Validate host-uploaded particles and count them per tile (err bit 4 = out of the slab).
 __global__ void k_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy,
                         const float* x, const float* y, int* counts, int* err) {
@@ -592,6 +655,16 @@ void launch_filter_x(const float* Jin, float* Jout, const GridDesc& g, int npass
     attr = smem;
   }
   k_filter_x<<<3 * g.ny, kBlock, smem, st>>>(Jin, Jout, g, npass, compensated, periodic);
+}
+void launch_apply_j_halo(float* J, const GridDesc& g, const float* rup, const float* rdn, int has_lo, int has_hi,
+                         cudaStream_t st) {
+  const int n = 3 * g.pitch;
+  k_apply_j_halo<<<(n + kBlock - 1) / kBlock, kBlock, 0, st>>>(J, g, rup, rdn, has_lo, has_hi);
+}
+size_t particle_msg_bytes(int cap) { return msg_bytes(cap); }
+PList particle_msg_list(void* buf, int cap) { return msg_list(buf, cap); }
+void launch_recv_insert(const PushParams& p, const PList& lo, const PList& hi, cudaStream_t st) {
+  k_recv_insert<<<148 * 2, kBlock, 0, st>>>(p, lo, hi);
 }
 void launch_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
                   const float* y, int* counts, int* err, cudaStream_t st) {

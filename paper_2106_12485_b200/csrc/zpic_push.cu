@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
         di -= p.shift;   // moving window: the cell index follows the shift at the end of the step
         ix += di; iy += dj;
         if ((unsigned)(lx + di) < (unsigned)tw && (unsigned)(ly + dj) < (unsigned)th) stay = true;
-        else move = domain_bc(ix, iy, p.g, p.bcx, p.bcy);
+        else move = domain_bc(ix, iy, p);
       }
       // extra pieces -> this warp's queue; drain full batches of 32 with every lane active
 #pragma unroll

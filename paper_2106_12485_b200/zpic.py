@@ -52,9 +52,12 @@ class zpic_options(ctypes.Structure):
                 ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", ctypes.c_void_p)]
 
 
+TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
+
+
 class zpic_dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int32), ("world", ctypes.c_int32), ("nccl_comm", ctypes.c_void_p),
-                ("device", ctypes.c_int32)]
+                ("device", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("transport", ctypes.c_int)]
 
 
 _P = ctypes.c_void_p
@@ -78,17 +81,20 @@ _lib.zpic_energy.argtypes = [_P, _I64P, _F64P, _F64P]
 _lib.zpic_layout.argtypes = [_P, _I32P, _I32P]
 _lib.zpic_counters.argtypes = [_P, _I64P, ctypes.c_int32]
 _lib.zpic_kernel_times.argtypes = [_P, ctypes.POINTER(ctypes.c_char_p), _F64P, _I32P, _I32P]
+_lib.zpic_step_group.argtypes = [ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_int32]
+_lib.zpic_nccl_unique_id.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 _lib.zpic_free.argtypes = [_P]
 _lib.zpic_free.restype = None
 _lib.zpic_last_error.argtypes = [_P]
 _lib.zpic_last_error.restype = ctypes.c_char_p
 for _f in ("zpic_init", "zpic_set_particles", "zpic_set_fields", "zpic_step", "zpic_sync", "zpic_get_fields",
-           "zpic_get_particles", "zpic_energy", "zpic_layout", "zpic_counters", "zpic_kernel_times"):
+           "zpic_get_particles", "zpic_energy", "zpic_layout", "zpic_counters", "zpic_kernel_times",
+           "zpic_step_group", "zpic_nccl_unique_id"):
     getattr(_lib, _f).restype = ctypes.c_int
 
-EXPORTED = ["zpic_init", "zpic_set_particles", "zpic_set_fields", "zpic_step", "zpic_sync", "zpic_get_fields",
-            "zpic_get_particles", "zpic_energy", "zpic_layout", "zpic_counters", "zpic_kernel_times", "zpic_free",
-            "zpic_last_error"]
+EXPORTED = ["zpic_init", "zpic_set_particles", "zpic_set_fields", "zpic_step", "zpic_step_group", "zpic_sync",
+            "zpic_get_fields", "zpic_get_particles", "zpic_energy", "zpic_layout", "zpic_counters",
+            "zpic_kernel_times", "zpic_nccl_unique_id", "zpic_free", "zpic_last_error"]
 
 
 class ZpicError(RuntimeError):
@@ -139,6 +145,18 @@ def zpic_set_fields(ctx, which, arr):
 
 def zpic_step(ctx, n):
     _check(_lib.zpic_step(ctx, n), ctx)
+
+
+def zpic_step_group(ctxs, n):
+    arr = (_P * len(ctxs))(*[c.value if isinstance(c, _P) else c for c in ctxs])
+    st = _lib.zpic_step_group(arr, len(ctxs), n)
+    _check(st, ctxs[0])
+
+
+def zpic_nccl_unique_id():
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.zpic_nccl_unique_id(buf, 128), None)
+    return buf.raw
 
 
 def zpic_sync(ctx):
@@ -215,7 +233,9 @@ class Simulation:
     PyTorch's current CUDA stream when torch_plumbing is True."""
 
     def __init__(self, cfg, inject=True, track_ids=False, tile=16, profile=False, capacity_slack=1.25,
-                 torch_plumbing=True, stream=None):
+                 torch_plumbing=True, stream=None, dist=None):
+        """dist: None (whole domain) or {"rank", "world", "transport": "nccl" | "loopback",
+        "nccl_id": 128 bytes | "nccl_comm": ncclComm_t address} (y-slab decomposition)."""
         self.cfg = cfg
         self.nx, self.ny = cfg["nx"], cfg["ny"]
         self.nspecies = len(cfg["species"])
@@ -255,7 +275,18 @@ class Simulation:
             a, f = ALLOC_FN(_alloc), FREE_FN(_free)
             self._keep += [a, f]
             opt.alloc, opt.free = a, f
-        self.ctx = zpic_init(grid, cfg["dt"], sps, bc, cfg["seed"], opt, None)
+        dst = None
+        if dist is not None:
+            dst = zpic_dist()
+            dst.rank, dst.world = dist["rank"], dist["world"]
+            dst.transport = TRANSPORT_LOOPBACK if dist.get("transport", "nccl") == "loopback" else TRANSPORT_NCCL
+            dst.nccl_comm = dist.get("nccl_comm")
+            self._nccl_id = ctypes.create_string_buffer(dist["nccl_id"], 128) if dist.get("nccl_id") else None
+            dst.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None
+            dst.device = dist.get("device", 0)
+        self.dist = dist
+        self.ctx = zpic_init(grid, cfg["dt"], sps, bc, cfg["seed"], opt, dst)
+        self.y0, self.ny_local = zpic_layout(self.ctx)
 
     def set_particles(self, s, p):
         zpic_set_particles(self.ctx, s, p["ix"], p["iy"], p["x"], p["y"], p["ux"], p["uy"], p["uz"], p.get("id"))

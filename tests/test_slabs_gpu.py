@@ -1,0 +1,126 @@
+"""y-slab decomposition on one B200 (P10 "regional deposit + ghost reduction
+= global deposit", P virtual slabs = 1 slab).  Loopback groups step P slab contexts together
+through the same exchange rounds the NCCL transport uses; the NCCL transport itself runs with a
+one-rank self-ring.  Needs a B200."""
+import numpy as np
+import pytest
+
+import synth
+from oracle.sim import from_config
+from parity_util import (CELL_FRAC, ENERGY_TOL, FIELD_TOL, MOM_TOL, POS_TOL, compare_particles, energy_agreement,
+                         oracle_particles, rel_l2)
+
+pytestmark = pytest.mark.gpu
+
+
+def _z():
+    import paper_2106_12485_b200 as z
+    return z
+
+
+def _group(cfg, world, parts, laser=False):
+    from paper_2106_12485_b200.dist import LoopbackGroup
+    g = LoopbackGroup(cfg, world, inject=False, track_ids=True)
+    for s, p in enumerate(parts):
+        g.set_particles(s, p)
+    if laser:
+        E, B = synth.laser_fields(cfg)
+        g.set_fields(0, E)
+        g.set_fields(1, B)
+    return g
+
+
+def _run_vs_oracle(cfg, world, steps, laser=False):
+    parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
+    g = _group(cfg, world, parts, laser)
+    o = from_config(cfg, particles=parts)
+    per = (cfg["bc"][0] == 0, cfg["bc"][1] == 0)
+    fe_g, fe_o = [], []
+    for n in range(steps):
+        g.step(1)
+        o.step()
+        it, fe, ke = g.energy()
+        assert it == n
+        fe_g.append(fe + sum(ke))
+        fe_o.append(o.fe[-1] + sum(o.ke[-1]))
+        if n in (0, 9, steps - 1):
+            for s in range(len(parts)):
+                c = compare_particles(g.particles(s, True), oracle_particles(o, s), cfg["nx"], cfg["ny"], per)
+                if n == 0:
+                    assert c["pos_max"] <= POS_TOL and c["mom_max"] <= MOM_TOL, c
+                assert c["cell_exact_frac"] >= CELL_FRAC, c
+        if n == 9:
+            for w in (0, 1):
+                e = rel_l2(g.fields(w), o.fields(w))
+                assert e <= FIELD_TOL, (w, e)
+    assert energy_agreement(fe_g, fe_o) <= ENERGY_TOL
+    assert g.counters()["particles"] == sum(len(s["ix"]) for s in o.species)
+    g.close()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_slabs_periodic_c1(world):
+    cfg = synth.config("C1", nx=48, ny=64)
+    cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
+    _run_vs_oracle(cfg, world, 12)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_slabs_open_x_c3(world):
+    cfg = synth.config("C3", nx=128, ny=32)
+    cfg["species"][0].update(x0=0.0, x1=6.4, uth=(0.1, 0.1, 0.1))
+    cfg["species"][1].update(x0=6.4, x1=12.8, uth=(0.1, 0.1, 0.1))
+    _run_vs_oracle(cfg, world, 20)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_slabs_window_open_y_c4(world):
+    cfg = synth.config("C4", nx=400, ny=64)
+    cfg["species"][0].update(x0=2.0, x1=2.4)
+    cfg["laser"] = dict(cfg["laser"], start=400 * cfg["dx"] - 2.0)
+    _run_vs_oracle(cfg, world, 20, laser=True)
+
+
+def test_slabs_equal_one_slab():
+    """P = 4 virtual slabs reproduce the unsplit domain (P10) to fp32 summation order."""
+    cfg = synth.config("C2", nx=64, ny=64)
+    parts = [synth.species_particles(cfg, s) for s in range(2)]
+    one = _z().Simulation(cfg, inject=False, track_ids=True)
+    for s, p in enumerate(parts):
+        one.set_particles(s, p)
+    four = _group(cfg, 4, parts)
+    for _ in range(15):
+        one.step(1)
+        four.step(1)
+    for w in (0, 1, 2):
+        assert rel_l2(four.fields(w), one.fields(w)) < 2e-5, w
+    for s in range(2):
+        c = compare_particles(four.particles(s, True), one.particles(s, True), 64, 64)
+        assert c["pos_max"] < 1e-4 and c["cell_exact_frac"] >= CELL_FRAC, c
+    one.close()
+    four.close()
+
+
+def test_nccl_transport_self_ring():
+    """The NCCL transport (send / recv in groups on the compute stream) with one rank whose lower
+    and upper neighbour is itself must reproduce the unsplit periodic domain."""
+    z = _z()
+    cfg = synth.config("C1", nx=48, ny=40)
+    cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
+    parts = [synth.species_particles(cfg, 0)]
+    ref = z.Simulation(cfg, inject=False, track_ids=True)
+    ref.set_particles(0, parts[0])
+    uid = z.zpic.zpic_nccl_unique_id()
+    ring = z.Simulation(cfg, inject=False, track_ids=True,
+                        dist={"rank": 0, "world": 1, "transport": "nccl", "nccl_id": uid})
+    ring.set_particles(0, parts[0])
+    for _ in range(12):
+        ref.step(1)
+        ring.step(1)
+    for w in (0, 1, 2):
+        assert rel_l2(ring.fields(w), ref.fields(w)) < 2e-5, w
+    c = compare_particles(ring.particles(0, True), ref.particles(0, True), 48, 40)
+    assert c["pos_max"] < 1e-4 and c["cell_exact_frac"] >= CELL_FRAC, c
+    assert abs(ring.energy()[1] - ref.energy()[1]) <= 1e-6 * max(abs(ref.energy()[1]), 1e-12)
+    ring.close()
+    ref.close()
