@@ -132,12 +132,15 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
-def e2e_run(args, cfg, torch, z):
+def e2e_run(args, cfg, torch, z, dist_kw=None, world=1):
     """End to end through the public API with HOST buffers: upload the initial particles from
     pinned host memory (zpic_set_particles), K steps with the energies read back every step,
-    and the final E, B fields read back; all inside the timed region."""
+    and the final E, B fields read back; all inside the timed region (max over ranks)."""
     import numpy as np
-    src = z.Simulation(cfg, inject=True)
+    if dist_kw is not None:
+        from paper_2106_12485_b200.dist import nccl_id_broadcast
+        dist_kw = dict(dist_kw, nccl_id=nccl_id_broadcast())
+    src = z.Simulation(cfg, inject=True, dist=dist_kw)
     host = []
     for s in range(len(cfg["species"])):
         p = src.particles(s)
@@ -150,8 +153,13 @@ def e2e_run(args, cfg, torch, z):
         host.append(pinned)
     src.close()
     del p
-    sim = z.Simulation(cfg, inject=False)
+    if dist_kw is not None:   # a fresh communicator for the second context
+        from paper_2106_12485_b200.dist import nccl_id_broadcast
+        dist_kw = dict(dist_kw, nccl_id=nccl_id_broadcast())
+    sim = z.Simulation(cfg, inject=False, dist=dist_kw)
     torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
     h2d = 0
     for s, hp in enumerate(host):
@@ -169,6 +177,10 @@ def e2e_run(args, cfg, torch, z):
     dt = time.perf_counter() - t0
     n = sum(v["ix"].numel() for v in host)
     sim.close()
+    if world > 1:
+        from paper_2106_12485_b200.dist import reduce_max, reduce_sum
+        dt = reduce_max(dt)
+        n, h2d, d2h = reduce_sum([float(n), float(h2d), float(d2h)])
     return {"value": n * args.steps / dt, "unit": UNIT, "h2d_bytes_per_step": int(h2d / args.steps),
             "d2h_bytes_per_step": int(d2h / args.steps), "seconds": dt,
             "note": "initial particles uploaded from pinned host memory, energies read every step, E and B read at the end"}
@@ -205,7 +217,11 @@ def main():
     if args.nx:
         cfg["nx"], cfg["ny"] = args.nx, args.ny or args.nx
         cfg["name"] += "-resized-%dx%d" % (cfg["nx"], cfg["ny"])
-    sim = z.Simulation(cfg, inject=True, profile=True, tile=args.tile)
+    dist_kw = None
+    if world > 1:   # y-slabs, one per GPU, NCCL send/recv halos
+        from paper_2106_12485_b200.dist import nccl_id_broadcast
+        dist_kw = {"rank": rank, "world": world, "transport": "nccl", "nccl_id": nccl_id_broadcast(), "device": local}
+    sim = z.Simulation(cfg, inject=True, profile=True, tile=args.tile, dist=dist_kw)
     n_particles = sim.counters()["particles"]
     n_cells = cfg["nx"] * cfg["ny"]
     sim.step(args.warmup)
@@ -265,8 +281,10 @@ def main():
     }
     if rank == 0 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline(args)
-    if rank == 0 and world == 1 and not args.no_e2e:
-        line["e2e"] = e2e_run(args, cfg, torch, z)
+    if not args.no_e2e:
+        e2e = e2e_run(args, cfg, torch, z, dict(dist_kw, nccl_id=None) if dist_kw else None, world)
+        if rank == 0:
+            line["e2e"] = e2e
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -144,6 +144,24 @@ PList alloc_list(zpic_ctx* c, int cap) {
   return L;
 }
 
+// Mover / loose list capacity: mover_fraction of the largest population the run can reach (with a
+// moving window the injected plasma fills the box: nx * ny * ppc per species); on window-shift
+// steps every particle of a tile's first column changes tile, so add 1.5 / T of it.
+int mover_capacity(zpic_ctx* c, int64_t total) {
+  int64_t pop = total;
+  double frac = c->opt.mover_fraction;
+  if (c->bcx == ZPIC_BC_MOVING_WINDOW) {
+    int64_t full = 0;
+    for (int s = 0; s < c->nspecies; ++s)
+      if (c->species[s].n > 0) full += (int64_t)c->g.nx * c->g.ny * c->species[s].ppc[0] * c->species[s].ppc[1];
+    pop = std::max(pop, full);
+    frac += 1.5 / c->T;
+  }
+  const int64_t cap = std::max<int64_t>(65536, (int64_t)std::ceil(pop * frac));
+  if (cap > 2000000000) throw Fail{ZPIC_E_INVALID, "mover list capacity exceeds 2^31"};
+  return (int)cap;
+}
+
 // Guard mode of an axis for a field (E, B) or the current.
 int field_guard_mode(int bc) { return bc == ZPIC_BC_PERIODIC ? 1 : 2; }
 
@@ -329,7 +347,16 @@ zpic_status check_sticky(zpic_ctx* c) {
   if (e != cudaSuccess) { c->last_error = std::string("CUDA: ") + cudaGetErrorString(e); return ZPIC_E_CUDA; }
   int err = 0;
   cudaMemcpy(&err, c->err, sizeof(int), cudaMemcpyDeviceToHost);
-  if (err & ERR_OVERFLOW) { c->last_error = "particle capacity overflow (mover / loose list full)"; return ZPIC_E_OVERFLOW; }
+  if (err & ERR_OVERFLOW) {
+    int counts[3] = {0, 0, 0};
+    cudaMemcpy(&counts[0], c->movers.count, 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&counts[1], c->spill[0].count, 4, cudaMemcpyDeviceToHost);
+    cudaMemcpy(&counts[2], c->spill[1].count, 4, cudaMemcpyDeviceToHost);
+    c->last_error = "particle capacity overflow (mover / loose / send list full): movers " + std::to_string(counts[0]) +
+                    " loose " + std::to_string(counts[1]) + "/" + std::to_string(counts[2]) + " cap " +
+                    std::to_string(c->movers.cap) + " err " + std::to_string(err) + " steps " + std::to_string(c->steps);
+    return ZPIC_E_OVERFLOW;
+  }
   if (err & ERR_MIGRATION) { c->last_error = "a particle moved >= 1 cell in one step"; return ZPIC_E_MIGRATION; }
   return ZPIC_OK;
 }
@@ -473,7 +500,7 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
         total += (int64_t)(col_hi - col_lo) * g.ny * ppc;
       }
     }
-    const int mcap = std::max<int64_t>(65536, (int64_t)std::ceil(total * c->opt.mover_fraction));
+    const int mcap = mover_capacity(c, total);
     c->movers = alloc_list(c, (int)mcap);
     c->spill[0] = alloc_list(c, (int)mcap);
     c->spill[1] = alloc_list(c, (int)mcap);
@@ -578,7 +605,7 @@ zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t*
       CUDA_OR_THROW(cudaMemcpy(cnt.data(), c->ps[q].cnt, c->ntiles * 4, cudaMemcpyDeviceToHost));
       for (int v : cnt) total += v;
     }
-    const int need = (int)std::max<int64_t>(65536, (int64_t)std::ceil(total * c->opt.mover_fraction));
+    const int need = mover_capacity(c, total);
     if (need > c->movers.cap) {
       for (PList* L : {&c->movers, &c->spill[0], &c->spill[1]}) {
         dev_free(c, L->cell); dev_free(c, L->x); dev_free(c, L->y); dev_free(c, L->ux); dev_free(c, L->uy);

@@ -270,8 +270,13 @@ class Simulation:
             def _alloc(nbytes, user):
                 return torch.cuda.caching_allocator_alloc(int(nbytes), dev, st)
 
+            cad = torch.cuda.caching_allocator_delete
+
             def _free(ptr, user):
-                torch.cuda.caching_allocator_delete(ptr)
+                try:
+                    cad(ptr)
+                except Exception:      # interpreter teardown: torch already gone, memory goes with the process
+                    pass
             a, f = ALLOC_FN(_alloc), FREE_FN(_free)
             self._keep += [a, f]
             opt.alloc, opt.free = a, f

@@ -102,6 +102,27 @@ def species_particles(cfg, s):
             "id": ids.astype(np.uint32)}
 
 
+def patch_species(cfg, s, gx0, gy0, w, h):
+    """The particles of the uniform species s whose cells lie in the w x h patch with global
+    origin (gx0, gy0) (periodic wrap of the global grid), with their GLOBAL ids and momenta, and
+    cell indices relative to the patch.  Used to rebuild a sub-domain of a full-size workload
+    exactly as the full lattice has it (the full-size sampled parity checks)."""
+    sp = cfg["species"][s]
+    nx, ny = cfg["nx"], cfg["ny"]
+    px, py = sp["ppc"]
+    lx, ly = np.meshgrid(np.arange(w), np.arange(h))
+    lx, ly = lx.ravel(), ly.ravel()
+    gx, gy = (gx0 + lx) % nx, (gy0 + ly) % ny
+    l, k = np.divmod(np.arange(px * py, dtype=np.int64), px)
+    rep = px * py
+    ids = ((np.repeat(gy, rep).astype(np.int64) * nx + np.repeat(gx, rep)) * py + np.tile(l, len(gx))) * px + np.tile(k, len(gx))
+    ux, uy, uz = momenta(sp, cfg["seed"], s, ids.astype(np.uint64))
+    return {"ix": np.repeat(lx, rep).astype(np.int32), "iy": np.repeat(ly, rep).astype(np.int32),
+            "x": ((np.tile(k, len(gx)) + 0.5) / px).astype(np.float32),
+            "y": ((np.tile(l, len(gx)) + 0.5) / py).astype(np.float32),
+            "ux": ux, "uy": uy, "uz": uz, "id": ids.astype(np.uint32)}
+
+
 def ramp_species(cfg, s):
     """C4 density (R16): n = 0 for x < x0, linear 0 -> n over [x0, x1), n beyond; equal-charge
     particles.  Along x, every y sub-lattice row places particles by inverting the cumulative
