@@ -101,13 +101,8 @@ void alloc_store(zpic_ctx* c, int s, int cap) {
   PStore& ps = c->ps[s];
   size_t n = (size_t)cap * c->ntiles;
   ps.cap = cap;
-  ps.cell = alloc_n<int32_t>(c, n);
-  ps.x = alloc_n<float>(c, n);
-  ps.y = alloc_n<float>(c, n);
-  ps.ux = alloc_n<float>(c, n);
-  ps.uy = alloc_n<float>(c, n);
-  ps.uz = alloc_n<float>(c, n);
-  ps.id = c->opt.track_ids ? alloc_n<uint32_t>(c, n) : nullptr;
+  ps.nf = c->opt.track_ids ? 7 : 6;
+  ps.data = (uint32_t*)dev_alloc(c, n * ps.nf * sizeof(uint32_t));   // contents defined by cnt, no memset
   ps.cnt = alloc_n<int32_t>(c, c->ntiles);
 }
 
@@ -124,8 +119,7 @@ void check_tile_capacity(zpic_ctx* c) {
 
 void free_store(zpic_ctx* c, int s) {
   PStore& ps = c->ps[s];
-  dev_free(c, ps.cell); dev_free(c, ps.x); dev_free(c, ps.y); dev_free(c, ps.ux); dev_free(c, ps.uy);
-  dev_free(c, ps.uz); dev_free(c, ps.id); dev_free(c, ps.cnt);
+  dev_free(c, ps.data); dev_free(c, ps.cnt);
   ps = PStore{};
 }
 

@@ -86,9 +86,11 @@ __device__ __forceinline__ void insert_particle(const PushParams& p, int s, int 
   const int slot = atomicAdd(ps.cnt + t, 1);
   const int cell = pack_cell(ix, iy);
   if (slot < ps.cap) {
-    const long k = (long)t * ps.cap + slot;
-    ps.cell[k] = cell; ps.x[k] = x; ps.y[k] = y; ps.ux[k] = ux; ps.uy[k] = uy; ps.uz[k] = uz;
-    if (ps.id) ps.id[k] = id;
+    uint32_t* q = ps.slot((long)t * ps.cap + slot);
+    q[F_CELL * 32] = (uint32_t)cell;
+    q[F_X * 32] = __float_as_uint(x); q[F_Y * 32] = __float_as_uint(y);
+    q[F_UX * 32] = __float_as_uint(ux); q[F_UY * 32] = __float_as_uint(uy); q[F_UZ * 32] = __float_as_uint(uz);
+    if (ps.nf > F_ID) q[F_ID * 32] = id;
   } else {
     atomicSub(ps.cnt + t, 1);
     list_append(p.spill_out, p.err, cell, x, y, ux, uy, uz, id, s);

@@ -27,14 +27,19 @@ struct GridDesc {
   __host__ __device__ long at(int i, int j) const { return (long)(j + 1) * pitch + (i + kXOff); }
 };
 
-// One species' tile-sorted SoA particle store.  Tile t owns slots [t * cap, t * cap + cnt[t]).
-// cell packs the local cell index: ix | iy << 16.
+// One species' tile-sorted particle store, AoSoA with 32-particle blocks: slot k lives in block
+// k / 32 at lane k % 32, and field f of the block is the contiguous run of 32 words at f * 32,
+// so a warp reading 32 consecutive slots gets one 128 B line per field and a thread needs one
+// address per particle (fields are immediate offsets).  Fields: 0 cell (ix | iy << 16), 1 x,
+// 2 y, 3 ux, 4 uy, 5 uz, 6 id (only with track_ids).  Tile t owns slots
+// [t * cap, t * cap + cnt[t]); cap is a multiple of 32.
+enum PField { F_CELL = 0, F_X, F_Y, F_UX, F_UY, F_UZ, F_ID };
 struct PStore {
-  int32_t* cell;
-  float *x, *y, *ux, *uy, *uz;
-  uint32_t* id;   // nullptr unless track_ids
-  int32_t* cnt;   // [ntiles]
-  int cap;        // slots per tile (multiple of 32)
+  uint32_t* data;  // ntiles * cap / 32 blocks of 32 * nf words
+  int nf;          // 6, or 7 with ids
+  int32_t* cnt;    // [ntiles]
+  int cap;         // slots per tile (multiple of 32)
+  __host__ __device__ uint32_t* slot(long k) const { return data + (k >> 5) * (32L * nf) + (k & 31); }
 };
 
 // Particles that left their tile (or could not be inserted): a flat SoA list.

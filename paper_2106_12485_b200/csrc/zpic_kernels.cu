@@ -435,14 +435,14 @@ __global__ void __launch_bounds__(kBlock) k_inject(InjectParams q) {
     const int ix = c_lo + ck % wc, iy = j0 + ck / wc;
     const int k = sub % q.px, l = sub / q.px;
     const uint64_t id = (((uint64_t)(iy + q.y0) * q.nx_global + ix) * q.py + l) * q.px + k;
-    const long o = base + p;
-    q.ps.cell[o] = pack_cell(ix, iy);
-    q.ps.x[o] = (float)(((double)k + 0.5) / q.px);
-    q.ps.y[o] = (float)(((double)l + 0.5) / q.py);
-    q.ps.ux[o] = thermal(q.key, id, 0, q.ufl[0], q.uth[0]);
-    q.ps.uy[o] = thermal(q.key, id, 1, q.ufl[1], q.uth[1]);
-    q.ps.uz[o] = thermal(q.key, id, 2, q.ufl[2], q.uth[2]);
-    if (q.ps.id) q.ps.id[o] = (uint32_t)id;
+    uint32_t* o = q.ps.slot(base + p);
+    o[F_CELL * 32] = (uint32_t)pack_cell(ix, iy);
+    o[F_X * 32] = __float_as_uint((float)(((double)k + 0.5) / q.px));
+    o[F_Y * 32] = __float_as_uint((float)(((double)l + 0.5) / q.py));
+    o[F_UX * 32] = __float_as_uint(thermal(q.key, id, 0, q.ufl[0], q.uth[0]));
+    o[F_UY * 32] = __float_as_uint(thermal(q.key, id, 1, q.ufl[1], q.uth[1]));
+    o[F_UZ * 32] = __float_as_uint(thermal(q.key, id, 2, q.ufl[2], q.uth[2]));
+    if (q.ps.nf > F_ID) o[F_ID * 32] = (uint32_t)id;
   }
   if (threadIdx.x == 0) q.ps.cnt[t] = n;
 }
@@ -581,10 +581,11 @@ __global__ void k_bin(PStore ps, int T, int ntx, int y0, long n, const int32_t* 
     const int t = (cy / T) * ntx + cx / T;
     const int slot = atomicAdd(ps.cnt + t, 1);
     if (slot >= ps.cap) { atomicOr(err, ERR_OVERFLOW); continue; }
-    const long o = (long)t * ps.cap + slot;
-    ps.cell[o] = pack_cell(cx, cy);
-    ps.x[o] = x[k]; ps.y[o] = y[k]; ps.ux[o] = ux[k]; ps.uy[o] = uy[k]; ps.uz[o] = uz[k];
-    if (ps.id) ps.id[o] = id ? id[k] : (uint32_t)k;
+    uint32_t* o = ps.slot((long)t * ps.cap + slot);
+    o[F_CELL * 32] = (uint32_t)pack_cell(cx, cy);
+    o[F_X * 32] = __float_as_uint(x[k]); o[F_Y * 32] = __float_as_uint(y[k]);
+    o[F_UX * 32] = __float_as_uint(ux[k]); o[F_UY * 32] = __float_as_uint(uy[k]); o[F_UZ * 32] = __float_as_uint(uz[k]);
+    if (ps.nf > F_ID) o[F_ID * 32] = id ? id[k] : (uint32_t)k;
   }
 }
 
@@ -597,12 +598,14 @@ __global__ void k_export(PStore ps, const int64_t* prefix, int y0, int32_t* ix, 
   const long src = (long)t * ps.cap;
   const int64_t dst = prefix[t];
   for (int k = threadIdx.x; k < n; k += blockDim.x) {
-    const int c = ps.cell[src + k];
+    const uint32_t* q = ps.slot(src + k);
+    const int c = (int)q[F_CELL * 32];
     ix[dst + k] = cell_ix(c);
     iy[dst + k] = cell_iy(c) + y0;
-    x[dst + k] = ps.x[src + k]; y[dst + k] = ps.y[src + k];
-    ux[dst + k] = ps.ux[src + k]; uy[dst + k] = ps.uy[src + k]; uz[dst + k] = ps.uz[src + k];
-    if (id) id[dst + k] = ps.id ? ps.id[src + k] : 0u;
+    x[dst + k] = __uint_as_float(q[F_X * 32]); y[dst + k] = __uint_as_float(q[F_Y * 32]);
+    ux[dst + k] = __uint_as_float(q[F_UX * 32]); uy[dst + k] = __uint_as_float(q[F_UY * 32]);
+    uz[dst + k] = __uint_as_float(q[F_UZ * 32]);
+    if (id) id[dst + k] = ps.nf > F_ID ? q[F_ID * 32] : 0u;
   }
 }
 

@@ -16,6 +16,7 @@
 // chunk, and only O(#leavers) particle moves.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "zpic_device.cuh"
 
@@ -39,9 +40,9 @@ struct SegQueue {
   }
 };
 
-template <int T>
-__global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
-  constexpr int W = T + 2, WJ = T + 3, NW = kBlock / 32;
+template <int T, int BLK, int MINB>
+__global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
+  constexpr int W = T + 2, WJ = T + 3, NW = BLK / 32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* s_eb1 = reinterpret_cast<float2*>(smem_raw);
   float2* s_eb2 = s_eb1 + W * W;
@@ -54,6 +55,8 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
   __shared__ unsigned s_bits[kHCap / 32];
   __shared__ int s_cnt[4];  // holes, holes below, stayers above, hole-list overflow
   __shared__ int s_wsum[2][NW];
+  __shared__ double s_ke[kMaxSpecies];
+  if (threadIdx.x < kMaxSpecies) s_ke[threadIdx.x] = 0.0;
 
   const int t = blockIdx.x;
   const int tx = t % p.ntx, ty = t / p.ntx;
@@ -63,7 +66,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned ltmask = lanemask_lt();
 
-  for (int k = threadIdx.x; k < W * W; k += kBlock) {
+  for (int k = threadIdx.x; k < W * W; k += BLK) {
     const int gi = i0 + k % W - 1, gj = j0 + k / W - 1;
     float ex = 0.f, ey = 0.f, ez = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
     if (gi <= p.g.nx + 1 && gj <= p.g.ny + 1) {
@@ -76,7 +79,7 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
     s_ez[k] = ez;
     s_bz[k] = bz;
   }
-  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += kBlock) { s_jhi[k] = 0; s_jlo[k] = 0; }
+  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) { s_jhi[k] = 0; s_jlo[k] = 0; }
 
   const SmemFields F{s_eb1, s_eb2, s_ez, s_bz, W};
   const SmemCurrentFx A{s_jhi, s_jlo, WJ};
@@ -91,33 +94,38 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
     const float jxs = sc.jx * kFxScale, jys = sc.jy * kFxScale, qs = sc.q * kFxScale;
     const int n = ps.cnt[t];
     const long base = (long)t * ps.cap;
+    const bool has_id = ps.nf > F_ID;
+    const int chunk_words = BLK * ps.nf;   // a chunk is BLK / 32 whole AoSoA blocks
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     float ke = 0.f;
     int qn = 0;  // warp-uniform queue fill
+    // this thread's slot of the current chunk (segments and chunks start on 32-slot blocks)
+    uint32_t* pp = ps.slot(base + threadIdx.x);
     // software pipeline: the next chunk's particle is loaded while this one is pushed
     int ncell = 0;
     float nxo = 0.f, nyo = 0.f, nux = 0.f, nuy = 0.f, nuz = 0.f;
     uint32_t nid = 0;
     if ((int)threadIdx.x < n) {
-      const long k = base + threadIdx.x;
-      ncell = __ldcs(ps.cell + k);
-      nxo = __ldcs(ps.x + k); nyo = __ldcs(ps.y + k);
-      nux = __ldcs(ps.ux + k); nuy = __ldcs(ps.uy + k); nuz = __ldcs(ps.uz + k);
-      if (ps.id) nid = __ldcs(ps.id + k);
+      ncell = (int)__ldcs(pp + F_CELL * 32);
+      nxo = __uint_as_float(__ldcs(pp + F_X * 32)); nyo = __uint_as_float(__ldcs(pp + F_Y * 32));
+      nux = __uint_as_float(__ldcs(pp + F_UX * 32)); nuy = __uint_as_float(__ldcs(pp + F_UY * 32));
+      nuz = __uint_as_float(__ldcs(pp + F_UZ * 32));
+      if (has_id) nid = __ldcs(pp + F_ID * 32);
     }
-    for (int c0 = 0; c0 < n; c0 += kBlock) {
+    for (int c0 = 0; c0 < n; c0 += BLK, pp += chunk_words) {
       const int i = c0 + threadIdx.x;
       const bool valid = i < n;
       const int cell = ncell;
       float x = nxo, y = nyo, ux = nux, uy = nuy, uz = nuz;
       const uint32_t id = nid;
-      if (i + kBlock < n) {
-        const long k = base + i + kBlock;
-        ncell = __ldcs(ps.cell + k);
-        nxo = __ldcs(ps.x + k); nyo = __ldcs(ps.y + k);
-        nux = __ldcs(ps.ux + k); nuy = __ldcs(ps.uy + k); nuz = __ldcs(ps.uz + k);
-        if (ps.id) nid = __ldcs(ps.id + k);
+      if (i + BLK < n) {
+        const uint32_t* qn_ = pp + chunk_words;
+        ncell = (int)__ldcs(qn_ + F_CELL * 32);
+        nxo = __uint_as_float(__ldcs(qn_ + F_X * 32)); nyo = __uint_as_float(__ldcs(qn_ + F_Y * 32));
+        nux = __uint_as_float(__ldcs(qn_ + F_UX * 32)); nuy = __uint_as_float(__ldcs(qn_ + F_UY * 32));
+        nuz = __uint_as_float(__ldcs(qn_ + F_UZ * 32));
+        if (has_id) nid = __ldcs(qn_ + F_ID * 32);
       }
       Seg seg[3];
       int nseg = 0, ix = 0, iy = 0;
@@ -140,14 +148,15 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
         else move = domain_bc(ix, iy, p);
       }
       // extra pieces -> this warp's queue; drain full batches of 32 with every lane active
-#pragma unroll
-      for (int k = 1; k < 3; ++k) {
-        const bool has = nseg > k;
-        const unsigned bal = __ballot_sync(0xffffffffu, has);
-        if (has) Q.put(qn + __popc(bal & ltmask), seg[k]);
-        qn += __popc(bal);
+      const unsigned bal1 = __ballot_sync(0xffffffffu, nseg > 1);
+      if (bal1) {   // warp-uniform: most warps of a thermal plasma have a crossing lane, not all
+        if (nseg > 1) Q.put(qn + __popc(bal1 & ltmask), seg[1]);
+        qn += __popc(bal1);
+        const unsigned bal2 = __ballot_sync(0xffffffffu, nseg > 2);
+        if (nseg > 2) Q.put(qn + __popc(bal2 & ltmask), seg[2]);
+        qn += __popc(bal2);
+        __syncwarp();
       }
-      __syncwarp();
       while (qn >= 32) {
         deposit_seg(A, Q.get(lane), jxs, jys);
         __syncwarp();
@@ -162,13 +171,14 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
         __syncwarp();
       }
       if (valid) {
-        const long k = base + i;
         if (stay) {
-          __stcs(ps.cell + k, pack_cell(ix, iy));
-          __stcs(ps.x + k, x); __stcs(ps.y + k, y);
-          __stcs(ps.ux + k, ux); __stcs(ps.uy + k, uy); __stcs(ps.uz + k, uz);
+          const int ncell_ = pack_cell(ix, iy);
+          if (ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);   // ~90 % keep their cell
+          __stcs(pp + F_X * 32, __float_as_uint(x)); __stcs(pp + F_Y * 32, __float_as_uint(y));
+          __stcs(pp + F_UX * 32, __float_as_uint(ux)); __stcs(pp + F_UY * 32, __float_as_uint(uy));
+          __stcs(pp + F_UZ * 32, __float_as_uint(uz));
         } else {
-          ps.cell[k] = kHole;
+          pp[F_CELL * 32] = (uint32_t)kHole;
           const int h = atomicAdd(&s_cnt[0], 1);
           if (h < kHCap) s_holes[h] = i;
           else s_cnt[3] = 1;
@@ -181,49 +191,55 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
       }
     }
     if (lane < qn) deposit_seg(A, Q.get(lane), jxs, jys);
-    block_add_double((double)ke, p.ke_slots + s * kEnergySlots + (t & (kEnergySlots - 1)));  // has barriers
+    // kinetic energy: warp reduction, one shared fp64 add per warp, one global add per CTA
+    for (int o = 16; o > 0; o >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, o);
+    if (lane == 0) atomicAdd(&s_ke[s], (double)ke);
+    __syncthreads();   // all deposits, hole records and in-place writes of this species are done
 
     // ---- re-sort: fill the holes below the new count from the tail --------------------------
     const int nh = s_cnt[0], n2 = n - nh;
     if (nh > 0 && s_cnt[3] == 0) {
-      for (int k = threadIdx.x; k < (nh + 31) / 32; k += kBlock) s_bits[k] = 0u;
-      __syncthreads();
-      for (int k = threadIdx.x; k < nh; k += kBlock) {
-        const int pos = s_holes[k];
-        if (pos >= n2) atomicOr(&s_bits[(pos - n2) >> 5], 1u << ((pos - n2) & 31));
-      }
-      __syncthreads();
-      for (int k = threadIdx.x; k < nh; k += kBlock) {
-        const int pos = s_holes[k];
-        if (pos < n2) s_hb[atomicAdd(&s_cnt[1], 1)] = pos;
-        const int q = n2 + k;   // the tail [n2, n) has exactly nh slots
-        if (!((s_bits[k >> 5] >> (k & 31)) & 1u)) s_sa[atomicAdd(&s_cnt[2], 1)] = q;
-      }
-      __syncthreads();
-      const int nmove = s_cnt[1];
-      for (int k = threadIdx.x; k < nmove; k += kBlock) {
-        const long d = base + s_hb[k], sidx = base + s_sa[k];
-        ps.cell[d] = ps.cell[sidx];
-        ps.x[d] = ps.x[sidx]; ps.y[d] = ps.y[sidx];
-        ps.ux[d] = ps.ux[sidx]; ps.uy[d] = ps.uy[sidx]; ps.uz[d] = ps.uz[sidx];
-        if (ps.id) ps.id[d] = ps.id[sidx];
+      if (warp == 0) {   // one warp, warp-synchronous: the other warps go on (J flush / next species)
+        for (int k = lane; k < (nh + 31) / 32; k += 32) s_bits[k] = 0u;
+        __syncwarp();
+        for (int k = lane; k < nh; k += 32) {
+          const int pos = s_holes[k];
+          if (pos >= n2) atomicOr(&s_bits[(pos - n2) >> 5], 1u << ((pos - n2) & 31));
+        }
+        __syncwarp();
+        int nhb = 0, nsa = 0;
+        for (int k0 = 0; k0 < nh; k0 += 32) {
+          const int k = k0 + lane;
+          const int pos = k < nh ? s_holes[k] : n2;
+          const bool hb = k < nh && pos < n2;                                   // hole below the new count
+          const bool sa = k < nh && !((s_bits[k >> 5] >> (k & 31)) & 1u);      // tail slot n2 + k holds a stayer
+          const unsigned mb = __ballot_sync(0xffffffffu, hb), ms = __ballot_sync(0xffffffffu, sa);
+          if (hb) s_hb[nhb + __popc(mb & ltmask)] = pos;
+          if (sa) s_sa[nsa + __popc(ms & ltmask)] = n2 + k;
+          nhb += __popc(mb);
+          nsa += __popc(ms);
+        }
+        __syncwarp();
+        for (int k = lane; k < nhb; k += 32) {
+          uint32_t* d = ps.slot(base + s_hb[k]);
+          const uint32_t* src = ps.slot(base + s_sa[k]);
+          for (int f = 0; f < ps.nf; ++f) d[f * 32] = src[f * 32];
+        }
       }
     } else if (nh > 0) {
       // more holes than the list holds: stable compaction of the whole segment by the sentinel
       __syncthreads();
       int out = 0, buf = 0;
-      for (int c0 = 0; c0 < n; c0 += kBlock) {
+      for (int c0 = 0; c0 < n; c0 += BLK) {
         const int i = c0 + threadIdx.x;
-        int cell = kHole;
-        float x = 0.f, y = 0.f, ux = 0.f, uy = 0.f, uz = 0.f;
-        uint32_t id = 0;
+        uint32_t v[7] = {(uint32_t)kHole, 0u, 0u, 0u, 0u, 0u, 0u};
         if (i < n) {
-          const long k = base + i;
-          cell = ps.cell[k];
-          x = ps.x[k]; y = ps.y[k]; ux = ps.ux[k]; uy = ps.uy[k]; uz = ps.uz[k];
-          if (ps.id) id = ps.id[k];
+          const uint32_t* src = ps.slot(base + i);
+#pragma unroll
+          for (int f = 0; f < 7; ++f)
+            if (f < ps.nf) v[f] = src[f * 32];
         }
-        const bool keep = cell != kHole;
+        const bool keep = (int)v[F_CELL] != kHole;
         const unsigned bal = __ballot_sync(0xffffffffu, keep);
         if (lane == 0) s_wsum[buf][warp] = __popc(bal);
         __syncthreads();
@@ -234,40 +250,62 @@ __global__ void __launch_bounds__(kBlock, 4) k_push_tiles(PushParams p) {
           tot += v;
         }
         buf ^= 1;
+        __syncthreads();   // every thread has read its slot before any slot of this chunk is rewritten
         if (keep) {
-          const long k = base + out + before + __popc(bal & ltmask);
-          ps.cell[k] = cell; ps.x[k] = x; ps.y[k] = y; ps.ux[k] = ux; ps.uy[k] = uy; ps.uz[k] = uz;
-          if (ps.id) ps.id[k] = id;
+          uint32_t* d = ps.slot(base + out + before + __popc(bal & ltmask));
+#pragma unroll
+          for (int f = 0; f < 7; ++f)
+            if (f < ps.nf) d[f * 32] = v[f];
         }
         out += tot;
       }
     }
     if (threadIdx.x == 0) ps.cnt[t] = n2;
-    __syncthreads();
+    if (s + 1 < p.nspecies) __syncthreads();   // the hole lists / counters are reused by the next species
   }
   float* jt = p.Jt + (long)t * 3 * WJ * WJ;
-  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += kBlock)
+  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK)
     __stcg(jt + k, (float)(fma((double)s_jhi[k], 32768.0, (double)s_jlo[k]) * kFxInv));
+  if (threadIdx.x < p.nspecies && s_ke[threadIdx.x] != 0.0)
+    atomicAdd(p.ke_slots + threadIdx.x * kEnergySlots + (t & (kEnergySlots - 1)), s_ke[threadIdx.x]);
 }
 
-template <int T>
+template <int T, int BLK, int MINB>
 static void launch_push_T(const PushParams& p, int ntiles, cudaStream_t st) {
   constexpr int W = T + 2, WJ = T + 3;
   constexpr size_t smem = (size_t)W * W * (2 * sizeof(float2) + 2 * sizeof(float)) + (size_t)6 * WJ * WJ * sizeof(int) +
-                          (size_t)6 * (kBlock / 32) * kQCap * sizeof(int);
+                          (size_t)6 * (BLK / 32) * kQCap * sizeof(int);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_push_tiles<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_push_tiles<T, BLK, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = true;
   }
-  k_push_tiles<T><<<ntiles, kBlock, smem, st>>>(p);
+  k_push_tiles<T, BLK, MINB><<<ntiles, BLK, smem, st>>>(p);
+}
+
+// K1 launch shape for 16x16 tiles (threads per CTA, CTAs per SM the register budget is sized
+// for).  ZPIC_K1_SHAPE selects it for tuning experiments: 0 = 256 x 3 (80 registers),
+// 1 = 256 x 4 (64 registers), 2 = 128 x 6 (80 registers), 3 = 128 x 8 (64 registers).
+static int k1_shape() {
+  static int v = [] {
+    const char* e = getenv("ZPIC_K1_SHAPE");
+    return e ? atoi(e) : 2;
+  }();
+  return v;
 }
 
 void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st) {
   switch (p.T) {
-    case 8: launch_push_T<8>(p, ntiles, st); break;
-    case 16: launch_push_T<16>(p, ntiles, st); break;
-    case 32: launch_push_T<32>(p, ntiles, st); break;
+    case 8: launch_push_T<8, 128, 8>(p, ntiles, st); break;
+    case 16:
+      switch (k1_shape()) {
+        case 0: launch_push_T<16, 256, 3>(p, ntiles, st); break;
+        case 1: launch_push_T<16, 256, 4>(p, ntiles, st); break;
+        case 3: launch_push_T<16, 128, 8>(p, ntiles, st); break;
+        default: launch_push_T<16, 128, 6>(p, ntiles, st); break;
+      }
+      break;
+    case 32: launch_push_T<32, 256, 2>(p, ntiles, st); break;
   }
 }
 

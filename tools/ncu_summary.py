@@ -18,6 +18,14 @@ for r in rows[2:]:
     for i, n in enumerate(h):
         if n in want:
             print("%-58s %-12s %s" % (n, units[i], r[i]))
+    st = [(float(r[i].replace(",", "")), n) for i, n in enumerate(h)
+          if n.startswith("smsp__pcsamp_warps_issue_stalled_") and not n.endswith("_not_issued")
+          and r[i] not in ("", "n/a")]
+    if st:
+        tot = sum(v for v, _ in st)
+        print("  stall reasons (share of warp-cycles per issued instruction):")
+        for v, n in sorted(st, reverse=True)[:10]:
+            print("    %-40s %5.1f%%" % (n.replace("smsp__pcsamp_warps_issue_stalled_", ""), 100 * v / tot))
 src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(src.splitlines()))
