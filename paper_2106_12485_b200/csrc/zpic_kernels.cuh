@@ -9,12 +9,12 @@ namespace zpic {
 // ---- field accessors -----------------------------------------------------------------------
 // Tile-staged fields: (Ex, By) share the (1/2, 0) stagger, (Ey, Bx) share (0, 1/2); Ez (0, 0),
 // Bz (1/2, 1/2).  Arrays cover local cells [-1, T+1) in both axes, row width W = T + 2.
+template <int W>   // row width (compile-time, so stencil offsets are immediates)
 struct SmemFields {
   const float2* eb1;  // (Ex, By)
   const float2* eb2;  // (Ey, Bx)
   const float* ez;
   const float* bz;
-  int W;
   __device__ __forceinline__ int o(int lx, int ly) const { return (ly + 1) * W + (lx + 1); }
   __device__ __forceinline__ void hi(int i, int j, float wx, float wy, float& ex, float& by) const {
     float2 a = eb1[o(i, j)], b = eb1[o(i + 1, j)], c = eb1[o(i, j + 1)], d = eb1[o(i + 1, j + 1)];
@@ -74,10 +74,10 @@ struct GlobalFields {
 // [-1, T+2), row width WJ = T + 3.
 constexpr float kFxScale = 4294967296.0f;  // 2^32
 constexpr double kFxInv = 2.3283064365386963e-10;  // 2^-32
+template <int WJ>   // row width (compile-time)
 struct SmemCurrentFx {
   int* hi;
   int* lo;
-  int WJ;
   __device__ __forceinline__ void add(int c, int i, int k, float v) const {
     const long long V = __float2ll_rn(v);
     const int o = c * WJ * WJ + (k + 1) * WJ + (i + 1);
@@ -138,46 +138,32 @@ struct Seg {
 // Villasenor-Buneman split of the path (x, y) -> (x + dxp, y + dyp) from local cell (lx, ly)
 // into 1-3 straight pieces at the cell edges it crosses (at most one per axis),
 // in time order; returns the piece count, the cell steps (di, dj) and the renormalised offset
-// with the R6 rounding rule.  Pieces beyond the count are left untouched.
+// with the R6 rounding rule.  Branch-free: with the edge-crossing times tx, ty (2 = no
+// crossing) sorted into t1 <= t2 (clamped to 1), the pieces are [0, t1] in the start cell,
+// [t1, t2] in the cell across the first edge and [t2, 1] in the final cell; a crossed
+// coordinate is pinned to the exact edge value.  Pieces beyond the count have zero length.
 __device__ __forceinline__ int split_path(int lx, int ly, float& x, float& y, float dxp, float dyp, float qvz, Seg* s,
                                           int& di, int& dj) {
   const float x1 = x + dxp, y1 = y + dyp;
   di = (x1 >= 1.0f) - (x1 < 0.0f);
   dj = (y1 >= 1.0f) - (y1 < 0.0f);
-  int n;
-  if ((di | dj) == 0) {
-    s[0] = Seg{lx, ly, x, y, x1, y1, qvz};
-    n = 1;
-  } else if (dj == 0) {
-    const float xb = di > 0 ? 1.0f : 0.0f;
-    const float t = (xb - x) / dxp;
-    const float yb = fmaf(t, dyp, y);
-    s[0] = Seg{lx, ly, x, y, xb, yb, qvz * t};
-    s[1] = Seg{lx + di, ly, xb - di, yb, x1 - di, y1, qvz * (1.0f - t)};
-    n = 2;
-  } else if (di == 0) {
-    const float yb = dj > 0 ? 1.0f : 0.0f;
-    const float t = (yb - y) / dyp;
-    const float xb = fmaf(t, dxp, x);
-    s[0] = Seg{lx, ly, x, y, xb, yb, qvz * t};
-    s[1] = Seg{lx, ly + dj, xb, yb - dj, x1, y1 - dj, qvz * (1.0f - t)};
-    n = 2;
-  } else {
-    const float xb = di > 0 ? 1.0f : 0.0f, yb = dj > 0 ? 1.0f : 0.0f;
-    const float tx = (xb - x) / dxp, ty = (yb - y) / dyp;
-    if (tx <= ty) {  // x edge first
-      const float yx = fmaf(tx, dyp, y), xy = fmaf(ty, dxp, x);
-      s[0] = Seg{lx, ly, x, y, xb, yx, qvz * tx};
-      s[1] = Seg{lx + di, ly, xb - di, yx, xy - di, yb, qvz * (ty - tx)};
-      s[2] = Seg{lx + di, ly + dj, xy - di, yb - dj, x1 - di, y1 - dj, qvz * (1.0f - ty)};
-    } else {         // y edge first
-      const float xy = fmaf(ty, dxp, x), yx = fmaf(tx, dyp, y);
-      s[0] = Seg{lx, ly, x, y, xy, yb, qvz * ty};
-      s[1] = Seg{lx, ly + dj, xy, yb - dj, xb, yx - dj, qvz * (tx - ty)};
-      s[2] = Seg{lx + di, ly + dj, xb - di, yx - dj, x1 - di, y1 - dj, qvz * (1.0f - tx)};
-    }
-    n = 3;
-  }
+  const float xb = di > 0 ? 1.0f : 0.0f, yb = dj > 0 ? 1.0f : 0.0f;
+  const float tx = di ? __fdividef(xb - x, dxp) : 2.0f;
+  const float ty = dj ? __fdividef(yb - y, dyp) : 2.0f;
+  const bool xfirst = tx <= ty;
+  const float t1 = fminf(fminf(tx, ty), 1.0f), t2 = fminf(fmaxf(tx, ty), 1.0f);
+  // the path at t1 and t2 (start-cell offsets); the coordinate crossing an edge at that time is
+  // pinned to the edge (t2 = 1 gives exactly x1, y1 since fma(1, d, x) = x + d)
+  const bool both = di && dj;
+  const float xa = (di && xfirst) ? xb : fmaf(t1, dxp, x);
+  const float ya = (dj && !xfirst) ? yb : fmaf(t1, dyp, y);
+  const float xc = (both && !xfirst) ? xb : fmaf(t2, dxp, x);
+  const float yc = (both && xfirst) ? yb : fmaf(t2, dyp, y);
+  const int c1x = xfirst ? di : 0, c1y = xfirst ? 0 : dj;   // cell across the first edge
+  s[0] = Seg{lx, ly, x, y, xa, ya, qvz * t1};
+  s[1] = Seg{lx + c1x, ly + c1y, xa - c1x, ya - c1y, xc - c1x, yc - c1y, qvz * (t2 - t1)};
+  s[2] = Seg{lx + di, ly + dj, xc - di, yc - dj, x1 - di, y1 - dj, qvz * (1.0f - t2)};
+  const int n = 1 + (di != 0) + (dj != 0);
   float xn = x1 - di, yn = y1 - dj;
   if (xn >= 1.0f) { xn = 0.0f; di += 1; }   // R6: only reachable when x1 < 0 rounds to 1
   if (yn >= 1.0f) { yn = 0.0f; dj += 1; }

@@ -81,8 +81,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
   }
   for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) { s_jhi[k] = 0; s_jlo[k] = 0; }
 
-  const SmemFields F{s_eb1, s_eb2, s_ez, s_bz, W};
-  const SmemCurrentFx A{s_jhi, s_jlo, WJ};
+  const SmemFields<W> F{s_eb1, s_eb2, s_ez, s_bz};
+  const SmemCurrentFx<WJ> A{s_jhi, s_jlo};
   const int qo = warp * kQCap;
   const SegQueue Q{s_q + qo, reinterpret_cast<float*>(s_q + NW * kQCap + qo),
                    reinterpret_cast<float*>(s_q + 2 * NW * kQCap + qo), reinterpret_cast<float*>(s_q + 3 * NW * kQCap + qo),
