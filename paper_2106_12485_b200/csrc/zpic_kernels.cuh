@@ -74,21 +74,27 @@ struct GlobalFields {
 // [-1, T+2), row width WJ = T + 3.
 constexpr float kFxScale = 4294967296.0f;  // 2^32
 constexpr double kFxInv = 2.3283064365386963e-10;  // 2^-32
+// Accumulator interface: index(i, k) = the linear index of node (i, k) in a component plane;
+// row() = the index step to (i, k+1); add(c, idx + offset, v).  The deposit computes one index
+// per path piece and reaches the other three nodes by constant offsets.
 template <int WJ>   // row width (compile-time)
 struct SmemCurrentFx {
   int* hi;
   int* lo;
-  __device__ __forceinline__ void add(int c, int i, int k, float v) const {
+  __device__ __forceinline__ int index(int i, int k) const { return (k + 1) * WJ + (i + 1); }
+  __device__ __forceinline__ int row() const { return WJ; }
+  __device__ __forceinline__ void add(int c, int o, float v) const {
     const long long V = __float2ll_rn(v);
-    const int o = c * WJ * WJ + (k + 1) * WJ + (i + 1);
-    atomicAdd(hi + o, (int)(V >> 15));
-    atomicAdd(lo + o, (int)(V & 0x7fff));
+    atomicAdd(hi + c * WJ * WJ + o, (int)(V >> 15));
+    atomicAdd(lo + c * WJ * WJ + o, (int)(V & 0x7fff));
   }
 };
 struct GlobalCurrent {
   float* J;
   GridDesc g;
-  __device__ __forceinline__ void add(int c, int i, int k, float v) const { atomicAdd(J + c * g.plane + g.at(i, k), v); }
+  __device__ __forceinline__ long index(int i, int k) const { return g.at(i, k); }
+  __device__ __forceinline__ long row() const { return g.pitch; }
+  __device__ __forceinline__ void add(int c, long o, float v) const { atomicAdd(J + c * g.plane + o, v); }
 };
 
 // ---- (1) interpolation, PAPER.md:144 -------------------------------------------------------
@@ -177,15 +183,17 @@ __device__ __forceinline__ void deposit_seg(const A& acc, const Seg& s, float jx
   const float da = s.a1 - s.a0, db = s.b1 - s.b0;
   const float xm = 0.5f * (s.a0 + s.a1), ym = 0.5f * (s.b0 + s.b1);
   const float wx = jxs * da, wy = jys * db;
-  acc.add(0, s.cx, s.cy, wx * (1.0f - ym));
-  acc.add(0, s.cx, s.cy + 1, wx * ym);
-  acc.add(1, s.cx, s.cy, wy * (1.0f - xm));
-  acc.add(1, s.cx + 1, s.cy, wy * xm);
+  const auto o = acc.index(s.cx, s.cy);
+  const auto r = acc.row();
+  acc.add(0, o, wx * (1.0f - ym));
+  acc.add(0, o + r, wx * ym);
+  acc.add(1, o, wy * (1.0f - xm));
+  acc.add(1, o + 1, wy * xm);
   const float c = da * db * (1.0f / 12.0f);
-  acc.add(2, s.cx, s.cy, s.wz * fmaf(1.0f - xm, 1.0f - ym, c));
-  acc.add(2, s.cx + 1, s.cy, s.wz * fmaf(xm, 1.0f - ym, -c));
-  acc.add(2, s.cx, s.cy + 1, s.wz * fmaf(1.0f - xm, ym, -c));
-  acc.add(2, s.cx + 1, s.cy + 1, s.wz * fmaf(xm, ym, c));
+  acc.add(2, o, s.wz * fmaf(1.0f - xm, 1.0f - ym, c));
+  acc.add(2, o + 1, s.wz * fmaf(xm, 1.0f - ym, -c));
+  acc.add(2, o + r, s.wz * fmaf(1.0f - xm, ym, -c));
+  acc.add(2, o + r + 1, s.wz * fmaf(xm, ym, c));
 }
 
 }  // namespace zpic
