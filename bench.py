@@ -35,6 +35,15 @@ def dist_env():
     return world, rank, local
 
 
+def k1_traffic(config, nx, ny):
+    """DRAM bytes per K1 launch from the committed ncu capture of the same workload
+    (profiles/r1_k1_traffic_c5.json), else None."""
+    p = os.path.join(ROOT, "profiles", "r1_k1_traffic_c5.json")
+    if config == "C5" and (nx, ny) == (8192, 8192) and os.path.exists(p):
+        return json.load(open(p))["per_launch_bytes"]
+    return None
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -273,7 +282,9 @@ def main():
         "cell_updates_per_s": n_cells * args.steps / (ms * 1e-3),
         "k1_pushes_per_s": cnt["particles"] / k1_avg_s,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": None, "kernel": "k_push_tiles", "peak_kind": peak_kind,
+                     "traffic": k1_traffic(args.config, cfg["nx"], cfg["ny"]) if world == 1 else None,
+                     "traffic_source": "profiles/r1_k1_traffic_c5.json (ncu dram__bytes_read+write, C5)",
+                     "kernel": "k_push_tiles", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg_s * 1e3},
         "kernel_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in kt.items() if v[1]},
         "gpu_launches": launches,

@@ -232,6 +232,8 @@ PushParams push_params(zpic_ctx* c) {
   p.slab = c->slab;
   p.has_lo = c->has_lo;
   p.has_hi = c->has_hi;
+  static const int skip = [] { const char* e = getenv("ZPIC_SKIP_CELL_STORE"); return e ? atoi(e) : 0; }();
+  p.skip_cell_store = skip;
   if (c->slab) {
     p.send[0] = particle_msg_list(c->pmsg_send[0], c->pcap);
     p.send[1] = particle_msg_list(c->pmsg_send[1], c->pcap);

@@ -81,6 +81,7 @@ struct PushParams {
   // slab go to send[0] (down, iy += ny) or send[1] (up, iy -= ny).
   int slab, has_lo, has_hi;
   PList send[2];
+  int skip_cell_store;  // tuning switch: write the cell word only when it changed
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
   int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
 };

@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
       if (valid) {
         if (stay) {
           const int ncell_ = pack_cell(ix, iy);
-          if (ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);   // ~90 % keep their cell
+          if (!p.skip_cell_store || ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);
           __stcs(pp + F_X * 32, __float_as_uint(x)); __stcs(pp + F_Y * 32, __float_as_uint(y));
           __stcs(pp + F_UX * 32, __float_as_uint(ux)); __stcs(pp + F_UY * 32, __float_as_uint(uy));
           __stcs(pp + F_UZ * 32, __float_as_uint(uz));
