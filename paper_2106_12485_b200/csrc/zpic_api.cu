@@ -106,15 +106,15 @@ void alloc_store(zpic_ctx* c, int s, int cap) {
   ps.cnt = alloc_n<int32_t>(c, c->ntiles);
 }
 
-// The tile current is accumulated as exact fixed point whose low halves must stay below 2^31:
-// a node receives at most 3 contributions per particle of the tile (one per sub-segment), each
-// below 2^15, so all species together may hold at most 21845 particles per tile.
+// The tile current is accumulated as fixed point with a per-tile scale 2^S chosen from the
+// tile's particle count (zpic_kernels.cuh fx_scale_exponent), which needs 2 * (particles per
+// tile) well below 2^31; 2^24 particles per tile is the sanity limit.
 void check_tile_capacity(zpic_ctx* c) {
   long total = 0;
   for (int s = 0; s < c->nspecies; ++s) total += c->ps[s].cap;
-  if (total > 21845)
+  if (total > (1L << 24))
     throw Fail{ZPIC_E_INVALID, "tile capacity " + std::to_string(total) +
-                                   " > 21845 particles (fixed-point current range): use a smaller tile"};
+                                   " > 2^24 particles (fixed-point current range): use a smaller tile"};
 }
 
 void free_store(zpic_ctx* c, int s) {

@@ -63,21 +63,33 @@ struct GlobalFields {
 };
 
 // ---- current accumulators ----------------------------------------------------------------
-// Shared-memory tile current as exact fixed point: every contribution v (already scaled by
-// kFxScale = 2^32, a power of two, so the scaling is exact) is rounded once to an int64
-// V = rint(v), split V = hi * 2^15 + lo with 0 <= lo < 2^15, and both halves are added with
-// native 32-bit shared-memory integer atomics (sm_100a has no native fp32 shared atomic add: it
-// compiles to a CAS loop).  Integer sums are exact and order-independent, so the tile current
-// is bit-reproducible; the only error is the 2^-33 rounding of each contribution.  Ranges:
-// |sum v| < 2^14 per node; lo sums stay below 2^31 for < 21845 contributions per node (the tile
-// capacity is capped accordingly, zpic_api.cu).  3 planes x 2 halves cover local nodes
-// [-1, T+2), row width WJ = T + 3.
-constexpr float kFxScale = 4294967296.0f;  // 2^32
-constexpr double kFxInv = 2.3283064365386963e-10;  // 2^-32
+// Shared-memory tile current as fixed point with one native 32-bit integer atomic per node
+// (sm_100a has no native fp32 shared-memory atomic add: it compiles to a CAS loop).  Every
+// contribution v is pre-scaled by the CTA's power of two 2^S (exact) and rounded once to an
+// int32; the integer sums are exact and order-independent, so the tile current is
+// bit-reproducible, and the only error is the rounding of each contribution to 2^-(S+1).
+// S is chosen per CTA from a bound on |J| (fx_scale_exponent): every particle adds at most |q|
+// in absolute value to any node of any component (|v| < 1 and the pieces' weights sum to 1), so
+// |sum| <= sum_s n_s |q_s| over the tile's particles.  3 planes cover local nodes [-1, T+2),
+// row width WJ = T + 3.
 // Accumulator interface: index(i, k) = the linear index of node (i, k) in a component plane;
 // row() = the index step to (i, k+1); add(c, idx + offset, v).  The deposit computes one index
 // per path piece and reaches the other three nodes by constant offsets.
 template <int WJ>   // row width (compile-time)
+struct SmemCurrentI32 {
+  int* j;
+  __device__ __forceinline__ int index(int i, int k) const { return (k + 1) * WJ + (i + 1); }
+  __device__ __forceinline__ int row() const { return WJ; }
+  __device__ __forceinline__ void add(int c, int o, float v) const { atomicAdd(j + c * WJ * WJ + o, __float2int_rn(v)); }
+};
+// The exact two-word form, used for tiles whose bound would leave S < kSMin (dense tiles): every
+// contribution is scaled by 2^32 and rounded once to an int64 V, split V = hi * 2^15 + lo with
+// 0 <= lo < 2^15, and both halves are added with 32-bit atomics (|sum| < 2^14 per node, lo sums
+// below 2^31 for < 21845 contributions per node).  Per contribution the error is <= 2^-33.
+constexpr int kSMin = 22;
+constexpr float kFxScale = 4294967296.0f;          // 2^32
+constexpr double kFxInv = 2.3283064365386963e-10;  // 2^-32
+template <int WJ>
 struct SmemCurrentFx {
   int* hi;
   int* lo;
@@ -89,6 +101,14 @@ struct SmemCurrentFx {
     atomicAdd(lo + c * WJ * WJ + o, (int)(V & 0x7fff));
   }
 };
+// Largest S such that bound * 2^S plus the rounding of up to 3 * npart contributions per node
+// stays below 2^31 (bound = sum_s n_s |q_s|); 32 for an empty tile.
+__device__ __forceinline__ int fx_scale_exponent(double bound, int npart) {
+  if (!(bound > 0.0)) return 32;
+  int e;
+  frexp((2147483648.0 - 2.0 * npart - 1024.0) / bound, &e);   // ratio = m 2^e, m in [0.5, 1)
+  return min(e - 1, 40);
+}
 struct GlobalCurrent {
   float* J;
   GridDesc g;
@@ -110,6 +130,39 @@ __device__ __forceinline__ void interpolate(const F& f, int lx, int ly, float x,
   f.ih(lx, jh, x, wyh, ey, bx);
   ez = f.fez(lx, ly, x, y);
   bz = f.fbz(ih, jh, wxh, wyh);
+}
+
+// Packed fp32x2 form for the shared-memory tile (sm_100a FFMA2: two lanes of fp32 per
+// instruction): the pairs (Ex, By), (Ey, Bx) share their stencil and weights, and (Ez, Bz) pair
+// two stencils with per-lane weights.  Each lerp is fma(w, b - a, a) with b - a = fma(a, -1, b),
+// the same roundings as the scalar form.
+__device__ __forceinline__ float2 lerp2(float2 a, float2 b, float2 w) {
+  const float2 d = __ffma2_rn(a, make_float2(-1.0f, -1.0f), b);
+  return __ffma2_rn(w, d, a);
+}
+template <int W>
+__device__ __forceinline__ void interpolate(const SmemFields<W>& f, int lx, int ly, float x, float y, float& ex,
+                                            float& ey, float& ez, float& bx, float& by, float& bz) {
+  const bool xl = x < 0.5f, yl = y < 0.5f;
+  const int ih = xl ? lx - 1 : lx, jh = yl ? ly - 1 : ly;
+  const float wxh = xl ? x + 0.5f : x - 0.5f, wyh = yl ? y + 0.5f : y - 0.5f;
+  const int oa = f.o(ih, ly), ob = f.o(lx, jh), oz = f.o(lx, ly), oh = f.o(ih, jh);
+  // (Ex, By) at (ih, ly) with weights (wxh, y)
+  float2 l0 = lerp2(f.eb1[oa], f.eb1[oa + 1], make_float2(wxh, wxh));
+  float2 l1 = lerp2(f.eb1[oa + W], f.eb1[oa + W + 1], make_float2(wxh, wxh));
+  const float2 r1 = lerp2(l0, l1, make_float2(y, y));
+  // (Ey, Bx) at (lx, jh) with weights (x, wyh)
+  l0 = lerp2(f.eb2[ob], f.eb2[ob + 1], make_float2(x, x));
+  l1 = lerp2(f.eb2[ob + W], f.eb2[ob + W + 1], make_float2(x, x));
+  const float2 r2 = lerp2(l0, l1, make_float2(wyh, wyh));
+  // (Ez at (lx, ly) weights (x, y), Bz at (ih, jh) weights (wxh, wyh))
+  const float2 wx = make_float2(x, wxh), wy = make_float2(y, wyh);
+  l0 = lerp2(make_float2(f.ez[oz], f.bz[oh]), make_float2(f.ez[oz + 1], f.bz[oh + 1]), wx);
+  l1 = lerp2(make_float2(f.ez[oz + W], f.bz[oh + W]), make_float2(f.ez[oz + W + 1], f.bz[oh + W + 1]), wx);
+  const float2 r3 = lerp2(l0, l1, wy);
+  ex = r1.x; by = r1.y;
+  ey = r2.x; bx = r2.y;
+  ez = r3.x; bz = r3.y;
 }
 
 // ---- (2) relativistic Boris, PAPER.md:144-145 -------------------------------------------------
@@ -141,41 +194,67 @@ struct Seg {
   float a0, b0, a1, b1, wz;
 };
 
-// Villasenor-Buneman split of the path (x, y) -> (x + dxp, y + dyp) from local cell (lx, ly)
-// into 1-3 straight pieces at the cell edges it crosses (at most one per axis),
-// in time order; returns the piece count, the cell steps (di, dj) and the renormalised offset
-// with the R6 rounding rule.  Branch-free: with the edge-crossing times tx, ty (2 = no
-// crossing) sorted into t1 <= t2 (clamped to 1), the pieces are [0, t1] in the start cell,
-// [t1, t2] in the cell across the first edge and [t2, 1] in the final cell; a crossed
-// coordinate is pinned to the exact edge value.  Pieces beyond the count have zero length.
-__device__ __forceinline__ int split_path(int lx, int ly, float& x, float& y, float dxp, float dyp, float qvz, Seg* s,
-                                          int& di, int& dj) {
-  const float x1 = x + dxp, y1 = y + dyp;
-  di = (x1 >= 1.0f) - (x1 < 0.0f);
-  dj = (y1 >= 1.0f) - (y1 < 0.0f);
-  const float xb = di > 0 ? 1.0f : 0.0f, yb = dj > 0 ? 1.0f : 0.0f;
-  const float tx = di ? __fdividef(xb - x, dxp) : 2.0f;
-  const float ty = dj ? __fdividef(yb - y, dyp) : 2.0f;
-  const bool xfirst = tx <= ty;
-  const float t1 = fminf(fminf(tx, ty), 1.0f), t2 = fminf(fmaxf(tx, ty), 1.0f);
-  // the path at t1 and t2 (start-cell offsets); the coordinate crossing an edge at that time is
-  // pinned to the edge (t2 = 1 gives exactly x1, y1 since fma(1, d, x) = x + d)
-  const bool both = di && dj;
-  const float xa = (di && xfirst) ? xb : fmaf(t1, dxp, x);
-  const float ya = (dj && !xfirst) ? yb : fmaf(t1, dyp, y);
-  const float xc = (both && !xfirst) ? xb : fmaf(t2, dxp, x);
-  const float yc = (both && xfirst) ? yb : fmaf(t2, dyp, y);
-  const int c1x = xfirst ? di : 0, c1y = xfirst ? 0 : dj;   // cell across the first edge
-  s[0] = Seg{lx, ly, x, y, xa, ya, qvz * t1};
-  s[1] = Seg{lx + c1x, ly + c1y, xa - c1x, ya - c1y, xc - c1x, yc - c1y, qvz * (t2 - t1)};
-  s[2] = Seg{lx + di, ly + dj, xc - di, yc - dj, x1 - di, y1 - dj, qvz * (1.0f - t2)};
-  const int n = 1 + (di != 0) + (dj != 0);
+// Cell-edge crossings of the straight path (x, y) -> (x1, y1) = (x + dxp, y + dyp) from the
+// start cell (at most one per axis, Villasenor-Buneman).  Branch-free: with the
+// edge-crossing times tx, ty (2 = no crossing) sorted into t1 <= t2 (clamped to 1), the pieces
+// are [0, t1] in the start cell, [t1, t2] in the cell across the first edge and [t2, 1] in the
+// final cell; a crossed coordinate is pinned to the exact edge value (t = 1 gives exactly x1, y1
+// since fma(1, d, x) = x + d).  The same inline arithmetic runs for the first piece in the main
+// loop and for the later pieces in the queue drain, so the pieces chain bit-exactly.
+struct Crossing {
+  int di, dj;              // cell steps of the end point (before the R6 rule)
+  bool xfirst;             // the x edge is crossed first (or together)
+  float t1, t2;            // piece boundaries in path time
+  float xa, ya, xc, yc;    // path points at t1, t2 (start-cell offsets)
+};
+__device__ __forceinline__ Crossing path_crossings(float x, float y, float dxp, float dyp, float x1, float y1) {
+  Crossing c;
+  c.di = (x1 >= 1.0f) - (x1 < 0.0f);
+  c.dj = (y1 >= 1.0f) - (y1 < 0.0f);
+  const float xb = c.di > 0 ? 1.0f : 0.0f, yb = c.dj > 0 ? 1.0f : 0.0f;
+  const float tx = c.di ? __fdividef(xb - x, dxp) : 2.0f;
+  const float ty = c.dj ? __fdividef(yb - y, dyp) : 2.0f;
+  c.xfirst = tx <= ty;
+  c.t1 = fminf(fminf(tx, ty), 1.0f);
+  c.t2 = fminf(fmaxf(tx, ty), 1.0f);
+  const bool both = c.di && c.dj;
+  c.xa = (c.di && c.xfirst) ? xb : fmaf(c.t1, dxp, x);
+  c.ya = (c.dj && !c.xfirst) ? yb : fmaf(c.t1, dyp, y);
+  c.xc = (both && !c.xfirst) ? xb : fmaf(c.t2, dxp, x);
+  c.yc = (both && c.xfirst) ? yb : fmaf(c.t2, dyp, y);
+  return c;
+}
+
+// The pieces after the first (only for a path that crosses an edge): [t1, t2] in the cell across
+// the first edge, and [t2, 1] in the final cell (zero length unless both edges are crossed).
+__device__ __forceinline__ void later_pieces(int lx, int ly, float x1, float y1, float qvz, const Crossing& c, Seg& s1,
+                                             Seg& s2) {
+  const int c1x = c.xfirst ? c.di : 0, c1y = c.xfirst ? 0 : c.dj;   // cell across the first edge
+  s1 = Seg{lx + c1x, ly + c1y, c.xa - c1x, c.ya - c1y, c.xc - c1x, c.yc - c1y, qvz * (c.t2 - c.t1)};
+  s2 = Seg{lx + c.di, ly + c.dj, c.xc - c.di, c.yc - c.dj, x1 - c.di, y1 - c.dj, qvz * (1.0f - c.t2)};
+}
+
+// Renormalised end offset with the R6 rounding rule (an offset that renormalises to exactly 1
+// becomes 0 in the next cell; only reachable when x1 < 0 rounds to 1).
+__device__ __forceinline__ void renormalise(float x1, float y1, int& di, int& dj, float& x, float& y) {
   float xn = x1 - di, yn = y1 - dj;
-  if (xn >= 1.0f) { xn = 0.0f; di += 1; }   // R6: only reachable when x1 < 0 rounds to 1
+  if (xn >= 1.0f) { xn = 0.0f; di += 1; }
   if (yn >= 1.0f) { yn = 0.0f; dj += 1; }
   x = xn;
   y = yn;
-  return n;
+}
+
+// The whole split (1-3 pieces in time order) for the loose-particle kernel.
+__device__ __forceinline__ int split_path(int lx, int ly, float& x, float& y, float dxp, float dyp, float qvz, Seg* s,
+                                          int& di, int& dj) {
+  const float x1 = x + dxp, y1 = y + dyp;
+  const Crossing c = path_crossings(x, y, dxp, dyp, x1, y1);
+  s[0] = Seg{lx, ly, x, y, c.xa, c.ya, qvz * c.t1};
+  later_pieces(lx, ly, x1, y1, qvz, c, s[1], s[2]);
+  di = c.di;
+  dj = c.dj;
+  renormalise(x1, y1, di, dj, x, y);
+  return 1 + (c.di != 0) + (c.dj != 0);
 }
 
 template <class A>

@@ -8,8 +8,10 @@
 // tile's particle segment.
 //
 // Divergence control: every lane deposits the first straight piece of its path in lock-step;
-// the extra pieces of cell-crossing paths go to a per-warp shared-memory queue that is drained
-// 32 at a time with all lanes active.
+// a path that crosses a cell edge is queued (start point, displacement, z weight) in a per-warp
+// ring buffer in shared memory, and the queue is drained 32 paths at a time with all lanes
+// active: each lane recomputes the crossings with the same arithmetic and deposits the later
+// pieces.
 // Re-sort: particles that stay in the tile are written back in place; leavers leave a hole
 // (cell = -1) and go to the mover list (K3 inserts them into their new tile).  Once per tile
 // and species, the holes below the new count are filled from the tail — no block barrier per
@@ -22,35 +24,46 @@
 
 namespace zpic {
 
-constexpr int kQCap = 96;   // per-warp queue of extra path pieces (<= 31 + 2 * 32 after a chunk)
+constexpr int kQRing = 64;  // per-warp ring of queued crossing paths (<= 31 left + 32 new)
 constexpr int kHCap = 256;  // holes recorded per tile and species (else the sentinel fallback)
 constexpr int kHole = -1;   // cell value of a vacated slot
 
-// Per-warp queue of path pieces in shared memory (structure of arrays: conflict-free lanes).
-struct SegQueue {
-  int* c;     // packed (cx + 8) | (cy + 8) << 16
-  float *a0, *b0, *a1, *b1, *wz;
-  __device__ __forceinline__ void put(int k, const Seg& s) const {
-    c[k] = (s.cx + 8) | ((s.cy + 8) << 16);
-    a0[k] = s.a0; b0[k] = s.b0; a1[k] = s.a1; b1[k] = s.b1; wz[k] = s.wz;
-  }
-  __device__ __forceinline__ Seg get(int k) const {
-    const int v = c[k];
-    return Seg{(v & 0xffff) - 8, (v >> 16) - 8, a0[k], b0[k], a1[k], b1[k], wz[k]};
+// Per-warp ring of crossing paths in shared memory (structure of arrays: conflict-free lanes).
+struct PathRing {
+  int* c;     // packed (lx + 8) | (ly + 8) << 16
+  float *x, *y, *dx, *dy, *qvz;
+  __device__ __forceinline__ void put(int k, int lx, int ly, float x0, float y0, float dxp, float dyp, float q) const {
+    c[k] = (lx + 8) | ((ly + 8) << 16);
+    x[k] = x0; y[k] = y0; dx[k] = dxp; dy[k] = dyp; qvz[k] = q;
   }
 };
+
+// Deposit the later pieces of queued path k (the split of PAPER.md:197).
+template <class A>
+__device__ __forceinline__ void drain_path(const A& acc, const PathRing& Q, int k, float jxs, float jys) {
+  const int v = Q.c[k];
+  const int lx = (v & 0xffff) - 8, ly = (v >> 16) - 8;
+  const float x = Q.x[k], y = Q.y[k], dxp = Q.dx[k], dyp = Q.dy[k], qvz = Q.qvz[k];
+  const float x1 = __fadd_rn(x, dxp), y1 = __fadd_rn(y, dyp);
+  const Crossing c = path_crossings(x, y, dxp, dyp, x1, y1);
+  Seg s1, s2;
+  later_pieces(lx, ly, x1, y1, qvz, c, s1, s2);
+  deposit_seg(acc, s1, jxs, jys);
+  if (c.di && c.dj) deposit_seg(acc, s2, jxs, jys);
+}
 
 template <int T, int BLK, int MINB>
 __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
   constexpr int W = T + 2, WJ = T + 3, NW = BLK / 32;
+  constexpr int JWORDS = (3 * WJ * WJ + 3) & ~3;   // int4-aligned
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float2* s_eb1 = reinterpret_cast<float2*>(smem_raw);
   float2* s_eb2 = s_eb1 + W * W;
   float* s_ez = reinterpret_cast<float*>(s_eb2 + W * W);
   float* s_bz = s_ez + W * W;
-  int* s_jhi = reinterpret_cast<int*>(s_bz + W * W);
-  int* s_jlo = s_jhi + 3 * WJ * WJ;
-  int* s_q = s_jlo + 3 * WJ * WJ;  // 6 arrays of NW * kQCap words
+  int* s_j = reinterpret_cast<int*>(s_bz + W * W);   // int32 current, or the high words (exact form)
+  int* s_jlo = s_j + JWORDS;                           // low words (exact form only)
+  int* s_q = s_jlo + JWORDS;  // 6 arrays of NW * kQRing words
   __shared__ int s_holes[kHCap], s_hb[kHCap], s_sa[kHCap];
   __shared__ unsigned s_bits[kHCap / 32];
   __shared__ int s_cnt[4];  // holes, holes below, stayers above, hole-list overflow
@@ -79,19 +92,30 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
     s_ez[k] = ez;
     s_bz[k] = bz;
   }
-  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) { s_jhi[k] = 0; s_jlo[k] = 0; }
+  // fixed-point scale of this tile's current: 2^S from the bound sum_s n_s |q_s| on |J|
+  double bound = 0.0;
+  int ntot = 0;
+  for (int s = 0; s < p.nspecies; ++s) {
+    const int n = p.ps[s].cnt[t];
+    bound += (double)n * fabs((double)p.sc[s].q);
+    ntot += n;
+  }
+  const int S = fx_scale_exponent(bound, ntot);
+  const bool fast = S >= kSMin;   // CTA-uniform: one int32 atomic per node, else the exact two-word form
+  for (int k = threadIdx.x; k < (fast ? 1 : 2) * JWORDS / 4; k += BLK)
+    reinterpret_cast<int4*>(s_j)[k] = make_int4(0, 0, 0, 0);
 
   const SmemFields<W> F{s_eb1, s_eb2, s_ez, s_bz};
-  const SmemCurrentFx<WJ> A{s_jhi, s_jlo};
-  const int qo = warp * kQCap;
-  const SegQueue Q{s_q + qo, reinterpret_cast<float*>(s_q + NW * kQCap + qo),
-                   reinterpret_cast<float*>(s_q + 2 * NW * kQCap + qo), reinterpret_cast<float*>(s_q + 3 * NW * kQCap + qo),
-                   reinterpret_cast<float*>(s_q + 4 * NW * kQCap + qo), reinterpret_cast<float*>(s_q + 5 * NW * kQCap + qo)};
+  const int qo = warp * kQRing;
+  const PathRing Q{s_q + qo, reinterpret_cast<float*>(s_q + NW * kQRing + qo),
+                   reinterpret_cast<float*>(s_q + 2 * NW * kQRing + qo), reinterpret_cast<float*>(s_q + 3 * NW * kQRing + qo),
+                   reinterpret_cast<float*>(s_q + 4 * NW * kQRing + qo), reinterpret_cast<float*>(s_q + 5 * NW * kQRing + qo)};
 
+  auto push_all = [&](const auto& A, const float fscale) {
   for (int s = 0; s < p.nspecies; ++s) {
     const PStore ps = p.ps[s];
     const SpeciesConst sc = p.sc[s];
-    const float jxs = sc.jx * kFxScale, jys = sc.jy * kFxScale, qs = sc.q * kFxScale;
+    const float jxs = sc.jx * fscale, jys = sc.jy * fscale, qs = sc.q * fscale;
     const int n = ps.cnt[t];
     const long base = (long)t * ps.cap;
     const bool has_id = ps.nf > F_ID;
@@ -99,7 +123,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
     __syncthreads();
     float ke = 0.f;
-    int qn = 0;  // warp-uniform queue fill
+    int qn = 0, qh = 0;  // warp-uniform ring fill and head
     // this thread's slot of the current chunk (segments and chunks start on 32-slot blocks)
     uint32_t* pp = ps.slot(base + threadIdx.x);
     // software pipeline: the next chunk's particle is loaded while this one is pushed
@@ -127,48 +151,45 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
         nuz = __uint_as_float(__ldcs(qn_ + F_UZ * 32));
         if (has_id) nid = __ldcs(qn_ + F_ID * 32);
       }
-      Seg seg[3];
-      int nseg = 0, ix = 0, iy = 0;
-      bool stay = false, move = false;
+      bool cross = false, stay = false, move = false;
+      int ix = 0, iy = 0, lx = 0, ly = 0;
+      float x0 = 0.f, y0 = 0.f, dxp = 0.f, dyp = 0.f, qvz = 0.f;
       if (valid) {
         ix = cell_ix(cell); iy = cell_iy(cell);
-        const int lx = ix - i0, ly = iy - j0;
+        lx = ix - i0; ly = iy - j0;
         float ex, ey, ez, bx, by, bz;
         interpolate(F, lx, ly, x, y, ex, ey, ez, bx, by, bz);
         ke += boris(ux, uy, uz, ex, ey, ez, bx, by, bz, sc.h);
         const float rg = rsqrtf(1.0f + fmaf(ux, ux, fmaf(uy, uy, uz * uz)));
-        const float dxp = ux * rg * p.dtdx, dyp = uy * rg * p.dtdy;
+        // __fmul_rn: no contraction into x + dxp, so the drain recomputes the same end point
+        dxp = __fmul_rn(ux * rg, p.dtdx);
+        dyp = __fmul_rn(uy * rg, p.dtdy);
         if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(p.err, ERR_MIGRATION);
-        int di, dj;
-        nseg = split_path(lx, ly, x, y, dxp, dyp, qs * uz * rg, seg, di, dj);
-        deposit_seg(A, seg[0], jxs, jys);
+        qvz = qs * uz * rg;
+        x0 = x; y0 = y;
+        const float x1 = __fadd_rn(x, dxp), y1 = __fadd_rn(y, dyp);
+        const Crossing c = path_crossings(x, y, dxp, dyp, x1, y1);
+        deposit_seg(A, Seg{lx, ly, x, y, c.xa, c.ya, qvz * c.t1}, jxs, jys);
+        cross = c.di || c.dj;
+        int di = c.di, dj = c.dj;
+        renormalise(x1, y1, di, dj, x, y);
         di -= p.shift;   // moving window: the cell index follows the shift at the end of the step
         ix += di; iy += dj;
         if ((unsigned)(lx + di) < (unsigned)tw && (unsigned)(ly + dj) < (unsigned)th) stay = true;
         else move = domain_bc(ix, iy, p);
       }
-      // extra pieces -> this warp's queue; drain full batches of 32 with every lane active
-      const unsigned bal1 = __ballot_sync(0xffffffffu, nseg > 1);
-      if (bal1) {   // warp-uniform: most warps of a thermal plasma have a crossing lane, not all
-        if (nseg > 1) Q.put(qn + __popc(bal1 & ltmask), seg[1]);
-        qn += __popc(bal1);
-        const unsigned bal2 = __ballot_sync(0xffffffffu, nseg > 2);
-        if (nseg > 2) Q.put(qn + __popc(bal2 & ltmask), seg[2]);
-        qn += __popc(bal2);
+      // crossing paths -> this warp's ring; drain full batches of 32 with every lane active
+      const unsigned bal = __ballot_sync(0xffffffffu, cross);
+      if (bal) {   // warp-uniform
+        if (cross) Q.put((qh + qn + __popc(bal & ltmask)) & (kQRing - 1), lx, ly, x0, y0, dxp, dyp, qvz);
+        qn += __popc(bal);
         __syncwarp();
-      }
-      while (qn >= 32) {
-        deposit_seg(A, Q.get(lane), jxs, jys);
-        __syncwarp();
-        const bool m1 = lane + 32 < qn, m2 = lane + 64 < qn;
-        Seg s1, s2;
-        if (m1) s1 = Q.get(lane + 32);
-        if (m2) s2 = Q.get(lane + 64);
-        __syncwarp();
-        if (m1) Q.put(lane, s1);
-        if (m2) Q.put(lane + 32, s2);
-        qn -= 32;
-        __syncwarp();
+        if (qn >= 32) {
+          drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys);
+          qh = (qh + 32) & (kQRing - 1);
+          qn -= 32;
+          __syncwarp();   // the drained entries are read before the next put overwrites them
+        }
       }
       if (valid) {
         if (stay) {
@@ -190,7 +211,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
         else atomicOr(p.err, ERR_OVERFLOW);
       }
     }
-    if (lane < qn) deposit_seg(A, Q.get(lane), jxs, jys);
+    if (lane < qn) drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys);
     // kinetic energy: warp reduction, one shared fp64 add per warp, one global add per CTA
     for (int o = 16; o > 0; o >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, o);
     if (lane == 0) atomicAdd(&s_ke[s], (double)ke);
@@ -263,9 +284,17 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
     if (threadIdx.x == 0) ps.cnt[t] = n2;
     if (s + 1 < p.nspecies) __syncthreads();   // the hole lists / counters are reused by the next species
   }
+  };
+  if (fast) push_all(SmemCurrentI32<WJ>{s_j}, ldexpf(1.0f, S));
+  else push_all(SmemCurrentFx<WJ>{s_j, s_jlo}, kFxScale);
   float* jt = p.Jt + (long)t * 3 * WJ * WJ;
-  for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK)
-    __stcg(jt + k, (float)(fma((double)s_jhi[k], 32768.0, (double)s_jlo[k]) * kFxInv));
+  if (fast) {
+    const float finv = ldexpf(1.0f, -S);
+    for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) __stcg(jt + k, (float)s_j[k] * finv);
+  } else {
+    for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK)
+      __stcg(jt + k, (float)(fma((double)s_j[k], 32768.0, (double)s_jlo[k]) * kFxInv));
+  }
   if (threadIdx.x < p.nspecies && s_ke[threadIdx.x] != 0.0)
     atomicAdd(p.ke_slots + threadIdx.x * kEnergySlots + (t & (kEnergySlots - 1)), s_ke[threadIdx.x]);
 }
@@ -273,8 +302,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
 template <int T, int BLK, int MINB>
 static void launch_push_T(const PushParams& p, int ntiles, cudaStream_t st) {
   constexpr int W = T + 2, WJ = T + 3;
-  constexpr size_t smem = (size_t)W * W * (2 * sizeof(float2) + 2 * sizeof(float)) + (size_t)6 * WJ * WJ * sizeof(int) +
-                          (size_t)6 * (BLK / 32) * kQCap * sizeof(int);
+  constexpr size_t smem = (size_t)W * W * (2 * sizeof(float2) + 2 * sizeof(float)) +
+                          (size_t)2 * ((3 * WJ * WJ + 3) & ~3) * sizeof(int) + (size_t)6 * (BLK / 32) * kQRing * sizeof(int);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_push_tiles<T, BLK, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
