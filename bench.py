@@ -44,6 +44,34 @@ def k1_traffic(config, nx, ny):
     return None
 
 
+def host_loaded(sim, cfg, synth, world, rank):
+    """Species the device injector does not generate (the C4 / P-LWFA density ramp) and the C4
+    laser are built host-side by synth and loaded through zpic_set_particles / zpic_set_fields
+    (single GPU only; the slab runs use device-injected configs)."""
+    ramp = [s for s, sp in enumerate(cfg["species"]) if sp.get("profile") == "ramp"]
+    if not ramp and "laser" not in cfg:
+        return
+    if world > 1:
+        raise SystemExit("ramp / laser configs are benchmarked on one GPU")
+    for s in ramp:
+        sim.set_particles(s, synth.species_particles(cfg, s))
+    if "laser" in cfg:
+        E, B = synth.laser_fields(cfg)
+        sim.set_fields(0, E)
+        sim.set_fields(1, B)
+
+
+def workload_name(name, cfg, n_particles):
+    """config.workload: the synth config, its BASELINE.json index if it is one, and its shape."""
+    idx = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}.get(name)
+    sp = cfg["species"]
+    ppc = "+".join("%dx%d" % tuple(s["ppc"]) for s in sp)
+    bc = {0: "periodic", 1: "open", 2: "window"}
+    return "%s%s: %dx%d cells, %d species, ppc %s, %d particles, bc x %s / y %s" % (
+        cfg["name"], " (BASELINE.json configs[%d])" % idx if idx is not None else " (SURVEY.md NEXT-3)",
+        cfg["nx"], cfg["ny"], len(sp), ppc, n_particles, bc[cfg["bc"][0]], bc[cfg["bc"][1]])
+
+
 def measured_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -209,6 +237,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--nx", type=int, default=0, help="override the grid (profiling runs only)")
     ap.add_argument("--ny", type=int, default=0)
+    ap.add_argument("--current-mode", type=int, default=0, choices=[0, 1],
+                    help="0 = tile-block reduction (K4), 1 = commutative global atomics (SURVEY.md NEXT-4)")
     args = ap.parse_args()
     world, rank, local = dist_env()
     if args.impl == "reference":
@@ -230,7 +260,8 @@ def main():
     if world > 1:   # y-slabs, one per GPU, NCCL send/recv halos
         from paper_2106_12485_b200.dist import nccl_id_broadcast
         dist_kw = {"rank": rank, "world": world, "transport": "nccl", "nccl_id": nccl_id_broadcast(), "device": local}
-    sim = z.Simulation(cfg, inject=True, profile=True, tile=args.tile, dist=dist_kw)
+    sim = z.Simulation(cfg, inject=True, profile=True, tile=args.tile, dist=dist_kw, current_mode=args.current_mode)
+    host_loaded(sim, cfg, synth, world, rank)
     n_particles = sim.counters()["particles"]
     n_cells = cfg["nx"] * cfg["ny"]
     sim.step(args.warmup)
@@ -275,9 +306,9 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "%s (BASELINE.json configs[4]): %dx%d cells, 4x4 ppc, %d particles, uth 0.1, periodic"
-                               % (cfg["name"], cfg["nx"], cfg["ny"], n_particles),
-                   "tile": args.tile, "l2": "inputs larger than L2 (particle store ~30 GB)",
+        "config": {"workload": workload_name(args.config, cfg, n_particles),
+                   "tile": args.tile, "current_mode": ["reduction", "commutative"][args.current_mode],
+                   "l2": "inputs larger than L2 (particle store %.1f GB)" % (n_particles * 24 / 1e9),
                    "parallelism": "y-slabs x%d" % world},
         "cell_updates_per_s": n_cells * args.steps / (ms * 1e-3),
         "k1_pushes_per_s": cnt["particles"] / k1_avg_s,

@@ -104,6 +104,12 @@ typedef struct {
   zpic_alloc_fn alloc;        /* device allocator hook (NULL: cudaMalloc) */
   zpic_free_fn free;
   void* alloc_user;
+  int32_t current_mode;       /* ghost-current combination of the tiles (the paper's
+                                 Table 1 second axis):
+                                 0 = "reduction" (default): every tile stores its private current block
+                                     and K4 sums the overlapping guard nodes (no atomics);
+                                 1 = "commutative": every tile adds its block into the global J with
+                                     fp32 global atomics (J zeroed first each step, no K4). */
 } zpic_options;
 
 /* y-slab decomposition (the paper's row-band regions).

@@ -218,6 +218,7 @@ PushParams push_params(zpic_ctx* c) {
   p.B = c->B[c->cur];
   p.J = c->J;
   p.Jt = c->Jt;
+  p.commutative = c->opt.current_mode == 1;
   p.T = c->T; p.ntx = c->ntx; p.nty = c->nty;
   p.nspecies = c->nspecies;
   for (int s = 0; s < c->nspecies; ++s) { p.sc[s] = c->sc[s]; p.ps[s] = c->ps[s]; }
@@ -454,8 +455,9 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     c->J = alloc_n<float>(c, 3 * g.plane);
     c->Jf = c->opt.filter_passes > 0 ? alloc_n<float>(c, 3 * g.plane) : nullptr;
     if (c->opt.filter_passes < 0 || c->opt.filter_passes > 64) throw Fail{ZPIC_E_INVALID, "filter_passes must be in [0, 64]"};
+    if (c->opt.current_mode != 0 && c->opt.current_mode != 1) throw Fail{ZPIC_E_INVALID, "current_mode must be 0 or 1"};
     const int WJ = c->T + 3;
-    c->Jt = alloc_n<float>(c, (size_t)c->ntiles * 3 * WJ * WJ);
+    c->Jt = c->opt.current_mode == 1 ? nullptr : alloc_n<float>(c, (size_t)c->ntiles * 3 * WJ * WJ);
     c->ke_slots = alloc_n<double>(c, kMaxSpecies * kEnergySlots);
     c->fe_slots = alloc_n<double>(c, kEnergySlots);
     c->energy = alloc_n<double>(c, 1 + 2 * kMaxSpecies);
@@ -652,9 +654,17 @@ StepState step_phase_a(zpic_ctx* c) {
   s.p.shift = s.shift;
   const int grid_small = 148 * 4;
   const PushParams& p = s.p;
+  if (p.commutative) {   // the tiles add into J: start from zero (guards included)
+    ProfScope ps(c, K_ASSEMBLE);
+    CUDA_OR_THROW(cudaMemsetAsync(c->J, 0, (size_t)3 * c->g.plane * sizeof(float), c->stream));
+  }
   { ProfScope ps(c, K_PUSH); launch_push_tiles(p, c->ntiles, c->stream); ++s.launches; }
   { ProfScope ps(c, K_INSERT); launch_insert(p, grid_small, c->stream); ++s.launches; }
-  { ProfScope ps(c, K_ASSEMBLE); launch_assemble(c->J, c->Jt, c->g, c->T, c->ntx, c->nty, c->stream); ++s.launches; }
+  if (!p.commutative) {
+    ProfScope ps(c, K_ASSEMBLE);
+    launch_assemble(c->J, c->Jt, c->g, c->T, c->ntx, c->nty, c->stream);
+    ++s.launches;
+  }
   { ProfScope ps(c, K_LOOSE); launch_loose(p, grid_small, c->stream); ++s.launches; }
   {
     ProfScope ps(c, K_FOLD);

@@ -82,6 +82,7 @@ struct PushParams {
   int slab, has_lo, has_hi;
   PList send[2];
   int skip_cell_store;  // tuning switch: write the cell word only when it changed
+  int commutative;      // 1: K1 adds its current block into J with global atomics (no Jt, no K4)
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
   int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
 };

@@ -9,8 +9,8 @@ import copy
 PERIODIC, OPEN, WINDOW = 0, 1, 2
 
 
-def _electrons(n, ppc, ufl=(0.0, 0.0, 0.0), uth=(0.0, 0.0, 0.0), profile="uniform", x0=0.0, x1=0.0):
-    return {"m_q": -1.0, "ppc": tuple(ppc), "n": float(n), "ufl": tuple(float(v) for v in ufl),
+def _electrons(n, ppc, ufl=(0.0, 0.0, 0.0), uth=(0.0, 0.0, 0.0), profile="uniform", x0=0.0, x1=0.0, m_q=-1.0):
+    return {"m_q": float(m_q), "ppc": tuple(ppc), "n": float(n), "ufl": tuple(float(v) for v in ufl),
             "uth": tuple(float(v) for v in uth), "profile": profile, "x0": float(x0), "x1": float(x1)}
 
 
@@ -41,6 +41,30 @@ CONFIGS = {
     "C5": {"name": "C5-uniform-8192", "nx": 8192, "ny": 8192, "dx": 0.1, "dy": 0.1, "dt": 0.07,
            "bc": (PERIODIC, PERIODIC), "steps": 50, "seed": 505,
            "species": [_electrons(1.0, (4, 4), uth=(0.1, 0.1, 0.1))]},
+    # ---- the paper's own workloads, B200-sized --------
+    # Readings: the paper gives grid, ppc, species and step counts only; dx, dy,
+    # dt, densities, drifts and temperatures reuse C2's (Weibel) and C4's (LWFA) values.
+    # Weibel: electron + positron clouds moving along +-z, 512^2, 256 ppc each
+    # (16 x 16), 500 steps -> 134,217,728 particles.
+    "P-WEIBEL": {"name": "paper-weibel-pairs-512", "nx": 512, "ny": 512, "dx": 0.1, "dy": 0.1, "dt": 0.07,
+                 "bc": (PERIODIC, PERIODIC), "steps": 500, "seed": 606,
+                 "species": [_electrons(0.5, (16, 16), ufl=(0, 0, 0.6), uth=(0.05, 0.05, 0.05)),
+                             _electrons(0.5, (16, 16), ufl=(0, 0, -0.6), uth=(0.05, 0.05, 0.05), m_q=1.0)]},
+    # LWFA: 2000 x 512 cells, 16 ppc (4 x 4), 4000 steps, moving window,
+    # compensated filter; C4's dx, dy, dt, laser and ramp with the laser's leading edge at Lx - 2.
+    "P-LWFA": {"name": "paper-lwfa-2000x512", "nx": 2000, "ny": 512, "dx": 0.02, "dy": 0.1, "dt": 0.019,
+               "bc": (WINDOW, OPEN), "steps": 4000, "seed": 707,
+               "species": [_electrons(1.0, (4, 4), profile="ramp", x0=20.0, x1=20.0 + 20 * 0.02)],
+               "filter": (4, 1),
+               "laser": {"a0": 2.0, "omega0": 10.0, "fwhm": 2.0, "W0": 4.0, "start": 38.0, "polarization": "y"}},
+    # Uniform cold / warm plasmas of the weak-scaling test: 16 x 16 ppc,
+    # u_th = 0 / 0.01; the grid per GPU is fixed (1024^2 here) and the global grid grows with N.
+    "P-COLD": {"name": "paper-uniform-cold", "nx": 1024, "ny": 1024, "dx": 0.1, "dy": 0.1, "dt": 0.07,
+               "bc": (PERIODIC, PERIODIC), "steps": 500, "seed": 808,
+               "species": [_electrons(1.0, (16, 16))]},
+    "P-WARM": {"name": "paper-uniform-warm", "nx": 1024, "ny": 1024, "dx": 0.1, "dy": 0.1, "dt": 0.07,
+               "bc": (PERIODIC, PERIODIC), "steps": 500, "seed": 909,
+               "species": [_electrons(1.0, (16, 16), uth=(0.01, 0.01, 0.01))]},
 }
 
 

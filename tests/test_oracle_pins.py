@@ -484,6 +484,38 @@ def test_cold_plasma_frequency():
     assert omega == pytest.approx(2 / dt * math.asin(dt / 2), rel=1e-7)
 
 
+def test_pair_plasma_frequency():
+    """Positive charges (m_q = +1, the paper's positron cloud): a cold
+    electron-positron plasma (n = 1 each) with the two species displaced in opposite directions
+    oscillates at the total plasma frequency w_p^2 = sum_s n_s q_s^2 / m_s = 2, i.e. the Yee /
+    leapfrog dispersion w = (2/dt) asin(sqrt(2) dt / 2); a sign error in the charge, the Boris
+    factor or the deposit of m_q > 0 changes w (or makes the mode grow)."""
+    nx = ny = 4
+    dx = dy = 0.1
+    dt = 0.07
+    N = nx * ny * 4
+    l, k = np.divmod(np.arange(4), 2)
+    ix = np.repeat(np.arange(nx * ny) % nx, 4).astype(np.int32)
+    iy = np.repeat(np.arange(nx * ny) // nx, 4).astype(np.int32)
+
+    def sp(m_q, u0):
+        return dict(m_q=m_q, n=1.0, ppc=(2, 2), ufl=(0, 0, 0), uth=(0, 0, 0), ix=ix.copy(), iy=iy.copy(),
+                    x=np.tile((k + 0.5) / 2, nx * ny), y=np.tile((l + 0.5) / 2, nx * ny),
+                    ux=np.full(N, u0), uy=np.zeros(N), uz=np.zeros(N))
+
+    sim = OracleSim(nx, ny, dx, dy, dt, [sp(-1.0, 1e-4), sp(1.0, -1e-4)])
+    ex = []
+    for _ in range(300):
+        sim.step()
+        ex.append(sim.E[0, 1, 1])
+    s_ = np.array(ex)
+    c = np.sum(s_[1:-1] * (s_[2:] + s_[:-2])) / (2 * np.sum(s_[1:-1] ** 2))
+    omega = math.acos(c) / dt
+    assert omega == pytest.approx(2 / dt * math.asin(math.sqrt(2.0) * dt / 2), rel=1e-7)
+    # the two species move in antiphase with equal and opposite momenta (equal mass, opposite charge)
+    assert np.allclose(sim.species[0]["ux"], -sim.species[1]["ux"], atol=1e-18, rtol=1e-12)
+
+
 # ---------------------------------------------------------------------------------------
 # P9 Mur-1 open boundary
 def test_mur_absorbs_normal_pulse():

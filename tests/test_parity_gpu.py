@@ -16,16 +16,16 @@ def _z():
     return z
 
 
-def gpu_from_particles(cfg, parts, tile=16, slack=1.25):
-    sim = _z().Simulation(cfg, inject=False, track_ids=True, tile=tile, capacity_slack=slack)
+def gpu_from_particles(cfg, parts, tile=16, slack=1.25, current_mode=0):
+    sim = _z().Simulation(cfg, inject=False, track_ids=True, tile=tile, capacity_slack=slack, current_mode=current_mode)
     for s, p in enumerate(parts):
         sim.set_particles(s, p)
     return sim
 
 
-def _parity_run(cfg, steps, tile=16, check_every_step=True, slack=1.25):
+def _parity_run(cfg, steps, tile=16, check_every_step=True, slack=1.25, current_mode=0):
     parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
-    g = gpu_from_particles(cfg, parts, tile, slack)
+    g = gpu_from_particles(cfg, parts, tile, slack, current_mode)
     o = from_config(cfg, particles=parts)
     nx, ny, dx, dy, dt = cfg["nx"], cfg["ny"], cfg["dx"], cfg["dy"], cfg["dt"]
     per = (cfg["bc"][0] == 0, cfg["bc"][1] == 0)
@@ -153,6 +153,57 @@ def test_c4_lwfa_window_filter_reduced():
     assert energy_agreement(ke_g, ke_o) <= ENERGY_TOL
     assert g.counters()["particles"] == len(o.species[0]["ix"])
     g.close()
+
+
+@pytest.mark.parametrize("tile", [8, 16])
+def test_paper_weibel_pairs_reduced(tile):
+    """the paper's Weibel case, an electron and a positron
+    cloud (m_q = -1, +1) counter-streaming along z at 256 ppc each, on 24 x 20 cells, 10 steps.
+    16 x 16 tiles hold 2 x 65536 particles (the tile current takes the exact two-word form),
+    8 x 8 tiles the int32 form."""
+    cfg = synth.config("P-WEIBEL", nx=24, ny=20)
+    _parity_run(cfg, 10, tile=tile, check_every_step=False)
+
+
+def test_paper_lwfa_16ppc_reduced():
+    """the paper's LWFA case at 16 ppc: C4 physics (moving
+    window, laser, ramp, compensated filter, absorbing y) on 300 x 48 cells, 12 steps."""
+    cfg = synth.config("P-LWFA", nx=300, ny=48)
+    cfg["species"][0].update(x0=2.0, x1=2.0 + 20 * cfg["dx"])
+    cfg["laser"] = dict(cfg["laser"], start=cfg["nx"] * cfg["dx"] - 2.0)
+    parts = [synth.species_particles(cfg, 0)]
+    g = _gpu_c4(cfg, parts)
+    o = from_config(cfg, particles=parts)
+    fe_g, fe_o = [], []
+    for n in range(12):
+        g.step(1)
+        o.step()
+        fe_g.append(g.energy()[1])
+        fe_o.append(o.fe[-1])
+        if n == 0:
+            c = compare_particles(g.particles(0, True), oracle_particles(o, 0), cfg["nx"], cfg["ny"], (False, False))
+            assert c["pos_max"] <= POS_TOL and c["mom_max"] <= MOM_TOL and c["cell_exact_frac"] >= CELL_FRAC, c
+        if n == 9:
+            for w in (0, 1):
+                assert rel_l2(g.fields(w), o.fields(w)) <= FIELD_TOL, (w, rel_l2(g.fields(w), o.fields(w)))
+    assert o.n_move > 0
+    assert energy_agreement(fe_g, fe_o) <= ENERGY_TOL
+    assert g.counters()["particles"] == len(o.species[0]["ix"])
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_commutative_current_mode(name):
+    """SURVEY.md NEXT-4, the paper's "commutative" ghost-current variant:
+    the tiles add their current blocks into J with global atomics instead of the K4 reduction;
+    same parity bar (C1 full size 12 steps; C3 physics reduced, open x, 20 steps)."""
+    if name == "C1":
+        cfg = synth.config("C1")
+    else:
+        cfg = synth.config("C3", nx=128, ny=32)
+        cfg["species"][0].update(x0=0.0, x1=6.4)
+        cfg["species"][1].update(x0=6.4, x1=12.8)
+    _parity_run(cfg, 12 if name == "C1" else 20, check_every_step=False, current_mode=1)
 
 
 def test_window_injection_ids_and_counts():
