@@ -211,6 +211,16 @@ void drain_profile(zpic_ctx* c) {
   c->prof_pending.clear();
 }
 
+// Smallest per-tile fixed-point exponent for the one-word int32 current (kSMin; the environment
+// variable ZPIC_FX_SMIN overrides it for precision experiments: 99 forces the exact two-word form).
+int fx_smin() {
+  static int v = [] {
+    const char* e = getenv("ZPIC_FX_SMIN");
+    return e ? atoi(e) : kSMin;
+  }();
+  return v;
+}
+
 PushParams push_params(zpic_ctx* c) {
   PushParams p{};
   p.g = c->g;
@@ -219,6 +229,7 @@ PushParams push_params(zpic_ctx* c) {
   p.J = c->J;
   p.Jt = c->Jt;
   p.commutative = c->opt.current_mode == 1;
+  p.fx_smin = fx_smin();
   p.T = c->T; p.ntx = c->ntx; p.nty = c->nty;
   p.nspecies = c->nspecies;
   for (int s = 0; s < c->nspecies; ++s) { p.sc[s] = c->sc[s]; p.ps[s] = c->ps[s]; }

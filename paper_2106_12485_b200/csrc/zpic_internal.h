@@ -15,6 +15,7 @@ constexpr int kMaxSpecies = 4;
 constexpr int kXOff = 4;          // interior column 0 sits at column 4 of a padded row (16 B aligned)
 constexpr int kEnergySlots = 256; // fp64 partial-sum slots (spread the atomics), per quantity
 constexpr int kBlock = 256;       // threads per CTA of the particle kernels
+constexpr int kSMin = 22;         // smallest tile scale exponent of the one-word int32 current
 
 // A guard-extended field grid: 3 planes of `rows` x `pitch` floats; interior cell (i, j) of a
 // plane is at (j + 1) * pitch + (i + kXOff), valid for -1 <= i <= nx + 1, -1 <= j <= ny + 1
@@ -83,6 +84,7 @@ struct PushParams {
   PList send[2];
   int skip_cell_store;  // tuning switch: write the cell word only when it changed
   int commutative;      // 1: K1 adds its current block into J with global atomics (no Jt, no K4)
+  int fx_smin;          // a tile uses the one-word int32 current when its scale exponent S >= fx_smin
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
   int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
 };

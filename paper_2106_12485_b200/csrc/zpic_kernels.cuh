@@ -86,7 +86,6 @@ struct SmemCurrentI32 {
 // contribution is scaled by 2^32 and rounded once to an int64 V, split V = hi * 2^15 + lo with
 // 0 <= lo < 2^15, and both halves are added with 32-bit atomics (|sum| < 2^14 per node, lo sums
 // below 2^31 for < 21845 contributions per node).  Per contribution the error is <= 2^-33.
-constexpr int kSMin = 22;
 constexpr float kFxScale = 4294967296.0f;          // 2^32
 constexpr double kFxInv = 2.3283064365386963e-10;  // 2^-32
 template <int WJ>

@@ -101,7 +101,14 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
     ntot += n;
   }
   const int S = fx_scale_exponent(bound, ntot);
-  const bool fast = S >= kSMin;   // CTA-uniform: one int32 atomic per node, else the exact two-word form
+  // CTA-uniform choice: one int32 atomic per node, else the exact two-word form.  A node sums
+  // about nnode = 4 ntot / (tw th) particles' contributions: its rounding noise grows like
+  // sqrt(nnode) 2^-S while the current's own shot noise shrinks like 1 / sqrt(nnode) (q = n / ppc),
+  // so the threshold rises by one bit per doubling of nnode above 80 (16 ppc + 25 % fluctuation):
+  // the noise-to-signal ratio never exceeds that of a 16-ppc tile at S = fx_smin.
+  const int nnode = 4 * ntot / (tw * th);
+  const int smin = p.fx_smin + (nnode > 80 ? 32 - __clz((nnode - 1) / 80) : 0);
+  const bool fast = S >= smin;
   for (int k = threadIdx.x; k < (fast ? 1 : 2) * JWORDS / 4; k += BLK)
     reinterpret_cast<int4*>(s_j)[k] = make_int4(0, 0, 0, 0);
 

@@ -162,7 +162,7 @@ def test_paper_weibel_pairs_reduced(tile):
     16 x 16 tiles hold 2 x 65536 particles (the tile current takes the exact two-word form),
     8 x 8 tiles the int32 form."""
     cfg = synth.config("P-WEIBEL", nx=24, ny=20)
-    _parity_run(cfg, 10, tile=tile, check_every_step=False)
+    print(_parity_run(cfg, 10, tile=tile, check_every_step=False))
 
 
 def test_paper_lwfa_16ppc_reduced():
