@@ -16,13 +16,55 @@
 namespace zpic {
 
 // =============================================================================================
-// K3: movers -> destination tiles (grid-stride over the device-side count).
+// K3: movers -> destination tiles (grid-stride over the device-side count).  Latency-bound by
+// the returning slot atomics, so each thread takes kInsU movers at once: all loads, then all
+// slot reservations, then all stores (kInsU independent chains in flight).
+constexpr int kInsU = 4;
 __global__ void __launch_bounds__(kBlock) k_insert(PushParams p) {
   const int n = min(*p.movers.count, p.movers.cap);
-  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-    const int cell = p.movers.cell[k];
-    insert_particle(p, p.movers.species[k], cell_ix(cell), cell_iy(cell), p.movers.x[k], p.movers.y[k],
-                    p.movers.ux[k], p.movers.uy[k], p.movers.uz[k], p.movers.id ? p.movers.id[k] : 0u);
+  const int stride = gridDim.x * blockDim.x;
+  for (int k0 = blockIdx.x * blockDim.x + threadIdx.x; k0 < n; k0 += kInsU * stride) {
+    int cell[kInsU], sp[kInsU], slot[kInsU], t[kInsU];
+    float x[kInsU], y[kInsU], ux[kInsU], uy[kInsU], uz[kInsU];
+    uint32_t id[kInsU];
+#pragma unroll
+    for (int u = 0; u < kInsU; ++u) {
+      const int k = k0 + u * stride;
+      if (k < n) {
+        cell[u] = p.movers.cell[k]; sp[u] = p.movers.species[k];
+        x[u] = p.movers.x[k]; y[u] = p.movers.y[k];
+        ux[u] = p.movers.ux[k]; uy[u] = p.movers.uy[k]; uz[u] = p.movers.uz[k];
+        id[u] = p.movers.id ? p.movers.id[k] : 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kInsU; ++u) {
+      slot[u] = -1;
+      if (k0 + u * stride < n) {
+        const int iy = cell_iy(cell[u]);
+        t[u] = (iy < 0 || iy >= p.g.ny) ? -1 : (iy / p.T) * p.ntx + cell_ix(cell[u]) / p.T;
+        if (t[u] >= 0) slot[u] = atomicAdd(p.ps[sp[u]].cnt + t[u], 1);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kInsU; ++u) {
+      if (k0 + u * stride >= n) continue;
+      if (t[u] < 0) {   // slab exchange (insert_particle routes it to the neighbour's send list)
+        insert_particle(p, sp[u], cell_ix(cell[u]), cell_iy(cell[u]), x[u], y[u], ux[u], uy[u], uz[u], id[u]);
+        continue;
+      }
+      const PStore& ps = p.ps[sp[u]];
+      if (slot[u] < ps.cap) {
+        uint32_t* q = ps.slot((long)t[u] * ps.cap + slot[u]);
+        q[F_CELL * 32] = (uint32_t)cell[u];
+        q[F_X * 32] = __float_as_uint(x[u]); q[F_Y * 32] = __float_as_uint(y[u]);
+        q[F_UX * 32] = __float_as_uint(ux[u]); q[F_UY * 32] = __float_as_uint(uy[u]); q[F_UZ * 32] = __float_as_uint(uz[u]);
+        if (ps.nf > F_ID) q[F_ID * 32] = id[u];
+      } else {
+        atomicSub(ps.cnt + t[u], 1);
+        list_append(p.spill_out, p.err, cell[u], x[u], y[u], ux[u], uy[u], uz[u], id[u], sp[u]);
+      }
+    }
   }
 }
 
@@ -156,6 +198,15 @@ __global__ void k_guard_y(float* F, GridDesc g, int mode, int keep_mask) {
 // [0, T] (the row/column T redundantly, so no second exchange is needed), B^{n+1} on [0, T).
 // Outputs go to the other buffer (E1, B1), interior plus periodic guard images, so no tile
 // reads a value another tile writes.  FE(n) of the inputs is reduced on the way.
+// 4-byte asynchronous global -> shared copy; valid = false zero-fills the destination.
+__device__ __forceinline__ void cp_async4(float* sdst, const float* gsrc, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(gsrc), "r"(valid ? 4 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
 constexpr int kYeeT = 32;
 __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   constexpr int T = kYeeT, WE = T + 3, WB = T + 2, WJ = T + 1;
@@ -171,27 +222,31 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   // interfaces whose guards come from the neighbour)
   const bool ylo_dom = p.bcy != ZPIC_BC_PERIODIC && p.ylo_edge, yhi_dom = p.bcy != ZPIC_BC_PERIODIC && p.yhi_edge;
 
+  // Staging with asynchronous global -> shared copies (cp.async, LDGSTS): every thread issues all
+  // of its copies before waiting, no registers hold the data; a node outside the guard-extended
+  // grid is zero-filled (source size 0).
   for (int k = threadIdx.x; k < WE * WE; k += kBlock) {
     const int gi = i0 + k % WE - 1, gj = j0 + k / WE - 1;
     const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
     const long a = in ? g.at(gi, gj) : 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) sE[c][k] = in ? __ldg(p.E0 + c * pl + a) : 0.f;
+    for (int c = 0; c < 3; ++c) cp_async4(&sE[c][k], p.E0 + c * pl + a, in);
   }
   for (int k = threadIdx.x; k < WB * WB; k += kBlock) {
     const int gi = i0 + k % WB - 1, gj = j0 + k / WB - 1;
     const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
     const long a = in ? g.at(gi, gj) : 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) sB[c][k] = in ? __ldg(p.B0 + c * pl + a) : 0.f;
+    for (int c = 0; c < 3; ++c) cp_async4(&sB[c][k], p.B0 + c * pl + a, in);
   }
   for (int k = threadIdx.x; k < WJ * WJ; k += kBlock) {
     const int gi = i0 + k % WJ, gj = j0 + k / WJ;
     const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
     const long a = in ? g.at(gi, gj) : 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) sJ[c][k] = in ? __ldg(p.J + c * pl + a) : 0.f;
+    for (int c = 0; c < 3; ++c) cp_async4(&sJ[c][k], p.J + c * pl + a, in);
   }
+  cp_async_wait_all();
   __syncthreads();
 
   // FE(n) = 1/2 dx dy sum(E^2 + B^2) over this tile's interior cells
@@ -610,7 +665,7 @@ __global__ void k_export(PStore ps, const int64_t* prefix, int y0, int32_t* ix, 
 }
 
 // ---- host-side launchers --------------------------------------------------------------------
-void launch_insert(const PushParams& p, int grid, cudaStream_t st) { k_insert<<<grid, kBlock, 0, st>>>(p); }
+void launch_insert(const PushParams& p, int grid, cudaStream_t st) { k_insert<<<grid * 2, kBlock, 0, st>>>(p); }
 void launch_loose(const PushParams& p, int grid, cudaStream_t st) { k_push_loose<<<grid, kBlock, 0, st>>>(p); }
 void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st) {
   dim3 grid((g.nx + 3 + kBlock - 1) / kBlock, g.ny + 3);
