@@ -237,6 +237,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--nx", type=int, default=0, help="override the grid (profiling runs only)")
     ap.add_argument("--ny", type=int, default=0)
+    ap.add_argument("--graphs", action="store_true",
+                    help="time zpic_step with CUDA-graph replay (no per-kernel events: no roofline / kernel times)")
     ap.add_argument("--current-mode", type=int, default=0, choices=[0, 1],
                     help="0 = tile-block reduction (K4), 1 = commutative global atomics (SURVEY.md NEXT-4)")
     args = ap.parse_args()
@@ -260,7 +262,8 @@ def main():
     if world > 1:   # y-slabs, one per GPU, NCCL send/recv halos
         from paper_2106_12485_b200.dist import nccl_id_broadcast
         dist_kw = {"rank": rank, "world": world, "transport": "nccl", "nccl_id": nccl_id_broadcast(), "device": local}
-    sim = z.Simulation(cfg, inject=True, profile=True, tile=args.tile, dist=dist_kw, current_mode=args.current_mode)
+    sim = z.Simulation(cfg, inject=True, profile=not args.graphs, tile=args.tile, dist=dist_kw,
+                       current_mode=args.current_mode)
     host_loaded(sim, cfg, synth, world, rank)
     n_particles = sim.counters()["particles"]
     n_cells = cfg["nx"] * cfg["ny"]
@@ -296,11 +299,11 @@ def main():
         n_particles = int(npt.item())
     sim.close()
 
-    k1_ms, k1_n = kt["k_push_tiles"]
-    k1_avg_s = k1_ms / max(k1_n, 1) * 1e-3
+    k1_ms, k1_n = kt.get("k_push_tiles", (0.0, 0))
+    k1_avg_s = k1_ms / max(k1_n, 1) * 1e-3 if k1_n else float("nan")
     k1_bytes = K1_BYTES_PER_PARTICLE * cnt["particles"] + K1_BYTES_PER_CELL * n_cells // max(world, 1)
     peak, peak_kind = measured_peaks()
-    achieved = k1_bytes / k1_avg_s / 1e9
+    achieved = k1_bytes / k1_avg_s / 1e9 if k1_n else None
     value = n_particles * args.steps / (ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -311,14 +314,17 @@ def main():
                    "l2": "inputs larger than L2 (particle store %.1f GB)" % (n_particles * 24 / 1e9),
                    "parallelism": "y-slabs x%d" % world},
         "cell_updates_per_s": n_cells * args.steps / (ms * 1e-3),
-        "k1_pushes_per_s": cnt["particles"] / k1_avg_s,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+        "k1_pushes_per_s": cnt["particles"] / k1_avg_s if k1_n else None,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak if k1_n else None,
                      "traffic": k1_traffic(args.config, cfg["nx"], cfg["ny"]) if world == 1 else None,
                      "traffic_source": "profiles/r1_k1_traffic_c5.json (ncu dram__bytes_read+write, C5)",
                      "kernel": "k_push_tiles", "peak_kind": peak_kind,
-                     "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg_s * 1e3},
+                     "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg_s * 1e3 if k1_n else None,
+                     **({"note": "--graphs: CUDA-graph replay, no per-kernel events"} if args.graphs else {})},
         "kernel_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in kt.items() if v[1]},
         "gpu_launches": launches,
+        "cuda_graphs": bool(args.graphs),
         "clocks": clk,
     }
     if rank == 0 and not args.no_cpu:

@@ -110,6 +110,9 @@ typedef struct {
                                      and K4 sums the overlapping guard nodes (no atomics);
                                  1 = "commutative": every tile adds its block into the global J with
                                      fp32 global atomics (J zeroed first each step, no K4). */
+  int32_t no_graphs;          /* 0 (default): zpic_step replays a captured CUDA graph of two steps
+                                 when it can (single domain, no moving window, profile = 0), which
+                                 removes the per-launch host cost of small grids; 1 = plain launches */
 } zpic_options;
 
 /* y-slab decomposition (the paper's row-band regions).

@@ -553,12 +553,15 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
   return ZPIC_OK;
 }
 
+static void drop_graphs(zpic_ctx* c);
+
 zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t* ix, const int32_t* iy, const float* x,
                                const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id) {
   if (!c) return ZPIC_E_INVALID;
   if (s < 0 || s >= c->nspecies || n < 0 || (n > 0 && (!ix || !iy || !x || !y || !ux || !uy || !uz))) {
     c->last_error = "set_particles: bad arguments"; return ZPIC_E_INVALID;
   }
+  drop_graphs(c);
   try {
     // upload, then validate + count per tile on the device
     char* tmp = (char*)dev_alloc(c, (size_t)std::max<int64_t>(n, 1) * (7 * 4 + 4));
@@ -767,8 +770,64 @@ zpic_status step_error(zpic_ctx* c) {
   return ZPIC_OK;
 }
 
+// ---- CUDA graphs ---------------------------------------------------------
+// Without a slab decomposition or a moving window, the launches of a step depend on the host
+// state only through the E/B buffer index and the loose-list parity, which both flip every step:
+// a two-step graph replayed from the same parity repeats exactly.  A graph bakes in the buffer
+// pointers, so anything that reallocates (zpic_set_particles) drops the graphs.
+static bool graphs_eligible(const zpic_ctx* c) {
+  return !c->opt.no_graphs && !c->prof && !c->slab && c->bcx != ZPIC_BC_MOVING_WINDOW;
+}
+static void drop_graphs(zpic_ctx* c) {
+  for (auto& g : c->graph)
+    if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+static void run_step(zpic_ctx* c) {
+  StepState s = step_phase_a(c);
+  step_phase_b(c, s);
+  step_phase_c(c, s);
+}
+static cudaGraphExec_t two_step_graph(zpic_ctx* c) {
+  cudaGraphExec_t& ge = c->graph[c->steps & 1];
+  if (ge) return ge;
+  const int cur = c->cur;
+  const int64_t steps = c->steps, launches = c->launches;
+  cudaGraph_t g = nullptr;
+  CUDA_OR_THROW(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    run_step(c);
+    run_step(c);
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CUDA_OR_THROW(cudaStreamEndCapture(c->stream, &g));
+  c->graph_launches = (int)(c->launches - launches);
+  c->cur = cur; c->steps = steps; c->launches = launches;   // capture only recorded the work
+  const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) { ge = nullptr; throw Fail{ZPIC_E_CUDA, std::string("graph: ") + cudaGetErrorString(e)}; }
+  return ge;
+}
+
 zpic_status zpic_step(zpic_ctx* c, int32_t n) {
   if (!c || n < 0) return ZPIC_E_INVALID;
+  if (graphs_eligible(c) && n >= 2) {
+    try {
+      int k = 0;
+      for (; k + 2 <= n; k += 2) {
+        CUDA_OR_THROW(cudaGraphLaunch(two_step_graph(c), c->stream));
+        c->steps += 2;
+        c->launches += c->graph_launches;
+      }
+      if (k < n) run_step(c);
+    } catch (const Fail& f) {
+      c->last_error = f.msg;
+      return f.st;
+    }
+    return step_error(c);
+  }
   if (c->slab && c->transport != ZPIC_TRANSPORT_NCCL) {
     c->last_error = "loopback slabs are stepped with zpic_step_group";
     return ZPIC_E_STATE;
@@ -1012,6 +1071,7 @@ zpic_status zpic_kernel_times(zpic_ctx* c, const char** names, double* ms, int32
 void zpic_free(zpic_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
+  drop_graphs(c);
   if (c->own_comm && c->comm) ncclCommDestroy((ncclComm_t)c->comm);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   for (void* p : c->allocations) {

@@ -163,6 +163,9 @@ struct zpic_ctx {
   bool halo_dirty;   // E/B guard rows of the current buffer must be exchanged before the next step
   std::vector<void*> allocations;
   std::string last_error;
+  // CUDA graphs of two steps, by step parity (the state a two-step replay returns to)
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  int graph_launches = 0;  // kernels in one two-step graph
   // profiling
   bool prof;
   std::vector<std::string> prof_names;

@@ -50,7 +50,7 @@ class zpic_options(ctypes.Structure):
                 ("track_ids", ctypes.c_int32), ("tile", ctypes.c_int32 * 2), ("capacity_slack", ctypes.c_double),
                 ("mover_fraction", ctypes.c_double), ("profile", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", ctypes.c_void_p),
-                ("current_mode", ctypes.c_int32)]
+                ("current_mode", ctypes.c_int32), ("no_graphs", ctypes.c_int32)]
 
 
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
@@ -234,7 +234,7 @@ class Simulation:
     PyTorch's current CUDA stream when torch_plumbing is True."""
 
     def __init__(self, cfg, inject=True, track_ids=False, tile=16, profile=False, capacity_slack=1.25,
-                 torch_plumbing=True, stream=None, dist=None, current_mode=0):
+                 torch_plumbing=True, stream=None, dist=None, current_mode=0, graphs=True):
         """dist: None (whole domain) or {"rank", "world", "transport": "nccl" | "loopback",
         "nccl_id": 128 bytes | "nccl_comm": ncclComm_t address} (y-slab decomposition)."""
         self.cfg = cfg
@@ -259,6 +259,7 @@ class Simulation:
         opt.mover_fraction = 0.05
         opt.profile = int(profile)
         opt.current_mode = int(current_mode)
+        opt.no_graphs = 0 if graphs else 1
         self._keep = []
         if torch_plumbing:
             import torch
