@@ -177,7 +177,9 @@ def e2e_run(args, cfg, torch, z, dist_kw=None, world=1):
     if dist_kw is not None:
         from paper_2106_12485_b200.dist import nccl_id_broadcast
         dist_kw = dict(dist_kw, nccl_id=nccl_id_broadcast())
-    src = z.Simulation(cfg, inject=True, dist=dist_kw)
+    import synth
+    src = z.Simulation(cfg, inject=True, dist=dist_kw, tile=args.tile)
+    host_loaded(src, cfg, synth, world, 0)
     host = []
     for s in range(len(cfg["species"])):
         p = src.particles(s)
@@ -190,10 +192,11 @@ def e2e_run(args, cfg, torch, z, dist_kw=None, world=1):
         host.append(pinned)
     src.close()
     del p
+    laser = synth.laser_fields(cfg) if "laser" in cfg else ()
     if dist_kw is not None:   # a fresh communicator for the second context
         from paper_2106_12485_b200.dist import nccl_id_broadcast
         dist_kw = dict(dist_kw, nccl_id=nccl_id_broadcast())
-    sim = z.Simulation(cfg, inject=False, dist=dist_kw)
+    sim = z.Simulation(cfg, inject=False, dist=dist_kw, tile=args.tile)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -202,6 +205,9 @@ def e2e_run(args, cfg, torch, z, dist_kw=None, world=1):
     for s, hp in enumerate(host):
         sim.set_particles(s, {k: v.numpy() for k, v in hp.items()})
         h2d += sum(v.numel() * v.element_size() for v in hp.values())
+    for w, F in enumerate(laser):
+        sim.set_fields(w, F)
+        h2d += F.nbytes
     d2h = 0
     for _ in range(args.steps):
         sim.step(1)
@@ -230,7 +236,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--tile", type=int, default=16)
+    ap.add_argument("--tile", type=int, default=0, help="tile size (0 = the library's auto choice)")
     ap.add_argument("--cpu-cells", type=int, default=1024)
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
@@ -310,7 +316,7 @@ def main():
         "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(args.config, cfg, n_particles),
-                   "tile": args.tile, "current_mode": ["reduction", "commutative"][args.current_mode],
+                   "tile": cnt["tile"], "current_mode": ["reduction", "commutative"][args.current_mode],
                    "l2": "inputs larger than L2 (particle store %.1f GB)" % (n_particles * 24 / 1e9),
                    "parallelism": "y-slabs x%d" % world},
         "cell_updates_per_s": n_cells * args.steps / (ms * 1e-3),

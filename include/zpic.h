@@ -96,7 +96,8 @@ typedef struct {
   int32_t filter_passes;      /* 0 = no filter; n passes of (1/4,1/2,1/4) along x */
   int32_t filter_compensated; /* 1 = add the (-n/4, 1+n/2, -n/4) compensator pass (R12) */
   int32_t track_ids;          /* 1 = carry a uint32 id per particle (validation runs) */
-  int32_t tile[2];            /* tile size in cells (default 16 x 16) */
+  int32_t tile[2];            /* tile size in cells: 8, 16 or 32 (square); 0 = auto (default):
+                                 16 x 16 unless that gives fewer than 2 tiles per SM, then 8 x 8 */
   double capacity_slack;      /* per-tile capacity = slack * initial count (default 1.5) */
   double mover_fraction;      /* mover buffer capacity as a fraction of particles (default 0.05) */
   int32_t profile;            /* 1 = record per-kernel CUDA-event times (zpic_kernel_times) */
@@ -186,7 +187,7 @@ zpic_status zpic_layout(zpic_ctx* ctx, int32_t* y0, int32_t* ny_local);
 
 /* Counters: out[0] particles (all species), out[1] movers of the last step, out[2] max
  * tile occupancy / capacity in per-mille, out[3] re-packs done, out[4] steps taken,
- * out[5] number of tiles, out[6] kernels launched by zpic_step so far. */
+ * out[5] number of tiles, out[6] kernels launched by zpic_step so far, out[7] tile size T. */
 zpic_status zpic_counters(zpic_ctx* ctx, int64_t* out, int32_t n);
 
 /* Per-kernel device time (ms) summed over the steps since the last call, when

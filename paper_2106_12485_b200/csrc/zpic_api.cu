@@ -409,16 +409,16 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
   zpic_ctx* c = new zpic_ctx();
   try {
     c->opt = zpic_options{};
-    c->opt.tile[0] = c->opt.tile[1] = 16;
+    c->opt.tile[0] = c->opt.tile[1] = 0;   // auto (below)
     c->opt.capacity_slack = 1.25;
     c->opt.mover_fraction = 0.05;
     if (options) {
       c->opt = *options;
-      if (c->opt.tile[0] == 0) c->opt.tile[0] = c->opt.tile[1] = 16;
       if (c->opt.capacity_slack <= 0) c->opt.capacity_slack = 1.25;
       if (c->opt.mover_fraction <= 0) c->opt.mover_fraction = 0.05;
     }
-    if (c->opt.tile[0] != c->opt.tile[1] || (c->opt.tile[0] != 8 && c->opt.tile[0] != 16 && c->opt.tile[0] != 32))
+    if (c->opt.tile[0] != c->opt.tile[1] ||
+        (c->opt.tile[0] != 0 && c->opt.tile[0] != 8 && c->opt.tile[0] != 16 && c->opt.tile[0] != 32))
       throw Fail{ZPIC_E_INVALID, "tile must be 8x8, 16x16 or 32x32"};
     if (c->opt.stream) { c->stream = (cudaStream_t)c->opt.stream; c->own_stream = false; }
     else { CUDA_OR_THROW(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)); c->own_stream = true; }
@@ -446,7 +446,10 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     g.pitch = round_up(g.nx + kXOff + 2, 32);
     g.rows = g.ny + 3;
     g.plane = (long)g.rows * g.pitch;
-    c->T = c->opt.tile[0];
+    // tile 0 = auto: 16 x 16 (the C5-tuned K1 shape) unless that leaves fewer than 2 tiles per SM,
+    // then 8 x 8 (small grids such as C1, C2 are otherwise latency-bound on a few CTAs)
+    c->T = c->opt.tile[0] ? c->opt.tile[0]
+                          : (((g.nx + 15) / 16) * ((g.ny + 15) / 16) >= 2 * 148 ? 16 : 8);
     c->ntx = (g.nx + c->T - 1) / c->T;
     c->nty = (g.ny + c->T - 1) / c->T;
     c->ntiles = c->ntx * c->nty;
@@ -1047,8 +1050,8 @@ zpic_status zpic_counters(zpic_ctx* c, int64_t* out, int32_t n) {
   }
   int nl = 0;
   cudaMemcpy(&nl, c->spill[c->steps & 1].count, 4, cudaMemcpyDeviceToHost);
-  const int64_t v[7] = {total + nl, stats[0], maxfill, c->repacks, c->steps, c->ntiles, c->launches};
-  for (int k = 0; k < n && k < 7; ++k) out[k] = v[k];
+  const int64_t v[8] = {total + nl, stats[0], maxfill, c->repacks, c->steps, c->ntiles, c->launches, c->T};
+  for (int k = 0; k < n && k < 8; ++k) out[k] = v[k];
   return ZPIC_OK;
 }
 

@@ -201,9 +201,9 @@ def zpic_energy(ctx, nspecies):
 
 
 def zpic_counters(ctx):
-    out = (ctypes.c_int64 * 7)()
-    _check(_lib.zpic_counters(ctx, out, 7), ctx)
-    keys = ("particles", "movers", "max_fill_permille", "repacks", "steps", "tiles", "launches")
+    out = (ctypes.c_int64 * 8)()
+    _check(_lib.zpic_counters(ctx, out, 8), ctx)
+    keys = ("particles", "movers", "max_fill_permille", "repacks", "steps", "tiles", "launches", "tile")
     return dict(zip(keys, list(out)))
 
 
