@@ -207,6 +207,19 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
+// (row, column) of a block-strided walk k = tid, tid + kBlock, ... over a W-wide array, advanced
+// without a division per step.
+template <int W>
+struct RowCol {
+  int r, c;
+  __device__ __forceinline__ explicit RowCol(int k) : r(k / W), c(k % W) {}
+  __device__ __forceinline__ void next() {
+    c += kBlock % W;
+    r += kBlock / W;
+    if (c >= W) { c -= W; ++r; }
+  }
+};
+
 constexpr int kYeeT = 32;
 __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   constexpr int T = kYeeT, WE = T + 3, WB = T + 2, WJ = T + 1;
@@ -225,26 +238,36 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   // Staging with asynchronous global -> shared copies (cp.async, LDGSTS): every thread issues all
   // of its copies before waiting, no registers hold the data; a node outside the guard-extended
   // grid is zero-filled (source size 0).
-  for (int k = threadIdx.x; k < WE * WE; k += kBlock) {
-    const int gi = i0 + k % WE - 1, gj = j0 + k / WE - 1;
-    const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
-    const long a = in ? g.at(gi, gj) : 0;
+  // (plane offsets fit in 32 bits: 3 planes of <= 2^29 floats)
+  {
+    RowCol<WE> rc(threadIdx.x);
+    for (int k = threadIdx.x; k < WE * WE; k += kBlock, rc.next()) {
+      const int gi = i0 + rc.c - 1, gj = j0 + rc.r - 1;
+      const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
+      const int a = in ? (int)g.at(gi, gj) : 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) cp_async4(&sE[c][k], p.E0 + c * pl + a, in);
+      for (int c = 0; c < 3; ++c) cp_async4(&sE[c][k], p.E0 + c * (int)pl + a, in);
+    }
   }
-  for (int k = threadIdx.x; k < WB * WB; k += kBlock) {
-    const int gi = i0 + k % WB - 1, gj = j0 + k / WB - 1;
-    const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
-    const long a = in ? g.at(gi, gj) : 0;
+  {
+    RowCol<WB> rc(threadIdx.x);
+    for (int k = threadIdx.x; k < WB * WB; k += kBlock, rc.next()) {
+      const int gi = i0 + rc.c - 1, gj = j0 + rc.r - 1;
+      const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
+      const int a = in ? (int)g.at(gi, gj) : 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) cp_async4(&sB[c][k], p.B0 + c * pl + a, in);
+      for (int c = 0; c < 3; ++c) cp_async4(&sB[c][k], p.B0 + c * (int)pl + a, in);
+    }
   }
-  for (int k = threadIdx.x; k < WJ * WJ; k += kBlock) {
-    const int gi = i0 + k % WJ, gj = j0 + k / WJ;
-    const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
-    const long a = in ? g.at(gi, gj) : 0;
+  {
+    RowCol<WJ> rc(threadIdx.x);
+    for (int k = threadIdx.x; k < WJ * WJ; k += kBlock, rc.next()) {
+      const int gi = i0 + rc.c, gj = j0 + rc.r;
+      const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
+      const int a = in ? (int)g.at(gi, gj) : 0;
 #pragma unroll
-    for (int c = 0; c < 3; ++c) cp_async4(&sJ[c][k], p.J + c * pl + a, in);
+      for (int c = 0; c < 3; ++c) cp_async4(&sJ[c][k], p.J + c * (int)pl + a, in);
+    }
   }
   cp_async_wait_all();
   __syncthreads();
@@ -263,8 +286,9 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
 #define BI(lx, ly) (((ly) + 1) * WB + (lx) + 1)
 #define JI(lx, ly) ((ly) * WJ + (lx))
   // B^{n+1/2} on [-1, T]^2
-  for (int k = threadIdx.x; k < WB * WB; k += kBlock) {
-    const int lx = k % WB - 1, ly = k / WB - 1;
+  RowCol<WB> rcb(threadIdx.x);
+  for (int k = threadIdx.x; k < WB * WB; k += kBlock, rcb.next()) {
+    const int lx = rcb.c - 1, ly = rcb.r - 1;
     const int gi = i0 + lx, gj = j0 + ly;
     if ((p.bcx != ZPIC_BC_PERIODIC && (gi < 0 || gi >= g.nx)) || (gj < 0 && ylo_dom) || (gj >= g.ny && yhi_dom))
       continue;   // B guards of a non-periodic axis stay 0 (only the interior is advanced)
@@ -289,8 +313,9 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   }
   __syncthreads();
   // E^{n+1} on [0, T]^2
-  for (int k = threadIdx.x; k < WJ * WJ; k += kBlock) {
-    const int lx = k % WJ, ly = k / WJ;
+  RowCol<WJ> rcj(threadIdx.x);
+  for (int k = threadIdx.x; k < WJ * WJ; k += kBlock, rcj.next()) {
+    const int lx = rcj.c, ly = rcj.r;
     const int e = EI(lx, ly), b = BI(lx, ly);
     sE[0][e] += p.dtdy * (sB[2][b] - sB[2][BI(lx, ly - 1)]) - p.dt * sJ[0][k];
     sE[1][e] -= p.dtdx * (sB[2][b] - sB[2][BI(lx - 1, ly)]) + p.dt * sJ[1][k];
@@ -343,28 +368,25 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
     const float bx = sB[0][b] - p.hdy * (sE[2][EI(lx, ly + 1)] - ez);
     const float by = sB[1][b] + p.hdx * (sE[2][EI(lx + 1, ly)] - ez);
     const float bz = sB[2][b] + p.hdy * (sE[0][EI(lx, ly + 1)] - sE[0][e]) - p.hdx * (sE[1][EI(lx + 1, ly)] - sE[1][e]);
-    const float vals[6] = {sE[0][e], sE[1][e], ez, bx, by, bz};
+    const float ex = sE[0][e], ey = sE[1][e];
     const int gi = i0 + lx - p.shift, gj = j0 + ly;   // window shift: column i is stored at i - 1
     if (gi < 0) continue;
-    int xs[3], ys[3], nxs = 1, nys = 1;
-    xs[0] = gi; ys[0] = gj;
-    if (p.bcx == ZPIC_BC_PERIODIC) {
-      if (gi <= 1) xs[nxs++] = gi + g.nx;
-      if (gi == g.nx - 1) xs[nxs++] = -1;
+    auto put = [&](int xi, int yj) {
+      const int o = (int)g.at(xi, yj), ipl = (int)pl;
+      p.E1[o] = ex; p.E1[ipl + o] = ey; p.E1[2 * ipl + o] = ez;
+      p.B1[o] = bx; p.B1[ipl + o] = by; p.B1[2 * ipl + o] = bz;
+    };
+    put(gi, gj);
+    // periodic guard images (x: columns nx, nx + 1 <- 0, 1 and -1 <- nx - 1; y likewise)
+    const bool px = p.bcx == ZPIC_BC_PERIODIC;
+    const bool xa = px && gi <= 1, xb = px && gi == g.nx - 1;
+    const bool ya = p.y_images && gj <= 1, yb = p.y_images && gj == g.ny - 1;
+    if (xa | xb | ya | yb) {
+      if (xa) put(gi + g.nx, gj);
+      if (xb) put(-1, gj);
+      if (ya) { put(gi, gj + g.ny); if (xa) put(gi + g.nx, gj + g.ny); if (xb) put(-1, gj + g.ny); }
+      if (yb) { put(gi, -1); if (xa) put(gi + g.nx, -1); if (xb) put(-1, -1); }
     }
-    if (p.y_images) {
-      if (gj <= 1) ys[nys++] = gj + g.ny;
-      if (gj == g.ny - 1) ys[nys++] = -1;
-    }
-    for (int a = 0; a < nys; ++a)
-      for (int c2 = 0; c2 < nxs; ++c2) {
-        const long o = g.at(xs[c2], ys[a]);
-#pragma unroll
-        for (int c = 0; c < 3; ++c) {
-          p.E1[c * pl + o] = vals[c];
-          p.B1[c * pl + o] = vals[3 + c];
-        }
-      }
   }
   // Mur nodes on the high edges sit in the first high guard (node nx / ny)
   if (p.bcx == ZPIC_BC_OPEN && xhi) {
