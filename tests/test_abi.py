@@ -8,6 +8,16 @@ import subprocess
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+def _build_module():
+    """paper_2106_12485_b200/build.py loaded by path (the package itself refuses to import until
+    the library exists), so the CPU suite also runs on a fresh checkout."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_zpic_build", os.path.join(ROOT, "paper_2106_12485_b200", "build.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    return mod
+
+
 def declared():
     src = open(os.path.join(ROOT, "include", "zpic.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
@@ -21,8 +31,7 @@ def test_header_declares_the_five_calls():
 
 
 def test_library_exports_every_declared_symbol():
-    from paper_2106_12485_b200 import build
-    so = build.build()
+    so = _build_module().build()
     lib = ctypes.CDLL(so)
     for n in declared():
         assert hasattr(lib, n), n
@@ -34,8 +43,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_library_is_sm100a():
-    from paper_2106_12485_b200 import build
-    so = build.build()
+    so = _build_module().build()
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True).stdout
     assert "sm_100a" in out
 
@@ -48,3 +56,27 @@ def test_product_never_imports_oracle():
                 txt = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+oracle", txt, flags=re.M), f
                 assert "zpic_oracle" not in txt and "liborc" not in txt, f
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The binding's ctypes mirrors of the ABI structs have the C compiler's size and field
+    offsets (a silent mismatch would corrupt every argument block)."""
+    _build_module().build()
+    import paper_2106_12485_b200 as z
+    structs = {name: getattr(z.zpic, name) for name in ("zpic_grid", "zpic_boundaries", "zpic_species",
+                                                          "zpic_options", "zpic_dist")}
+    lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "zpic.h"', "int main(void) {"]
+    for name, cls in structs.items():
+        lines.append('printf("%s size %%zu\\n", sizeof(%s));' % (name, name))
+        for f in cls._fields_:
+            lines.append('printf("%s.%s %%zu\\n", offsetof(%s, %s));' % (name, f[0], name, f[0]))
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    for name, cls in structs.items():
+        assert int(got["%s size" % name]) == ctypes.sizeof(cls), name
+        for f in cls._fields_:
+            assert int(got["%s.%s" % (name, f[0])]) == getattr(cls, f[0]).offset, (name, f[0])
