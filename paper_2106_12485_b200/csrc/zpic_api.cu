@@ -16,6 +16,7 @@
 namespace zpic {
 void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st);
 void launch_insert(const PushParams& p, int grid, cudaStream_t st);
+void launch_mail_gather(const PushParams& p, cudaStream_t st);
 void launch_loose(const PushParams& p, int grid, cudaStream_t st);
 void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st);
 void launch_guard_x(float* F, const GridDesc& g, int mode, int keep, cudaStream_t st);
@@ -104,6 +105,16 @@ void alloc_store(zpic_ctx* c, int s, int cap) {
   ps.nf = c->opt.track_ids ? 7 : 6;
   ps.data = (uint32_t*)dev_alloc(c, n * ps.nf * sizeof(uint32_t));   // contents defined by cnt, no memset
   ps.cnt = alloc_n<int32_t>(c, c->ntiles);
+  // mailboxes: an edge box holds half a tile column of the species' lattice, a corner box 32
+  MailBox& M = c->mail[s];
+  const int ppc = c->species[s].ppc[0] * c->species[s].ppc[1];
+  M.cap_edge = round_up(std::max(32, c->T * ppc / 2), 32);
+  M.cap_corner = 32;
+  M.per_tile = 4 * M.cap_edge + 4 * M.cap_corner;
+  M.stride = (long)c->ntiles * M.per_tile;
+  M.nf = ps.nf;
+  M.data = (uint32_t*)dev_alloc(c, (size_t)M.stride * M.nf * sizeof(uint32_t));
+  M.cnt = alloc_n<int32_t>(c, (size_t)c->ntiles * 8);
 }
 
 // The tile current is accumulated as fixed point with a per-tile scale 2^S chosen from the
@@ -121,6 +132,8 @@ void free_store(zpic_ctx* c, int s) {
   PStore& ps = c->ps[s];
   dev_free(c, ps.data); dev_free(c, ps.cnt);
   ps = PStore{};
+  dev_free(c, c->mail[s].data); dev_free(c, c->mail[s].cnt);
+  c->mail[s] = MailBox{};
 }
 
 PList alloc_list(zpic_ctx* c, int cap) {
@@ -174,10 +187,10 @@ void refresh_field_guards(zpic_ctx* c, float* F, bool is_E) {
 
 // ---- profiling ---------------------------------------------------------------------------
 enum KId { K_PUSH = 0, K_INSERT, K_ASSEMBLE, K_LOOSE, K_FOLD, K_HALO, K_FILTER, K_YEE, K_WINDOW, K_EPI, K_EXCHANGE,
-           K_COUNT };
+           K_MAIL, K_COUNT };
 const char* kNames[K_COUNT] = {"k_push_tiles", "k_insert",        "k_assemble_j", "k_push_loose",
                                "k_guard_fold", "k_apply_halo",    "k_filter_x",   "k_yee",
-                               "k_inject_column", "k_epilogue",   "halo_exchange"};
+                               "k_inject_column", "k_epilogue",   "halo_exchange", "k_mail_gather"};
 
 struct ProfScope {
   zpic_ctx* c;
@@ -229,6 +242,9 @@ PushParams push_params(zpic_ctx* c) {
   p.J = c->J;
   p.Jt = c->Jt;
   p.commutative = c->opt.current_mode == 1;
+  static const int mail = [] { const char* e = getenv("ZPIC_MAIL"); return e ? atoi(e) : 1; }();
+  p.use_mail = mail;
+  for (int s = 0; s < c->nspecies; ++s) p.mail[s] = c->mail[s];
   p.fx_smin = fx_smin();
   p.T = c->T; p.ntx = c->ntx; p.nty = c->nty;
   p.nspecies = c->nspecies;
@@ -676,6 +692,7 @@ StepState step_phase_a(zpic_ctx* c) {
     CUDA_OR_THROW(cudaMemsetAsync(c->J, 0, (size_t)3 * c->g.plane * sizeof(float), c->stream));
   }
   { ProfScope ps(c, K_PUSH); launch_push_tiles(p, c->ntiles, c->stream); ++s.launches; }
+  if (p.use_mail) { ProfScope ps(c, K_MAIL); launch_mail_gather(p, c->stream); ++s.launches; }
   { ProfScope ps(c, K_INSERT); launch_insert(p, grid_small, c->stream); ++s.launches; }
   if (!p.commutative) {
     ProfScope ps(c, K_ASSEMBLE);

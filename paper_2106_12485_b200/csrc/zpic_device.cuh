@@ -38,6 +38,26 @@ __device__ __forceinline__ void block_add_double(double v, double* slot) {
   __syncthreads();
 }
 
+// Mailbox direction of travel (dx, dy) in {-1, 0, 1}^2 \ {0}: d = 3 (dy + 1) + (dx + 1), the
+// centre skipped.  Corners are d = 0, 2, 5, 7; edges 1, 3, 4, 6.
+__host__ __device__ __forceinline__ int mail_dir(int dx, int dy) {
+  const int k = 3 * (dy + 1) + (dx + 1);
+  return k < 4 ? k : k - 1;
+}
+__host__ __device__ __forceinline__ void mail_delta(int d, int& dx, int& dy) {
+  const int k = d < 4 ? d : d + 1;
+  dx = k % 3 - 1;
+  dy = k / 3 - 1;
+}
+__host__ __device__ __forceinline__ bool mail_corner(int d) { return (0xA5u >> d) & 1u; }
+__host__ __device__ __forceinline__ int mail_cap(const MailBox& M, int d) {
+  return mail_corner(d) ? M.cap_corner : M.cap_edge;
+}
+__host__ __device__ __forceinline__ int mail_offset(const MailBox& M, int d) {
+  const int corners = (0x33222110u >> (4 * d)) & 0xFu;   // corner boxes before d
+  return corners * M.cap_corner + (d - corners) * M.cap_edge;
+}
+
 __device__ __forceinline__ int pack_cell(int ix, int iy) { return (ix & 0xffff) | (iy << 16); }
 __device__ __forceinline__ int cell_ix(int c) { return c & 0xffff; }
 __device__ __forceinline__ int cell_iy(int c) { return c >> 16; }

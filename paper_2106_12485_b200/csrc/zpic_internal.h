@@ -43,6 +43,20 @@ struct PStore {
   __host__ __device__ uint32_t* slot(long k) const { return data + (k >> 5) * (32L * nf) + (k & 31); }
 };
 
+// Per-tile mailboxes of one species (K1 -> K3m): a particle leaving tile t across an edge or a
+// corner goes to slot k of box (t, d), d = the direction of travel (mail_dir); the destination
+// tile's warp in K3m reads the 8 boxes addressed to it and appends them to its segment with
+// coalesced stores.  Boxes have fixed capacities (edges cap_edge, corners cap_corner); a
+// particle that finds its box full goes through the flat mover list instead.  Fields as in
+// PStore, field f of slot q at data[f * stride + q], q = t * per_tile + offset(d) + k.
+struct MailBox {
+  uint32_t* data;
+  int32_t* cnt;    // [ntiles][8] entries of each box this step
+  int cap_edge, cap_corner, per_tile;
+  long stride;     // ntiles * per_tile
+  int nf;
+};
+
 // Particles that left their tile (or could not be inserted): a flat SoA list.
 struct PList {
   int32_t* cell;
@@ -84,6 +98,8 @@ struct PushParams {
   PList send[2];
   int skip_cell_store;  // tuning switch: write the cell word only when it changed
   int commutative;      // 1: K1 adds its current block into J with global atomics (no Jt, no K4)
+  int use_mail;         // 1: tile leavers go through the per-tile mailboxes (K3m), else the mover list
+  MailBox mail[kMaxSpecies];
   int fx_smin;          // a tile uses the one-word int32 current when its scale exponent S >= fx_smin
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
   int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
@@ -138,6 +154,7 @@ struct zpic_ctx {
   float* Jf;       // filtered current (only with a filter; J keeps the pre-filter values)
   float* Jt;       // per-tile blocks
   zpic::PStore ps[zpic::kMaxSpecies];
+  zpic::MailBox mail[zpic::kMaxSpecies];
   zpic::PList movers, spill[2];
   double* ke_slots;
   double* fe_slots;

@@ -18,37 +18,49 @@ namespace zpic {
 // =============================================================================================
 // K3: movers -> destination tiles (grid-stride over the device-side count).  Latency-bound by
 // the returning slot atomics, so each thread takes kInsU movers at once: all loads, then all
-// slot reservations, then all stores (kInsU independent chains in flight).
+// slot reservations, then all stores (kInsU independent chains in flight).  A warp's movers come
+// from a few source tiles (K1 appends them warp by warp) and go to a few destination tiles: lanes
+// with the same destination reserve their slots with one atomic (match_any), so their stores
+// land on consecutive slots (coalesced in the AoSoA blocks).
 constexpr int kInsU = 4;
 __global__ void __launch_bounds__(kBlock) k_insert(PushParams p) {
   const int n = min(*p.movers.count, p.movers.cap);
   const int stride = gridDim.x * blockDim.x;
-  for (int k0 = blockIdx.x * blockDim.x + threadIdx.x; k0 < n; k0 += kInsU * stride) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  // warp-uniform trip count: every lane takes part in the warp collectives
+  const int wbase = (blockIdx.x * blockDim.x + (threadIdx.x & ~31));
+  for (int k0w = wbase; k0w < n; k0w += kInsU * stride) {
+    const int k0 = k0w + lane;
     int cell[kInsU], sp[kInsU], slot[kInsU], t[kInsU];
     float x[kInsU], y[kInsU], ux[kInsU], uy[kInsU], uz[kInsU];
     uint32_t id[kInsU];
 #pragma unroll
     for (int u = 0; u < kInsU; ++u) {
       const int k = k0 + u * stride;
+      t[u] = -2;   // no mover
       if (k < n) {
         cell[u] = p.movers.cell[k]; sp[u] = p.movers.species[k];
         x[u] = p.movers.x[k]; y[u] = p.movers.y[k];
         ux[u] = p.movers.ux[k]; uy[u] = p.movers.uy[k]; uz[u] = p.movers.uz[k];
         id[u] = p.movers.id ? p.movers.id[k] : 0u;
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kInsU; ++u) {
-      slot[u] = -1;
-      if (k0 + u * stride < n) {
         const int iy = cell_iy(cell[u]);
         t[u] = (iy < 0 || iy >= p.g.ny) ? -1 : (iy / p.T) * p.ntx + cell_ix(cell[u]) / p.T;
-        if (t[u] >= 0) slot[u] = atomicAdd(p.ps[sp[u]].cnt + t[u], 1);
       }
     }
 #pragma unroll
     for (int u = 0; u < kInsU; ++u) {
-      if (k0 + u * stride >= n) continue;
+      const int key = t[u] >= 0 ? (sp[u] << 27) | t[u] : -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(peers) - 1;
+      int base = 0;
+      if (key >= 0 && lane == leader) base = atomicAdd(p.ps[sp[u]].cnt + t[u], __popc(peers));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      slot[u] = base + __popc(peers & lt);
+    }
+#pragma unroll
+    for (int u = 0; u < kInsU; ++u) {
+      if (t[u] == -2) continue;
       if (t[u] < 0) {   // slab exchange (insert_particle routes it to the neighbour's send list)
         insert_particle(p, sp[u], cell_ix(cell[u]), cell_iy(cell[u]), x[u], y[u], ux[u], uy[u], uz[u], id[u]);
         continue;
@@ -66,6 +78,84 @@ __global__ void __launch_bounds__(kBlock) k_insert(PushParams p) {
       }
     }
   }
+}
+
+// =============================================================================================
+// K3m: one warp per (destination tile, species) appends the particles of the 8 mailboxes
+// addressed to its tile (the migration to the adjacent region of PAPER.md:197): box (n, d) of
+// the neighbour n = tile - delta(d), read and written with consecutive lanes (coalesced loads
+// from the box, coalesced stores into the AoSoA segment).  The warp owns the tile's count in
+// this kernel; a full segment sends the rest to the loose list.
+__global__ void __launch_bounds__(kBlock) k_mail_gather(PushParams p) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int ntiles = p.ntx * p.nty;
+  if (w >= ntiles * p.nspecies) return;
+  const int s = w / ntiles, t = w - s * ntiles;
+  const MailBox& M = p.mail[s];
+  const PStore& ps = p.ps[s];
+  // lane d < 8: the sender of box direction d and its fill (one round trip for all 8 boxes)
+  int n = -1, c = 0;
+  if (lane < 8) {
+    const int tx = t % p.ntx, ty = t / p.ntx;
+    int dx, dy;
+    mail_delta(lane, dx, dy);
+    int sx = tx - dx, sy = ty - dy;
+    bool ok = true;
+    if (sx < 0 || sx >= p.ntx) {
+      ok = p.bcx == ZPIC_BC_PERIODIC;
+      sx = sx < 0 ? sx + p.ntx : sx - p.ntx;
+    }
+    if (sy < 0 || sy >= p.nty) {
+      ok = ok && p.bcy == ZPIC_BC_PERIODIC && !p.slab;
+      sy = sy < 0 ? sy + p.nty : sy - p.nty;
+    }
+    if (ok) {
+      n = sy * p.ntx + sx;
+      c = M.cnt[n * 8 + lane];
+    }
+  }
+  const int pos = ps.cnt[t];
+  // exclusive prefix of the 8 fills, then every lane takes entries e = lane, lane + 32, ...
+  int off = c;
+#pragma unroll
+  for (int o = 1; o < 8; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, off, o);
+    if (lane >= o) off += v;
+  }
+  const int total = __shfl_sync(0xffffffffu, off, 7);
+  off -= c;
+  int offs[8], ns[8];
+#pragma unroll
+  for (int d = 0; d < 8; ++d) {
+    offs[d] = __shfl_sync(0xffffffffu, off, d);
+    ns[d] = __shfl_sync(0xffffffffu, n, d);
+  }
+  for (int e = lane; e < total; e += 32) {
+    int d = 0;
+#pragma unroll
+    for (int q = 1; q < 8; ++q) d = e >= offs[q] ? q : d;   // offsets are non-decreasing
+    int nd = ns[0], od = offs[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) {
+      if (q == d) { nd = ns[q]; od = offs[q]; }
+    }
+    const uint32_t* src = M.data + (long)nd * M.per_tile + mail_offset(M, d) + (e - od);
+    const uint32_t cell = src[F_CELL * M.stride];
+    const uint32_t x = src[F_X * M.stride], y = src[F_Y * M.stride];
+    const uint32_t ux = src[F_UX * M.stride], uy = src[F_UY * M.stride], uz = src[F_UZ * M.stride];
+    const uint32_t id = M.nf > F_ID ? src[F_ID * M.stride] : 0u;
+    const int slot = pos + e;
+    if (slot < ps.cap) {
+      uint32_t* q = ps.slot((long)t * ps.cap + slot);
+      q[F_CELL * 32] = cell; q[F_X * 32] = x; q[F_Y * 32] = y;
+      q[F_UX * 32] = ux; q[F_UY * 32] = uy; q[F_UZ * 32] = uz;
+      if (ps.nf > F_ID) q[F_ID * 32] = id;
+    } else {
+      list_append(p.spill_out, p.err, (int)cell, __uint_as_float(x), __uint_as_float(y), __uint_as_float(ux),
+                  __uint_as_float(uy), __uint_as_float(uz), id, s);
+    }
+  }
+  if (lane == 0) ps.cnt[t] = min(pos + total, ps.cap);
 }
 
 // =============================================================================================
@@ -687,6 +777,10 @@ __global__ void k_export(PStore ps, const int64_t* prefix, int y0, int32_t* ix, 
 }
 
 // ---- host-side launchers --------------------------------------------------------------------
+void launch_mail_gather(const PushParams& p, cudaStream_t st) {
+  const long warps = (long)p.ntx * p.nty * p.nspecies;
+  k_mail_gather<<<(int)((warps * 32 + kBlock - 1) / kBlock), kBlock, 0, st>>>(p);
+}
 void launch_insert(const PushParams& p, int grid, cudaStream_t st) { k_insert<<<grid * 2, kBlock, 0, st>>>(p); }
 void launch_loose(const PushParams& p, int grid, cudaStream_t st) { k_push_loose<<<grid, kBlock, 0, st>>>(p); }
 void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st) {

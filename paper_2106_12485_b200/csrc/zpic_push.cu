@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
   __shared__ int s_holes[kHCap], s_hb[kHCap], s_sa[kHCap];
   __shared__ unsigned s_bits[kHCap / 32];
   __shared__ int s_cnt[4];  // holes, holes below, stayers above, hole-list overflow
+  __shared__ int s_mbc[8];  // mailbox fill per direction (this species)
   __shared__ int s_wsum[2][NW];
   __shared__ double s_ke[kMaxSpecies];
   if (threadIdx.x < kMaxSpecies) s_ke[threadIdx.x] = 0.0;
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
     const bool has_id = ps.nf > F_ID;
     const int chunk_words = BLK * ps.nf;   // a chunk is BLK / 32 whole AoSoA blocks
     if (threadIdx.x < 4) s_cnt[threadIdx.x] = 0;
+    if (threadIdx.x < 8) s_mbc[threadIdx.x] = 0;
     __syncthreads();
     float ke = 0.f;
     int qn = 0, qh = 0;  // warp-uniform ring fill and head
@@ -159,7 +161,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
         if (has_id) nid = __ldcs(qn_ + F_ID * 32);
       }
       bool cross = false, stay = false, move = false;
-      int ix = 0, iy = 0, lx = 0, ly = 0;
+      int ix = 0, iy = 0, lx = 0, ly = 0, mdir = -1;
       float x0 = 0.f, y0 = 0.f, dxp = 0.f, dyp = 0.f, qvz = 0.f;
       if (valid) {
         ix = cell_ix(cell); iy = cell_iy(cell);
@@ -184,6 +186,11 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
         ix += di; iy += dj;
         if ((unsigned)(lx + di) < (unsigned)tw && (unsigned)(ly + dj) < (unsigned)th) stay = true;
         else move = domain_bc(ix, iy, p);
+        // direction of travel out of the tile (a slab exit in y goes through the mover list)
+        if (move && p.use_mail && !(p.slab && (iy < 0 || iy >= p.g.ny))) {
+          const int ex = lx + di, ey = ly + dj;
+          mdir = mail_dir(ex < 0 ? -1 : (ex >= tw ? 1 : 0), ey < 0 ? -1 : (ey >= th ? 1 : 0));
+        }
       }
       // crossing paths -> this warp's ring; drain full batches of 32 with every lane active
       const unsigned bal = __ballot_sync(0xffffffffu, cross);
@@ -212,8 +219,24 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
           else s_cnt[3] = 1;
         }
       }
-      const int m = warp_reserve(p.movers.count, move);
-      if (move) {
+      // leavers: this tile's mailbox for their direction, else (box full, slab exit) the list
+      int mslot = -1;
+      if (mdir >= 0) {
+        const int k = atomicAdd(&s_mbc[mdir], 1);
+        if (k < mail_cap(p.mail[s], mdir)) mslot = k;
+      }
+      const bool glob = move && mslot < 0;
+      const int m = warp_reserve(p.movers.count, glob);
+      if (mslot >= 0) {
+        const MailBox& M = p.mail[s];
+        uint32_t* q = M.data + (long)t * M.per_tile + mail_offset(M, mdir) + mslot;
+        q[F_CELL * M.stride] = (uint32_t)pack_cell(ix, iy);
+        q[F_X * M.stride] = __float_as_uint(x); q[F_Y * M.stride] = __float_as_uint(y);
+        q[F_UX * M.stride] = __float_as_uint(ux); q[F_UY * M.stride] = __float_as_uint(uy);
+        q[F_UZ * M.stride] = __float_as_uint(uz);
+        if (M.nf > F_ID) q[F_ID * M.stride] = id;
+      }
+      if (glob) {
         if (m < p.movers.cap) list_put(p.movers, m, pack_cell(ix, iy), x, y, ux, uy, uz, id, s);
         else atomicOr(p.err, ERR_OVERFLOW);
       }
@@ -223,6 +246,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
     for (int o = 16; o > 0; o >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, o);
     if (lane == 0) atomicAdd(&s_ke[s], (double)ke);
     __syncthreads();   // all deposits, hole records and in-place writes of this species are done
+    if (p.use_mail && threadIdx.x < 8)
+      p.mail[s].cnt[t * 8 + threadIdx.x] = min(s_mbc[threadIdx.x], mail_cap(p.mail[s], threadIdx.x));
 
     // ---- re-sort: fill the holes below the new count from the tail --------------------------
     const int nh = s_cnt[0], n2 = n - nh;
