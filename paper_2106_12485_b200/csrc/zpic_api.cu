@@ -17,6 +17,8 @@ namespace zpic {
 void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st);
 void launch_insert(const PushParams& p, int grid, cudaStream_t st);
 void launch_mail_gather(const PushParams& p, cudaStream_t st);
+void launch_loose_extract(const PList& L, int s, int y0, int64_t out0, int32_t* ix, int32_t* iy, float* x, float* y,
+                          float* ux, float* uy, float* uz, uint32_t* id, int* counter, cudaStream_t st);
 void launch_loose(const PushParams& p, int grid, cudaStream_t st);
 void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st);
 void launch_guard_x(float* F, const GridDesc& g, int mode, int keep, cudaStream_t st);
@@ -26,7 +28,7 @@ void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nsp
                      int* sic, int* soc, int* stats, cudaStream_t st);
 void launch_inject(const InjectParams& q, int ntiles, cudaStream_t st);
 void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
-                const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err,
+                const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err, const PList& loose, int s,
                 cudaStream_t st);
 void launch_export(const PStore& ps, int ntiles, const int64_t* prefix, int y0, int32_t* ix, int32_t* iy, float* x,
                    float* y, float* ux, float* uy, float* uz, uint32_t* id, cudaStream_t st);
@@ -512,7 +514,8 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       }
       int maxcount = c->T * c->T * ppc;
       if (sp.profile == ZPIC_DENS_NONE || sp.n == 0.0) { col_lo = col_hi = 0; }
-      const int cap = std::max(32, round_up((int)std::ceil(maxcount * c->opt.capacity_slack), 32));
+      // the device injector writes every lattice particle into its tile: no less than a full tile
+      const int cap = std::max(32, round_up((int)std::ceil(maxcount * std::max(1.0, c->opt.capacity_slack)), 32));
       if ((double)cap * c->ntiles > 2.0e9) throw Fail{ZPIC_E_INVALID, "particle store exceeds 2^31 slots"};
       alloc_store(c, s, cap);
       check_tile_capacity(c);
@@ -528,6 +531,7 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
         total += (int64_t)(col_hi - col_lo) * g.ny * ppc;
       }
     }
+    c->population = total;
     const int mcap = mover_capacity(c, total);
     c->movers = alloc_list(c, (int)mcap);
     c->spill[0] = alloc_list(c, (int)mcap);
@@ -574,6 +578,163 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
 
 static void drop_graphs(zpic_ctx* c);
 
+// Bin n particles held on the device (SoA block `tmp`: ix, iy (global), x, y, ux, uy, uz, id, n
+// entries each) into species s's tile store, sized anew for the largest tile; frees `tmp`.
+static void load_species(zpic_ctx* c, int s, int64_t n, char* tmp, bool has_id) {
+  int32_t* dix = (int32_t*)tmp;
+  int32_t* diy = dix + n;
+  float* dx_ = (float*)(diy + n);
+  float* dy_ = dx_ + n;
+  float* dux = dy_ + n;
+  float* duy = dux + n;
+  float* duz = duy + n;
+  uint32_t* did = (uint32_t*)(duz + n);
+  int* dcounts = alloc_n<int>(c, c->ntiles + 1);
+  if (n > 0) {
+    launch_count(c->T, c->ntx, c->g.nx, c->g.ny, c->y0, (long)n, dix, diy, dx_, dy_, dcounts, dcounts + c->ntiles,
+                 c->stream);
+    CUDA_OR_THROW(cudaGetLastError());
+  }
+  std::vector<int> counts(c->ntiles + 1, 0);
+  CUDA_OR_THROW(cudaMemcpyAsync(counts.data(), dcounts, (c->ntiles + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  dev_free(c, dcounts);
+  if (counts[c->ntiles]) {
+    dev_free(c, tmp);
+    throw Fail{ZPIC_E_INVALID, "set_particles: a particle is outside the local slab or its offset is not in [0,1)"};
+  }
+  int maxc = 0;
+  for (int t = 0; t < c->ntiles; ++t) maxc = std::max(maxc, counts[t]);
+  const int ppc = c->species[s].ppc[0] * c->species[s].ppc[1];
+  const double slack = c->repacking ? std::max(1.1, c->opt.capacity_slack) : c->opt.capacity_slack;
+  const int cap = std::max({32, round_up((int)std::ceil(maxc * slack), 32),
+                            round_up((int)std::ceil(c->T * c->T * ppc * slack), 32)});
+  free_store(c, s);
+  alloc_store(c, s, cap);
+  check_tile_capacity(c);
+  if (n > 0) {
+    launch_bin(c->ps[s], c->T, c->ntx, c->y0, (long)n, dix, diy, dx_, dy_, dux, duy, duz, has_id ? did : nullptr, c->err,
+               c->spill[c->steps & 1], s, c->stream);
+    CUDA_OR_THROW(cudaGetLastError());
+  }
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  dev_free(c, tmp);
+}
+
+// Movers / loose lists sized for the current population (the live loose list keeps its
+// contents when it grows).
+static void size_lists(zpic_ctx* c) {
+  int64_t total = 0;
+  for (int q = 0; q < c->nspecies; ++q) {
+    std::vector<int> cnt(c->ntiles);
+    CUDA_OR_THROW(cudaMemcpy(cnt.data(), c->ps[q].cnt, c->ntiles * 4, cudaMemcpyDeviceToHost));
+    for (int v : cnt) total += v;
+  }
+  int nl = 0;
+  PList& live = c->spill[c->steps & 1];
+  CUDA_OR_THROW(cudaMemcpy(&nl, live.count, 4, cudaMemcpyDeviceToHost));
+  nl = std::min(nl, live.cap);
+  c->population = total + nl;
+  const int need = mover_capacity(c, c->population);
+  if (need > c->movers.cap) {
+    for (PList* L : {&c->movers, &c->spill[0], &c->spill[1]}) {
+      PList N = alloc_list(c, need);
+      if (L == &live && nl > 0) {
+        const size_t b = (size_t)nl * 4;
+        CUDA_OR_THROW(cudaMemcpyAsync(N.cell, L->cell, b, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_OR_THROW(cudaMemcpyAsync(N.x, L->x, b, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_OR_THROW(cudaMemcpyAsync(N.y, L->y, b, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_OR_THROW(cudaMemcpyAsync(N.ux, L->ux, b, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_OR_THROW(cudaMemcpyAsync(N.uy, L->uy, b, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_OR_THROW(cudaMemcpyAsync(N.uz, L->uz, b, cudaMemcpyDeviceToDevice, c->stream));
+        if (N.id && L->id) CUDA_OR_THROW(cudaMemcpyAsync(N.id, L->id, b, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_OR_THROW(cudaMemcpyAsync(N.species, L->species, b, cudaMemcpyDeviceToDevice, c->stream));
+        CUDA_OR_THROW(cudaMemcpyAsync(N.count, &nl, 4, cudaMemcpyHostToDevice, c->stream));
+        CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+      }
+      dev_free(c, L->cell); dev_free(c, L->x); dev_free(c, L->y); dev_free(c, L->ux); dev_free(c, L->uy);
+      dev_free(c, L->uz); dev_free(c, L->id); dev_free(c, L->species); dev_free(c, L->count);
+      *L = N;
+    }
+  }
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+}
+
+// Re-pack (SURVEY.md §8(d) "slack plus an overflow -> global re-pack path"): when the loose list
+// (particles that found no slack in their tile) grows, every species is exported from its tiles
+// and the loose list to a flat device buffer and binned again into tiles sized for the current
+// largest tile.  Host-driven and rare: zpic_step checks the loose count every kRepackCheck steps.
+constexpr int kRepackCheck = 16;
+static void repack(zpic_ctx* c) {
+  c->repacking = true;
+  const PList L = c->spill[c->steps & 1];   // the loose particles of the next step
+  int nl = 0;
+  CUDA_OR_THROW(cudaMemcpy(&nl, L.count, 4, cudaMemcpyDeviceToHost));
+  nl = std::min(nl, L.cap);
+  // 1. every species out to a flat device block (tiles, then its loose particles)
+  std::vector<char*> tmps(c->nspecies, nullptr);
+  std::vector<int64_t> ms(c->nspecies, 0);
+  for (int s = 0; s < c->nspecies; ++s) {
+    std::vector<int> cnt(c->ntiles);
+    CUDA_OR_THROW(cudaMemcpy(cnt.data(), c->ps[s].cnt, c->ntiles * 4, cudaMemcpyDeviceToHost));
+    std::vector<int64_t> prefix(c->ntiles + 1, 0);
+    for (int t = 0; t < c->ntiles; ++t) prefix[t + 1] = prefix[t] + std::min(cnt[t], c->ps[s].cap);
+    const int64_t nt = prefix[c->ntiles], n = nt + nl;   // upper bound (the loose list mixes species)
+    char* tmp = (char*)dev_alloc(c, (size_t)std::max<int64_t>(n, 1) * 32);
+    int32_t* dix = (int32_t*)tmp;
+    int32_t* diy = dix + n;
+    float* dxx = (float*)(diy + n);
+    float* dyy = dxx + n;
+    float* dux = dyy + n;
+    float* duy = dux + n;
+    float* duz = duy + n;
+    uint32_t* did = (uint32_t*)(duz + n);
+    const bool ids = c->ps[s].nf > F_ID;
+    int64_t* dprefix = (int64_t*)dev_alloc(c, (c->ntiles + 1) * 8);
+    int* dn = alloc_n<int>(c, 1);
+    CUDA_OR_THROW(cudaMemcpyAsync(dprefix, prefix.data(), (c->ntiles + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+    launch_export(c->ps[s], c->ntiles, dprefix, c->y0, dix, diy, dxx, dyy, dux, duy, duz, ids ? did : nullptr, c->stream);
+    launch_loose_extract(L, s, c->y0, nt, dix, diy, dxx, dyy, dux, duy, duz, ids ? did : nullptr, dn, c->stream);
+    CUDA_OR_THROW(cudaGetLastError());
+    int ns = 0;
+    CUDA_OR_THROW(cudaMemcpyAsync(&ns, dn, 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+    dev_free(c, dprefix);
+    dev_free(c, dn);
+    // compact the SoA block to m = nt + ns entries per field (load_species expects that layout)
+    const int64_t m = nt + ns;
+    if (m < n) {
+      char* t2 = (char*)dev_alloc(c, (size_t)std::max<int64_t>(m, 1) * 32);
+      for (int f = 0; f < 8; ++f)
+        CUDA_OR_THROW(cudaMemcpyAsync(t2 + (size_t)f * m * 4, tmp + (size_t)f * n * 4, (size_t)m * 4,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+      CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+      dev_free(c, tmp);
+      tmp = t2;
+    }
+    tmps[s] = tmp;
+    ms[s] = m;
+  }
+  // 2. empty loose list; every species back into tiles sized for its largest tile (+10 %)
+  CUDA_OR_THROW(cudaMemsetAsync(L.count, 0, 4, c->stream));
+  for (int s = 0; s < c->nspecies; ++s) load_species(c, s, ms[s], tmps[s], c->ps[s].nf > F_ID);
+  c->repacking = false;
+  size_lists(c);
+  drop_graphs(c);
+  c->repacks += 1;
+}
+
+// Called between steps: re-pack when the loose list holds more than a quarter of its capacity
+// (or 4096 particles, whichever is larger).
+static void maybe_repack(zpic_ctx* c) {
+  if (c->since_check < kRepackCheck) return;
+  c->since_check = 0;
+  int nl = 0;
+  CUDA_OR_THROW(cudaMemcpyAsync(&nl, c->spill[c->steps & 1].count, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  if (nl > std::max<int64_t>(4096, std::min<int64_t>(c->spill[0].cap / 4, c->population / 64))) repack(c);
+}
+
 zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t* ix, const int32_t* iy, const float* x,
                                const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id) {
   if (!c) return ZPIC_E_INVALID;
@@ -582,7 +743,7 @@ zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t*
   }
   drop_graphs(c);
   try {
-    // upload, then validate + count per tile on the device
+    // upload, then validate + count per tile and bin on the device
     char* tmp = (char*)dev_alloc(c, (size_t)std::max<int64_t>(n, 1) * (7 * 4 + 4));
     int32_t* dix = (int32_t*)tmp;
     int32_t* diy = dix + n;
@@ -592,7 +753,6 @@ zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t*
     float* duy = dux + n;
     float* duz = duy + n;
     uint32_t* did = (uint32_t*)(duz + n);
-    int* dcounts = alloc_n<int>(c, c->ntiles + 1);
     if (n > 0) {
       CUDA_OR_THROW(cudaMemcpyAsync(dix, ix, n * 4, cudaMemcpyHostToDevice, c->stream));
       CUDA_OR_THROW(cudaMemcpyAsync(diy, iy, n * 4, cudaMemcpyHostToDevice, c->stream));
@@ -602,49 +762,9 @@ zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t*
       CUDA_OR_THROW(cudaMemcpyAsync(duy, uy, n * 4, cudaMemcpyHostToDevice, c->stream));
       CUDA_OR_THROW(cudaMemcpyAsync(duz, uz, n * 4, cudaMemcpyHostToDevice, c->stream));
       if (id) CUDA_OR_THROW(cudaMemcpyAsync(did, id, n * 4, cudaMemcpyHostToDevice, c->stream));
-      launch_count(c->T, c->ntx, c->g.nx, c->g.ny, c->y0, (long)n, dix, diy, dx_, dy_, dcounts, dcounts + c->ntiles,
-                   c->stream);
-      CUDA_OR_THROW(cudaGetLastError());
     }
-    std::vector<int> counts(c->ntiles + 1, 0);
-    CUDA_OR_THROW(cudaMemcpyAsync(counts.data(), dcounts, (c->ntiles + 1) * 4, cudaMemcpyDeviceToHost, c->stream));
-    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
-    dev_free(c, dcounts);
-    if (counts[c->ntiles]) {
-      dev_free(c, tmp);
-      throw Fail{ZPIC_E_INVALID, "set_particles: a particle is outside the local slab or its offset is not in [0,1)"};
-    }
-    int maxc = 0;
-    for (int t = 0; t < c->ntiles; ++t) maxc = std::max(maxc, counts[t]);
-    const int ppc = c->species[s].ppc[0] * c->species[s].ppc[1];
-    const int cap = std::max({32, round_up((int)std::ceil(maxc * c->opt.capacity_slack), 32),
-                              round_up((int)std::ceil(c->T * c->T * ppc * c->opt.capacity_slack), 32)});
-    free_store(c, s);
-    alloc_store(c, s, cap);
-    check_tile_capacity(c);
-    if (n > 0) {
-      launch_bin(c->ps[s], c->T, c->ntx, c->y0, (long)n, dix, diy, dx_, dy_, dux, duy, duz, id ? did : nullptr, c->err,
-                 c->stream);
-      CUDA_OR_THROW(cudaGetLastError());
-    }
-    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
-    dev_free(c, tmp);
-    // movers / loose lists sized for the new population
-    int64_t total = 0;
-    for (int q = 0; q < c->nspecies; ++q) {
-      std::vector<int> cnt(c->ntiles);
-      CUDA_OR_THROW(cudaMemcpy(cnt.data(), c->ps[q].cnt, c->ntiles * 4, cudaMemcpyDeviceToHost));
-      for (int v : cnt) total += v;
-    }
-    const int need = mover_capacity(c, total);
-    if (need > c->movers.cap) {
-      for (PList* L : {&c->movers, &c->spill[0], &c->spill[1]}) {
-        dev_free(c, L->cell); dev_free(c, L->x); dev_free(c, L->y); dev_free(c, L->ux); dev_free(c, L->uy);
-        dev_free(c, L->uz); dev_free(c, L->id); dev_free(c, L->species); dev_free(c, L->count);
-        *L = alloc_list(c, need);
-      }
-    }
-    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+    load_species(c, s, n, tmp, id != nullptr);
+    size_lists(c);
   } catch (const Fail& f) {
     c->last_error = f.msg;
     return f.st;
@@ -781,6 +901,7 @@ void step_phase_c(zpic_ctx* c, StepState& s) {
   }
   c->cur ^= 1;
   c->steps += 1;
+  c->since_check += 1;
   c->launches += s.launches;
 }
 
@@ -837,11 +958,13 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
     try {
       int k = 0;
       for (; k + 2 <= n; k += 2) {
+        maybe_repack(c);
         CUDA_OR_THROW(cudaGraphLaunch(two_step_graph(c), c->stream));
         c->steps += 2;
+        c->since_check += 2;
         c->launches += c->graph_launches;
       }
-      if (k < n) run_step(c);
+      if (k < n) { maybe_repack(c); run_step(c); }
     } catch (const Fail& f) {
       c->last_error = f.msg;
       return f.st;
@@ -859,6 +982,7 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
       c->halo_dirty = false;
     }
     for (int k = 0; k < n; ++k) {
+      maybe_repack(c);
       StepState s = step_phase_a(c);
       if (c->slab) {
         ProfScope ps(c, K_EXCHANGE);

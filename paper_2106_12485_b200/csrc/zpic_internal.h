@@ -164,6 +164,9 @@ struct zpic_ctx {
   int cur;         // index of the current E/B buffer
   int64_t steps;
   int64_t repacks;
+  int since_check = 0;   // steps since the last loose-list check (re-pack, zpic_api.cu)
+  bool repacking = false;
+  int64_t population = 0;  // particles at the last (re)load
   int64_t launches;  // kernels enqueued by zpic_step so far
   int64_t n_move;    // moving-window shifts so far
   // y-slab decomposition (§8(e)); slab == false: the whole domain, no exchanges

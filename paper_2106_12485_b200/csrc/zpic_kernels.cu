@@ -742,12 +742,17 @@ __global__ void k_count(int T, int ntx, int nx, int ny, int y0, long n, const in
 
 // Bin host-uploaded particles (global iy -> slab-local) into tiles.
 __global__ void k_bin(PStore ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
-                      const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err) {
+                      const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err,
+                      PList loose, int s) {
   for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
     const int cx = ix[k], cy = iy[k] - y0;
     const int t = (cy / T) * ntx + cx / T;
     const int slot = atomicAdd(ps.cnt + t, 1);
-    if (slot >= ps.cap) { atomicOr(err, ERR_OVERFLOW); continue; }
+    if (slot >= ps.cap) {   // tile full (capacity slack < 1): the loose list takes it
+      atomicSub(ps.cnt + t, 1);
+      list_append(loose, err, pack_cell(cx, cy), x[k], y[k], ux[k], uy[k], uz[k], id ? id[k] : (uint32_t)k, s);
+      continue;
+    }
     uint32_t* o = ps.slot((long)t * ps.cap + slot);
     o[F_CELL * 32] = (uint32_t)pack_cell(cx, cy);
     o[F_X * 32] = __float_as_uint(x[k]); o[F_Y * 32] = __float_as_uint(y[k]);
@@ -777,6 +782,25 @@ __global__ void k_export(PStore ps, const int64_t* prefix, int y0, int32_t* ix, 
 }
 
 // ---- host-side launchers --------------------------------------------------------------------
+// Re-pack: the loose particles of species s appended after out0 (global iy), in any order.
+__global__ void k_loose_extract(PList L, int s, int y0, int32_t* ix, int32_t* iy, float* x, float* y, float* ux,
+                                float* uy, float* uz, uint32_t* id, int* counter) {
+  const int n = min(*L.count, L.cap);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    if (L.species[k] != s) continue;
+    const int o = atomicAdd(counter, 1);
+    const int c = L.cell[k];
+    ix[o] = cell_ix(c); iy[o] = cell_iy(c) + y0;
+    x[o] = L.x[k]; y[o] = L.y[k]; ux[o] = L.ux[k]; uy[o] = L.uy[k]; uz[o] = L.uz[k];
+    if (id) id[o] = L.id ? L.id[k] : 0u;
+  }
+}
+void launch_loose_extract(const PList& L, int s, int y0, int64_t out0, int32_t* ix, int32_t* iy, float* x, float* y,
+                          float* ux, float* uy, float* uz, uint32_t* id, int* counter, cudaStream_t st) {
+  k_loose_extract<<<148 * 2, kBlock, 0, st>>>(L, s, y0, ix + out0, iy + out0, x + out0, y + out0, ux + out0, uy + out0,
+                                              uz + out0, id ? id + out0 : nullptr, counter);
+}
+
 void launch_mail_gather(const PushParams& p, cudaStream_t st) {
   const long warps = (long)p.ntx * p.nty * p.nspecies;
   k_mail_gather<<<(int)((warps * 32 + kBlock - 1) / kBlock), kBlock, 0, st>>>(p);
@@ -810,9 +834,9 @@ void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nsp
 void launch_inject(const InjectParams& q, int ntiles, cudaStream_t st) { k_inject<<<ntiles, kBlock, 0, st>>>(q); }
 void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
                 const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err,
-                cudaStream_t st) {
+                const PList& loose, int s, cudaStream_t st) {
   const int grid = (int)std::min<long>((n + kBlock - 1) / kBlock, 148L * 32);
-  if (grid > 0) k_bin<<<grid, kBlock, 0, st>>>(ps, T, ntx, y0, n, ix, iy, x, y, ux, uy, uz, id, err);
+  if (grid > 0) k_bin<<<grid, kBlock, 0, st>>>(ps, T, ntx, y0, n, ix, iy, x, y, ux, uy, uz, id, err, loose, s);
 }
 void launch_inject_column(const PushParams& p, int s, int px, int py, int n_move, int ny_global, int y0, uint64_t key,
                           const double* ufl, const double* uth, cudaStream_t st) {

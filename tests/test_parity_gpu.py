@@ -359,3 +359,73 @@ def test_vacuum_wave_matches_oracle():
     assert rel_l2(g.fields(0), o.fields(0)) < 1e-5
     assert rel_l2(g.fields(1), o.fields(1)) < 1e-5
     g.close()
+
+
+def _b_energy(sim, cfg):
+    B = sim.fields(1).astype(np.float64)
+    return 0.5 * cfg["dx"] * cfg["dy"] * float(np.sum(B * B))
+
+
+def test_p12_weibel_field_growth_full_c2():
+    """SURVEY.md P12 (physics sanity, not parity): in BASELINE.json's configs[1] (C2, full size,
+    the 500-step run) the counter-streaming electrons filament and the magnetic energy grows by
+    orders of magnitude (SPEC: B-energy(500) >= 10 x B-energy(10)); the total energy stays within
+    a few per cent (leapfrog with a charge-conserving current)."""
+    cfg = synth.config("C2")
+    sim = _z().Simulation(cfg, inject=True)
+    sim.step(10)
+    b10 = _b_energy(sim, cfg)
+    _, fe0, ke0 = sim.energy()
+    sim.step(490)
+    b500 = _b_energy(sim, cfg)
+    it, fe, ke = sim.energy()
+    assert it == 499
+    assert b500 >= 10 * b10, (b10, b500)
+    tot0, tot = fe0 + sum(ke0), fe + sum(ke)
+    assert abs(tot - tot0) <= 0.05 * tot0, (tot0, tot)
+    sim.close()
+
+
+def test_p12_thermal_plasma_stable_full_c1():
+    """P12: BASELINE.json configs[0] (C1, 100 steps): a uniform thermal plasma stays uniform and
+    stable — kinetic energy drifts by < 2 %, the field energy stays a small fraction of it, and no
+    particle is lost."""
+    cfg = synth.config("C1")
+    sim = _z().Simulation(cfg, inject=True)
+    n0 = sim.counters()["particles"]
+    sim.step(1)
+    _, fe0, ke0 = sim.energy()
+    sim.step(99)
+    _, fe, ke = sim.energy()
+    assert abs(ke[0] - ke0[0]) <= 0.02 * ke0[0], (ke0, ke)
+    assert fe <= 0.05 * ke[0], (fe, ke)
+    assert sim.counters()["particles"] == n0
+    sim.close()
+
+
+def test_repack_when_loose_list_grows():
+    """Tile capacity slack 0.97: 3 % of the particles start in the loose list (global-memory
+    push, re-inserted where slack appears) and thermal fluctuations keep it populated; at the
+    check after 16 steps the library re-packs every species into tiles sized for the current
+    largest tile (+10 %).  Same results as the oracle across the re-pack: the particle set (ids),
+    fields after 18 steps, energies."""
+    cfg = synth.config("C1", nx=128, ny=128)
+    cfg["species"][0]["uth"] = (0.4, 0.4, 0.4)
+    parts = [synth.species_particles(cfg, 0)]
+    g = gpu_from_particles(cfg, parts, tile=16, slack=0.97)
+    o = from_config(cfg, particles=parts)
+    fe_g, fe_o = [], []
+    for n in range(18):
+        g.step(1)
+        o.step()
+        fe_g.append(g.energy()[1])
+        fe_o.append(o.fe[-1])
+    cnt = g.counters()
+    assert cnt["repacks"] >= 1, cnt
+    assert cnt["particles"] == len(parts[0]["ix"])
+    c = compare_particles(g.particles(0, True), oracle_particles(o, 0), cfg["nx"], cfg["ny"])
+    assert c["cell_exact_frac"] >= CELL_FRAC, c
+    for w in (0, 1):
+        assert rel_l2(g.fields(w), o.fields(w)) <= FIELD_TOL, (w, rel_l2(g.fields(w), o.fields(w)))
+    assert energy_agreement(fe_g, fe_o) <= ENERGY_TOL
+    g.close()
