@@ -61,15 +61,26 @@ def host_loaded(sim, cfg, synth, world, rank):
         sim.set_fields(1, B)
 
 
+def full_count(cfg):
+    """Particles of a config's uniform species (nx ny ppc each); None if a species is not uniform."""
+    n = 0
+    for sp in cfg["species"]:
+        if sp.get("profile", "uniform") != "uniform":
+            return None
+        n += cfg["nx"] * cfg["ny"] * sp["ppc"][0] * sp["ppc"][1]
+    return n
+
+
 def workload_name(name, cfg, n_particles):
     """config.workload: the synth config, its BASELINE.json index if it is one, and its shape."""
     idx = {"C1": 0, "C2": 1, "C3": 2, "C4": 3, "C5": 4}.get(name)
     sp = cfg["species"]
     ppc = "+".join("%dx%d" % tuple(s["ppc"]) for s in sp)
     bc = {0: "periodic", 1: "open", 2: "window"}
-    return "%s%s: %dx%d cells, %d species, ppc %s, %d particles, bc x %s / y %s" % (
+    count = "%d particles, " % n_particles if n_particles is not None else ""
+    return "%s%s: %dx%d cells, %d species, ppc %s, %sbc x %s / y %s" % (
         cfg["name"], " (BASELINE.json configs[%d])" % idx if idx is not None else " (SURVEY.md NEXT-3)",
-        cfg["nx"], cfg["ny"], len(sp), ppc, n_particles, bc[cfg["bc"][0]], bc[cfg["bc"][1]])
+        cfg["nx"], cfg["ny"], len(sp), ppc, count, bc[cfg["bc"][0]], bc[cfg["bc"][1]])
 
 
 def measured_peaks():
@@ -160,8 +171,10 @@ def run_reference(args, world, rank):
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "%s physics, %dx%d-cell sample" % (args.config, args.cpu_cells, args.cpu_cells),
-                       "particles": n},
+            "config": {"workload": workload_name(args.config, synth.config(args.config), full_count(synth.config(args.config))),
+                       "sample": "%s physics on a %dx%d-cell periodic patch, %d particles (the oracle takes ~3 s "
+                                 "per step there; the full workload would take hours)" % (args.config, args.cpu_cells,
+                                                                                           args.cpu_cells, n)},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": "%dx%d-cell periodic patch of %s, %d particles, %d steps"
                                        % (args.cpu_cells, args.cpu_cells, args.config, n, args.steps)},
