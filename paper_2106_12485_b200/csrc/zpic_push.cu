@@ -346,10 +346,13 @@ static void launch_push_T(const PushParams& p, int ntiles, cudaStream_t st) {
   constexpr int W = T + 2, WJ = T + 3;
   constexpr size_t smem = (size_t)W * W * (2 * sizeof(float2) + 2 * sizeof(float)) +
                           (size_t)2 * ((3 * WJ * WJ + 3) & ~3) * sizeof(int) + (size_t)6 * (BLK / 32) * kQRing * sizeof(int);
-  static bool attr = false;
-  if (!attr) {
+  // the attribute is per device: set it once for every device this process launches on
+  static unsigned attr_set = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 32 || !((attr_set >> dev) & 1u)) {
     cudaFuncSetAttribute(k_push_tiles<T, BLK, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr = true;
+    if (dev < 32) attr_set |= 1u << dev;
   }
   k_push_tiles<T, BLK, MINB><<<ntiles, BLK, smem, st>>>(p);
 }
