@@ -170,6 +170,14 @@ zpic_status zpic_sync(zpic_ctx* ctx);
  * 3 = J of the last step before the filter.  out: 3*nx*ny_local floats [comp][y][x]. */
 zpic_status zpic_get_fields(zpic_ctx* ctx, int32_t which, float* out, size_t out_len);
 
+/* Diagnostics (validation only): the charge density at the nodes from the
+ * current particle positions, summed over species, rho(i, j) = sum_p q_s * W, with the bilinear
+ * area weights W = (1-x)(1-y), x(1-y), (1-x)y, xy to nodes (ix, iy), (ix+1, iy), (ix, iy+1),
+ * (ix+1, iy+1), node indices wrapped periodically in x and (one domain) y.
+ * With a slab decomposition, nodes beyond the slab's rows are dropped.  out: nx*ny_local floats
+ * [y][x].  Errors: ZPIC_E_INVALID, ZPIC_E_BUFSIZE, ZPIC_E_CUDA. */
+zpic_status zpic_get_charge(zpic_ctx* ctx, float* out, size_t out_len);
+
 /* Size query when ix == NULL (count_inout <- count).  Otherwise fills up to *count_inout
  * particles (order unspecified) with global ix, iy; id requires track_ids (may be NULL). */
 zpic_status zpic_get_particles(zpic_ctx* ctx, int32_t species, int64_t* count_inout, int32_t* ix,

@@ -17,6 +17,7 @@ namespace zpic {
 void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st);
 void launch_insert(const PushParams& p, int grid, cudaStream_t st);
 void launch_mail_gather(const PushParams& p, cudaStream_t st);
+void launch_charge(const PushParams& p, float* rho, int wrap_y, cudaStream_t st);
 void launch_loose_extract(const PList& L, int s, int y0, int64_t out0, int32_t* ix, int32_t* iy, float* x, float* y,
                           float* ux, float* uy, float* uz, uint32_t* id, int* counter, cudaStream_t st);
 void launch_loose(const PushParams& p, int grid, cudaStream_t st);
@@ -1166,6 +1167,27 @@ zpic_status zpic_energy(zpic_ctx* c, int64_t* iter, double* field, double* kinet
   if (field) *field = e[0];
   if (kinetic)
     for (int s = 0; s < c->nspecies; ++s) kinetic[s] = e[1 + s];
+  return ZPIC_OK;
+}
+
+zpic_status zpic_get_charge(zpic_ctx* c, float* out, size_t out_len) {
+  if (!c || !out) return ZPIC_E_INVALID;
+  zpic_status st = check_sticky(c);
+  if (st != ZPIC_OK) return st;
+  const GridDesc& g = c->g;
+  if (out_len < (size_t)g.nx * g.ny) { c->last_error = "get_charge: buffer too small"; return ZPIC_E_BUFSIZE; }
+  try {
+    float* rho = alloc_n<float>(c, (size_t)g.nx * g.ny);   // zeroed
+    const PushParams p = push_params(c);                    // spill_in = the live loose list
+    launch_charge(p, rho, !c->slab && c->bcy == ZPIC_BC_PERIODIC ? 1 : 0, c->stream);
+    CUDA_OR_THROW(cudaGetLastError());
+    CUDA_OR_THROW(cudaMemcpyAsync(out, rho, (size_t)g.nx * g.ny * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+    dev_free(c, rho);
+  } catch (const Fail& f) {
+    c->last_error = f.msg;
+    return f.st;
+  }
   return ZPIC_OK;
 }
 

@@ -761,6 +761,47 @@ __global__ void k_bin(PStore ps, int T, int ntx, int y0, long n, const int32_t* 
   }
 }
 
+// Diagnostic charge density (zpic_get_charge): one CTA per tile (and one grid-stride pass over
+// the loose list), fp32 global atomics into an [ny][nx] node grid, indices wrapped (x, and y
+// unless a slab), nodes outside dropped.
+__device__ __forceinline__ void charge_add(float* rho, int nx, int ny, bool wrap_y, int i, int j, float v) {
+  if (i >= nx) i -= nx;
+  if (j >= ny) {
+    if (!wrap_y) return;
+    j -= ny;
+  }
+  atomicAdd(rho + (long)j * nx + i, v);
+}
+__device__ __forceinline__ void charge_particle(float* rho, int nx, int ny, bool wrap_y, int c, float x, float y, float q) {
+  const int i = cell_ix(c), j = cell_iy(c);
+  charge_add(rho, nx, ny, wrap_y, i, j, q * (1.f - x) * (1.f - y));
+  charge_add(rho, nx, ny, wrap_y, i + 1, j, q * x * (1.f - y));
+  charge_add(rho, nx, ny, wrap_y, i, j + 1, q * (1.f - x) * y);
+  charge_add(rho, nx, ny, wrap_y, i + 1, j + 1, q * x * y);
+}
+__global__ void k_charge(PushParams p, float* rho, int wrap_y) {
+  const int t = blockIdx.x;
+  if (t < p.ntx * p.nty) {
+    for (int s = 0; s < p.nspecies; ++s) {
+      const PStore& ps = p.ps[s];
+      const int n = min(ps.cnt[t], ps.cap);
+      for (int k = threadIdx.x; k < n; k += blockDim.x) {
+        const uint32_t* q = ps.slot((long)t * ps.cap + k);
+        charge_particle(rho, p.g.nx, p.g.ny, wrap_y, (int)q[F_CELL * 32], __uint_as_float(q[F_X * 32]),
+                        __uint_as_float(q[F_Y * 32]), p.sc[s].q);
+      }
+    }
+  } else {
+    const int n = min(*p.spill_in.count, p.spill_in.cap);
+    for (int k = (t - p.ntx * p.nty) * blockDim.x + threadIdx.x; k < n; k += 148 * blockDim.x)
+      charge_particle(rho, p.g.nx, p.g.ny, wrap_y, p.spill_in.cell[k], p.spill_in.x[k], p.spill_in.y[k],
+                      p.sc[p.spill_in.species[k]].q);
+  }
+}
+void launch_charge(const PushParams& p, float* rho, int wrap_y, cudaStream_t st) {
+  k_charge<<<p.ntx * p.nty + 148, kBlock, 0, st>>>(p, rho, wrap_y);
+}
+
 // Copy every tile segment of one species to a contiguous buffer (prefix[t] = output offset);
 // global ix, iy on the way out.
 __global__ void k_export(PStore ps, const int64_t* prefix, int y0, int32_t* ix, int32_t* iy, float* x, float* y,

@@ -77,6 +77,7 @@ _lib.zpic_set_fields.argtypes = [_P, ctypes.c_int32, _F32P, ctypes.c_size_t]
 _lib.zpic_step.argtypes = [_P, ctypes.c_int32]
 _lib.zpic_sync.argtypes = [_P]
 _lib.zpic_get_fields.argtypes = [_P, ctypes.c_int32, _F32P, ctypes.c_size_t]
+_lib.zpic_get_charge.argtypes = [_P, _F32P, ctypes.c_size_t]
 _lib.zpic_get_particles.argtypes = [_P, ctypes.c_int32, _I64P, _I32P, _I32P, _F32P, _F32P, _F32P, _F32P, _F32P, _U32P]
 _lib.zpic_energy.argtypes = [_P, _I64P, _F64P, _F64P]
 _lib.zpic_layout.argtypes = [_P, _I32P, _I32P]
@@ -94,7 +95,7 @@ for _f in ("zpic_init", "zpic_set_particles", "zpic_set_fields", "zpic_step", "z
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ["zpic_init", "zpic_set_particles", "zpic_set_fields", "zpic_step", "zpic_step_group", "zpic_sync",
-            "zpic_get_fields", "zpic_get_particles", "zpic_energy", "zpic_layout", "zpic_counters",
+            "zpic_get_fields", "zpic_get_charge", "zpic_get_particles", "zpic_energy", "zpic_layout", "zpic_counters",
             "zpic_kernel_times", "zpic_nccl_unique_id", "zpic_free", "zpic_last_error"]
 
 
@@ -174,6 +175,13 @@ def zpic_get_fields(ctx, which, nx, ny_local, out=None):
     if out is None:
         out = np.empty((3, ny_local, nx), dtype=np.float32)
     _check(_lib.zpic_get_fields(ctx, which, _ptr(out, _F32P), out.size), ctx)
+    return out
+
+
+def zpic_get_charge(ctx, nx, ny_local, out=None):
+    if out is None:
+        out = np.empty((ny_local, nx), dtype=np.float32)
+    _check(_lib.zpic_get_charge(ctx, _ptr(out, _F32P), out.size), ctx)
     return out
 
 
@@ -311,6 +319,10 @@ class Simulation:
     def fields(self, which):
         y0, nyl = zpic_layout(self.ctx)
         return zpic_get_fields(self.ctx, which, self.nx, nyl)
+
+    def charge(self):
+        y0, nyl = zpic_layout(self.ctx)
+        return zpic_get_charge(self.ctx, self.nx, nyl)
 
     def particles(self, s, with_id=False):
         return zpic_get_particles(self.ctx, s, with_id)

@@ -429,3 +429,22 @@ def test_repack_when_loose_list_grows():
         assert rel_l2(g.fields(w), o.fields(w)) <= FIELD_TOL, (w, rel_l2(g.fields(w), o.fields(w)))
     assert energy_agreement(fe_g, fe_o) <= ENERGY_TOL
     g.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C2"])
+def test_get_charge_diagnostic(name):
+    """zpic_get_charge (SURVEY.md §8(b) diagnostics) equals the host-side bilinear node charge of
+    the exported particles (R21), and with it the discrete continuity equation holds on the GPU
+    path: |rho^{n+1} - rho^n + dt div J^{n+1/2}| <= 1e-5 (north star)."""
+    cfg = synth.config(name, nx=48, ny=40)
+    parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
+    g = gpu_from_particles(cfg, parts)
+    q = [synth.configs.charge(sp) for sp in cfg["species"]]
+    rho0 = g.charge().astype(np.float64)
+    host0 = sum(rho_nodes(cfg["nx"], cfg["ny"], q[s], g.particles(s)) for s in range(len(parts)))
+    assert np.max(np.abs(rho0 - host0)) <= 1e-5 * max(1.0, np.max(np.abs(host0)))
+    g.step(1)
+    rho1 = g.charge().astype(np.float64)
+    r = continuity_residual(cfg["nx"], cfg["ny"], cfg["dx"], cfg["dy"], cfg["dt"], rho0, rho1, g.fields(3), cfg["bc"])
+    assert r <= CONT_TOL, r
+    g.close()
