@@ -44,23 +44,6 @@ def k1_traffic(config, nx, ny):
     return None
 
 
-def host_loaded(sim, cfg, synth, world, rank):
-    """Species the device injector does not generate (the C4 / P-LWFA density ramp) and the C4
-    laser are built host-side by synth and loaded through zpic_set_particles / zpic_set_fields
-    (single GPU only; the slab runs use device-injected configs)."""
-    ramp = [s for s, sp in enumerate(cfg["species"]) if sp.get("profile") == "ramp"]
-    if not ramp and "laser" not in cfg:
-        return
-    if world > 1:
-        raise SystemExit("ramp / laser configs are benchmarked on one GPU")
-    for s in ramp:
-        sim.set_particles(s, synth.species_particles(cfg, s))
-    if "laser" in cfg:
-        E, B = synth.laser_fields(cfg)
-        sim.set_fields(0, E)
-        sim.set_fields(1, B)
-
-
 def full_count(cfg):
     """Particles of a config's uniform species (nx ny ppc each); None if a species is not uniform."""
     n = 0
@@ -192,7 +175,6 @@ def e2e_run(args, cfg, torch, z, dist_kw=None, world=1):
         dist_kw = dict(dist_kw, nccl_id=nccl_id_broadcast())
     import synth
     src = z.Simulation(cfg, inject=True, dist=dist_kw, tile=args.tile)
-    host_loaded(src, cfg, synth, world, 0)
     host = []
     for s in range(len(cfg["species"])):
         p = src.particles(s)
@@ -283,7 +265,6 @@ def main():
         dist_kw = {"rank": rank, "world": world, "transport": "nccl", "nccl_id": nccl_id_broadcast(), "device": local}
     sim = z.Simulation(cfg, inject=True, profile=not args.graphs, tile=args.tile, dist=dist_kw,
                        current_mode=args.current_mode)
-    host_loaded(sim, cfg, synth, world, rank)
     n_particles = sim.counters()["particles"]
     n_cells = cfg["nx"] * cfg["ny"]
     sim.step(args.warmup)

@@ -73,7 +73,12 @@ typedef struct {
 typedef enum {
   ZPIC_DENS_UNIFORM = 0, /* n everywhere */
   ZPIC_DENS_SLAB = 1,    /* n for cell-centre x in [x0, x1), 0 elsewhere */
-  ZPIC_DENS_NONE = 2     /* no particles from zpic_init: load them with zpic_set_particles */
+  ZPIC_DENS_NONE = 2,    /* no particles from zpic_init: load them with zpic_set_particles */
+  ZPIC_DENS_RAMP = 3     /* 0 for x < x0, linear 0 -> n over [x0, x1), n beyond:
+                            along x every y sub-row places its particles by inverting the
+                            cumulative density, X_k = x0 + sqrt(2 L (k + 1/2) dx / ppc_x) in the
+                            ramp (L = x1 - x0), the regular sub-lattice from x1 on; ids follow the
+                            sub-row-major order of that list */
 } zpic_dens;
 
 /* One species.  The device injector (zpic_init) fills the ppc_x x ppc_y regular sub-lattice
@@ -111,6 +116,12 @@ typedef struct {
                                      and K4 sums the overlapping guard nodes (no atomics);
                                  1 = "commutative": every tile adds its block into the global J with
                                      fp32 global atomics (J zeroed first each step, no K4). */
+  int32_t laser;              /* 1 = initialise E, B with a laser pulse: linearly
+                                 polarised along y, travelling along +x, E_y = a0 w0 env(x)
+                                 exp(-(y - Ly/2)^2 / W0^2) cos(w0 (x - xc)), B_z = E_y at B_z's points;
+                                 env = sin^2 rise and fall of length fwhm each ending at x = start,
+                                 xc = start - fwhm (no divergence cleaning) */
+  double laser_a0, laser_omega0, laser_fwhm, laser_W0, laser_start;
   int32_t no_graphs;          /* 0 (default): zpic_step replays a captured CUDA graph of two steps
                                  when it can (single domain, no moving window, profile = 0), which
                                  removes the per-launch host cost of small grids; 1 = plain launches */

@@ -18,6 +18,11 @@ void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st);
 void launch_insert(const PushParams& p, int grid, cudaStream_t st);
 void launch_mail_gather(const PushParams& p, cudaStream_t st);
 void launch_charge(const PushParams& p, float* rho, int wrap_y, cudaStream_t st);
+void launch_ramp_rows(long n, int n_row, int py, int y0, const int32_t* ixr, const float* xr, uint64_t key,
+                      const double* ufl, const double* uth, int32_t* ix, int32_t* iy, float* x, float* y, float* ux,
+                      float* uy, float* uz, uint32_t* id, cudaStream_t st);
+void launch_laser(float* E, float* B, const GridDesc& g, int y0, double dx, double dy, const LaserParams& L,
+                  cudaStream_t st);
 void launch_loose_extract(const PList& L, int s, int y0, int64_t out0, int32_t* ix, int32_t* iy, float* x, float* y,
                           float* ux, float* uy, float* uz, uint32_t* id, int* counter, cudaStream_t st);
 void launch_loose(const PushParams& p, int grid, cudaStream_t st);
@@ -395,6 +400,33 @@ extern "C" {
 
 const char* zpic_last_error(const zpic_ctx* ctx) { return ctx ? ctx->last_error.c_str() : g_init_error.c_str(); }
 
+static void load_species(zpic_ctx* c, int s, int64_t n, char* tmp, bool has_id);
+static void size_lists(zpic_ctx* c);
+
+// The one x sub-row of a ramp species (R16), in the oracle-independent arithmetic of the library:
+// ramp positions by cumulative inversion, then the regular sub-lattice from x1 on; cell index and
+// fp32 offset with the R6 rule.
+static void ramp_row(const zpic_species& sp, int nx, double dx, std::vector<int32_t>& ix, std::vector<float>& x) {
+  const int px = sp.ppc[0];
+  const double x0 = sp.x0, x1 = sp.x1, L = x1 - x0;
+  std::vector<double> X;
+  const long nramp = (long)std::nearbyint(px * L / (2.0 * dx));
+  for (long k = 0; k < nramp; ++k) X.push_back(x0 + std::sqrt(2.0 * L * ((double)k + 0.5) * dx / px));
+  const int first = (int)std::ceil(x1 / dx - 1e-9);
+  for (int col = std::max(first, 0); col < nx; ++col)
+    for (int k = 0; k < px; ++k) X.push_back(((double)col + ((double)k + 0.5) / px) * dx);
+  ix.clear(); x.clear();
+  for (double Xv : X) {
+    const double gx = Xv / dx;
+    int i = (int)std::floor(gx);
+    float f = (float)(gx - i);
+    if (f >= 1.0f) { i += 1; f = 0.0f; }
+    if (i < 0 || i >= nx) continue;
+    ix.push_back(i);
+    x.push_back(f);
+  }
+}
+
 zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zpic_species* species, int32_t n_species,
                       const zpic_boundaries* bc, uint64_t seed, const zpic_options* options, const zpic_dist* dist) {
   if (!out || !grid || !species || !bc) { g_init_error = "NULL argument"; return ZPIC_E_INVALID; }
@@ -514,7 +546,7 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
         col_hi = std::max(col_lo, std::min(g.nx, col_hi));
       }
       int maxcount = c->T * c->T * ppc;
-      if (sp.profile == ZPIC_DENS_NONE || sp.n == 0.0) { col_lo = col_hi = 0; }
+      if (sp.profile == ZPIC_DENS_NONE || sp.profile == ZPIC_DENS_RAMP || sp.n == 0.0) { col_lo = col_hi = 0; }
       // the device injector writes every lattice particle into its tile: no less than a full tile
       const int cap = std::max(32, round_up((int)std::ceil(maxcount * std::max(1.0, c->opt.capacity_slack)), 32));
       if ((double)cap * c->ntiles > 2.0e9) throw Fail{ZPIC_E_INVALID, "particle store exceeds 2^31 slots"};
@@ -539,6 +571,50 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     c->spill[1] = alloc_list(c, (int)mcap);
     c->cur = 0;
     c->steps = 0;
+    // ramp species (R16): generated on the device from one host-computed x sub-row, then binned
+    bool ramped = false;
+    for (int s = 0; s < n_species; ++s) {
+      const zpic_species& sp = species[s];
+      if (sp.profile != ZPIC_DENS_RAMP || !(sp.n > 0)) continue;
+      std::vector<int32_t> ixr;
+      std::vector<float> xr;
+      ramp_row(sp, g.nx, grid->dx, ixr, xr);
+      const int n_row = (int)ixr.size();
+      const int64_t n = (int64_t)n_row * g.ny * sp.ppc[1];
+      int32_t* dixr = alloc_n<int32_t>(c, std::max(n_row, 1));
+      float* dxr = alloc_n<float>(c, std::max(n_row, 1));
+      CUDA_OR_THROW(cudaMemcpyAsync(dixr, ixr.data(), n_row * 4, cudaMemcpyHostToDevice, c->stream));
+      CUDA_OR_THROW(cudaMemcpyAsync(dxr, xr.data(), n_row * 4, cudaMemcpyHostToDevice, c->stream));
+      char* tmp = (char*)dev_alloc(c, (size_t)std::max<int64_t>(n, 1) * 32);
+      int32_t* dix = (int32_t*)tmp;
+      int32_t* diy = dix + n;
+      float* dxx = (float*)(diy + n);
+      float* dyy = dxx + n;
+      float* dux = dyy + n;
+      float* duy = dux + n;
+      float* duz = duy + n;
+      uint32_t* did = (uint32_t*)(duz + n);
+      launch_ramp_rows((long)n, n_row, sp.ppc[1], c->y0, dixr, dxr, host_mix64(host_mix64(seed) + (uint64_t)s), sp.ufl,
+                       sp.uth, dix, diy, dxx, dyy, dux, duy, duz, c->opt.track_ids ? did : nullptr, c->stream);
+      CUDA_OR_THROW(cudaGetLastError());
+      load_species(c, s, n, tmp, c->opt.track_ids != 0);
+      dev_free(c, dixr);
+      dev_free(c, dxr);
+      ramped = true;
+    }
+    if (ramped) size_lists(c);
+    // laser initial fields (R17)
+    if (c->opt.laser) {
+      const LaserParams L{c->opt.laser_a0, c->opt.laser_omega0, c->opt.laser_fwhm, c->opt.laser_W0, c->opt.laser_start,
+                          0.5 * grid->ny * grid->dy};
+      if (!(L.fwhm > 0) || !(L.W0 > 0)) throw Fail{ZPIC_E_LASER, "laser: fwhm and W0 must be > 0"};
+      if (L.start - 2.0 * L.fwhm < 0.0 || L.start > grid->nx * grid->dx)
+        throw Fail{ZPIC_E_LASER, "laser: the pulse [start - 2 fwhm, start] must lie inside the box"};
+      launch_laser(c->E[0], c->B[0], g, c->y0, grid->dx, grid->dy, L, c->stream);
+      CUDA_OR_THROW(cudaGetLastError());
+      refresh_field_guards(c, c->E[0], true);
+      refresh_field_guards(c, c->B[0], false);
+    }
     if (c->slab) {
       // halo buffers: raw J rows from both neighbours; particle messages sized for two rows of
       // cells at 2x the densest species sum (a particle crosses at most one row per step)

@@ -128,6 +128,10 @@ struct InjectParams {
   double ufl[3], uth[3];
 };
 
+struct LaserParams {
+  double a0, omega0, fwhm, W0, start, yc;
+};
+
 enum ErrBits { ERR_OVERFLOW = 1, ERR_MIGRATION = 2 };
 
 }  // namespace zpic

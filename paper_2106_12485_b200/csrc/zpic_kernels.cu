@@ -761,6 +761,59 @@ __global__ void k_bin(PStore ps, int T, int ntx, int y0, long n, const int32_t* 
   }
 }
 
+// Ramp species (ZPIC_DENS_RAMP, R16): the host gives one x sub-row (cell ix_r[c], offset x_r[c],
+// c < n_row); every y sub-row r of the slab repeats it at y = ((r mod py) + 1/2) / py, with
+// id = r_global n_row + c and the seeded momenta.  Output: the flat SoA block of load_species.
+__global__ void k_ramp_rows(long n, int n_row, int py, int y0, const int32_t* ixr, const float* xr, uint64_t key,
+                            double ufl0, double ufl1, double ufl2, double uth0, double uth1, double uth2, int32_t* ix,
+                            int32_t* iy, float* x, float* y, float* ux, float* uy, float* uz, uint32_t* id) {
+  for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const long r = (long)y0 * py + k / n_row;   // global sub-row
+    const int c = (int)(k % n_row);
+    const uint64_t gid = (uint64_t)r * n_row + c;
+    ix[k] = ixr[c];
+    iy[k] = (int)(r / py);
+    x[k] = xr[c];
+    y[k] = (float)(((double)(r % py) + 0.5) / py);
+    ux[k] = thermal(key, gid, 0, ufl0, uth0);
+    uy[k] = thermal(key, gid, 1, ufl1, uth1);
+    uz[k] = thermal(key, gid, 2, ufl2, uth2);
+    if (id) id[k] = (uint32_t)gid;
+  }
+}
+void launch_ramp_rows(long n, int n_row, int py, int y0, const int32_t* ixr, const float* xr, uint64_t key,
+                      const double* ufl, const double* uth, int32_t* ix, int32_t* iy, float* x, float* y, float* ux,
+                      float* uy, float* uz, uint32_t* id, cudaStream_t st) {
+  const int grid = (int)std::min<long>((n + kBlock - 1) / kBlock, 148L * 32);
+  if (grid > 0)
+    k_ramp_rows<<<grid, kBlock, 0, st>>>(n, n_row, py, y0, ixr, xr, key, ufl[0], ufl[1], ufl[2], uth[0], uth[1],
+                                         uth[2], ix, iy, x, y, ux, uy, uz, id);
+}
+
+// Laser initial fields (zpic_options.laser, R17): E_y at (i, j + 1/2), B_z at (i + 1/2, j + 1/2)
+// of the slab's interior (global row j = y0 + local), fp64 then rounded; other components 0.
+__device__ __forceinline__ double laser_profile(const LaserParams& L, double xp, double yp) {
+  const double lo = L.start - 2.0 * L.fwhm;
+  if (!(xp >= lo && xp <= L.start)) return 0.0;
+  const double s = sin(3.141592653589793 * (xp - lo) / (2.0 * L.fwhm));
+  const double dy = yp - L.yc;
+  return L.a0 * L.omega0 * (s * s) * exp(-(dy * dy) / (L.W0 * L.W0)) * cos(L.omega0 * (xp - (L.start - L.fwhm)));
+}
+__global__ void k_laser(float* E, float* B, GridDesc g, int y0, double dx, double dy, LaserParams L) {
+  const long n = (long)g.nx * g.ny;
+  for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
+    const int i = (int)(k % g.nx), j = (int)(k / g.nx);
+    const double yj = ((double)(y0 + j) + 0.5) * dy;
+    E[g.plane + g.at(i, j)] = (float)laser_profile(L, (double)i * dx, yj);
+    B[2 * g.plane + g.at(i, j)] = (float)laser_profile(L, ((double)i + 0.5) * dx, yj);
+  }
+}
+void launch_laser(float* E, float* B, const GridDesc& g, int y0, double dx, double dy, const LaserParams& L,
+                  cudaStream_t st) {
+  const int grid = (int)std::min<long>(((long)g.nx * g.ny + kBlock - 1) / kBlock, 148L * 32);
+  k_laser<<<grid, kBlock, 0, st>>>(E, B, g, y0, dx, dy, L);
+}
+
 // Diagnostic charge density (zpic_get_charge): one CTA per tile (and one grid-stride pass over
 // the loose list), fp32 global atomics into an [ny][nx] node grid, indices wrapped (x, and y
 // unless a slab), nodes outside dropped.

@@ -24,7 +24,7 @@ STATUS = {0: "ZPIC_OK", -1: "ZPIC_E_INVALID", -2: "ZPIC_E_CFL", -3: "ZPIC_E_EMPT
           -5: "ZPIC_E_LASER", -6: "ZPIC_E_OOM", -7: "ZPIC_E_CUDA", -8: "ZPIC_E_NCCL", -9: "ZPIC_E_OVERFLOW",
           -10: "ZPIC_E_MIGRATION", -11: "ZPIC_E_BUFSIZE", -12: "ZPIC_E_STATE"}
 BC_PERIODIC, BC_OPEN, BC_MOVING_WINDOW = 0, 1, 2
-DENS_UNIFORM, DENS_SLAB, DENS_NONE = 0, 1, 2
+DENS_UNIFORM, DENS_SLAB, DENS_NONE, DENS_RAMP = 0, 1, 2, 3
 
 
 class zpic_grid(ctypes.Structure):
@@ -50,7 +50,9 @@ class zpic_options(ctypes.Structure):
                 ("track_ids", ctypes.c_int32), ("tile", ctypes.c_int32 * 2), ("capacity_slack", ctypes.c_double),
                 ("mover_fraction", ctypes.c_double), ("profile", ctypes.c_int32), ("stream", ctypes.c_void_p),
                 ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", ctypes.c_void_p),
-                ("current_mode", ctypes.c_int32), ("no_graphs", ctypes.c_int32)]
+                ("current_mode", ctypes.c_int32), ("laser", ctypes.c_int32), ("laser_a0", ctypes.c_double),
+                ("laser_omega0", ctypes.c_double), ("laser_fwhm", ctypes.c_double), ("laser_W0", ctypes.c_double),
+                ("laser_start", ctypes.c_double), ("no_graphs", ctypes.c_int32)]
 
 
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
@@ -252,7 +254,8 @@ class Simulation:
         bc = zpic_boundaries(*cfg["bc"])
         sps = []
         for s in cfg["species"]:
-            prof = {"uniform": DENS_UNIFORM, "slab": DENS_SLAB}.get(s.get("profile", "uniform"), DENS_NONE)
+            prof = {"uniform": DENS_UNIFORM, "slab": DENS_SLAB, "ramp": DENS_RAMP}.get(s.get("profile", "uniform"),
+                                                                                    DENS_NONE)
             if not inject:
                 prof = DENS_NONE
             sps.append(zpic_species(s["m_q"], (ctypes.c_int32 * 2)(*s["ppc"]), s["n"], prof, s.get("x0", 0.0),
@@ -268,6 +271,13 @@ class Simulation:
         opt.profile = int(profile)
         opt.current_mode = int(current_mode)
         opt.no_graphs = 0 if graphs else 1
+        if inject and "laser" in cfg:     # the laser initial fields (R17) on the device
+            las = cfg["laser"]
+            if las.get("polarization", "y") != "y":
+                raise ValueError("only a y-polarised laser is implemented (R17)")
+            opt.laser = 1
+            opt.laser_a0, opt.laser_omega0, opt.laser_fwhm = las["a0"], las["omega0"], las["fwhm"]
+            opt.laser_W0, opt.laser_start = las["W0"], las["start"]
         self._keep = []
         if torch_plumbing:
             import torch

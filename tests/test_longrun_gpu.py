@@ -19,14 +19,7 @@ def _z():
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
 def test_full_length_run(name):
     cfg = synth.config(name)
-    sim = _z().Simulation(cfg, inject=True)
-    for s, sp in enumerate(cfg["species"]):
-        if sp.get("profile") == "ramp":
-            sim.set_particles(s, synth.species_particles(cfg, s))
-    if "laser" in cfg:
-        E, B = synth.laser_fields(cfg)
-        sim.set_fields(0, E)
-        sim.set_fields(1, B)
+    sim = _z().Simulation(cfg, inject=True)   # device init: lattices, C4's ramp and laser
     n0 = sim.counters()["particles"]
     sim.step(1)
     _, fe0, ke0 = sim.energy()

@@ -448,3 +448,25 @@ def test_get_charge_diagnostic(name):
     r = continuity_residual(cfg["nx"], cfg["ny"], cfg["dx"], cfg["dy"], cfg["dt"], rho0, rho1, g.fields(3), cfg["bc"])
     assert r <= CONT_TOL, r
     g.close()
+
+
+@pytest.mark.parametrize("name", ["C4", "P-LWFA"])
+def test_device_ramp_and_laser_match_generator(name):
+    """zpic_init builds the density ramp (ZPIC_DENS_RAMP, R16) and the laser fields
+    (zpic_options.laser, R17) on the device, in the library's own arithmetic; they agree with
+    synth's generator: particles bit-exact (cold plasma: u = 0), E and B within 1 fp32 ulp."""
+    cfg = synth.config(name, nx=300, ny=48)
+    cfg["species"][0].update(x0=2.0, x1=2.0 + 20 * cfg["dx"])
+    cfg["laser"] = dict(cfg["laser"], start=cfg["nx"] * cfg["dx"] - 2.0)
+    sim = _z().Simulation(cfg, inject=True, track_ids=True)
+    g = sim.particles(0, True)
+    h = synth.species_particles(cfg, 0)
+    o = np.argsort(g["id"])
+    g = {k: v[o] for k, v in g.items()}
+    assert np.array_equal(g["id"], h["id"])
+    for k in ("ix", "iy", "x", "y", "ux", "uy", "uz"):
+        assert np.array_equal(g[k], h[k]), k
+    E, B = synth.laser_fields(cfg)
+    for got, want in ((sim.fields(0), E), (sim.fields(1), B)):
+        assert np.all(np.abs(got - want) <= np.spacing(np.abs(want)) + 1e-30)
+    sim.close()
