@@ -14,7 +14,7 @@
 #include "zpic_internal.h"
 
 namespace zpic {
-void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st);
+void launch_push_tiles(const PushParams& p, int tile_begin, int tile_end, cudaStream_t st);
 void launch_insert(const PushParams& p, int grid, cudaStream_t st);
 void launch_mail_gather(const PushParams& p, cudaStream_t st);
 void launch_charge(const PushParams& p, float* rho, int wrap_y, cudaStream_t st);
@@ -29,7 +29,8 @@ void launch_loose(const PushParams& p, int grid, cudaStream_t st);
 void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st);
 void launch_guard_x(float* F, const GridDesc& g, int mode, int keep, cudaStream_t st);
 void launch_guard_y(float* F, const GridDesc& g, int mode, int keep, cudaStream_t st);
-void launch_yee(const YeeParams& p, cudaStream_t st);
+void launch_yee(const YeeParams& p, cudaStream_t st, int row_begin = 0, int row_end = -1);
+int yee_tile_rows(const GridDesc& g);
 void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4, int* mc,
                      int* sic, int* soc, int* stats, cudaStream_t st);
 void launch_inject(const InjectParams& q, int ntiles, cudaStream_t st);
@@ -284,26 +285,26 @@ PushParams push_params(zpic_ctx* c) {
 float* jrow(zpic_ctx* c, int comp, int row) { return c->J + comp * c->g.plane + (long)(row + 1) * c->g.pitch; }
 float* frow(float* F, const GridDesc& g, int comp, int row) { return F + comp * g.plane + (long)(row + 1) * g.pitch; }
 
-ncclResult_t nccl_exchange_round1(zpic_ctx* c) {
+ncclResult_t nccl_exchange_round1(zpic_ctx* c, cudaStream_t st) {
   ncclComm_t comm = (ncclComm_t)c->comm;
   const size_t rows2 = 2 * (size_t)c->g.pitch;
   const size_t mb = particle_msg_bytes(c->pcap);
   ncclResult_t r = ncclGroupStart();
   if (c->has_hi) {   // up: my raw J rows ny, ny+1 and my up-going particles
-    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(jrow(c, k, c->g.ny), rows2, ncclFloat, c->upper, comm, c->stream);
-    if (r == ncclSuccess) r = ncclSend(c->pmsg_send[1], mb, ncclChar, c->upper, comm, c->stream);
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(jrow(c, k, c->g.ny), rows2, ncclFloat, c->upper, comm, st);
+    if (r == ncclSuccess) r = ncclSend(c->pmsg_send[1], mb, ncclChar, c->upper, comm, st);
   }
   if (c->has_lo && r == ncclSuccess) {   // from below: the lower's rows ny, ny+1 and its up-going particles
-    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(c->jrdn + k * rows2, rows2, ncclFloat, c->lower, comm, c->stream);
-    if (r == ncclSuccess) r = ncclRecv(c->pmsg_recv[0], mb, ncclChar, c->lower, comm, c->stream);
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(c->jrdn + k * rows2, rows2, ncclFloat, c->lower, comm, st);
+    if (r == ncclSuccess) r = ncclRecv(c->pmsg_recv[0], mb, ncclChar, c->lower, comm, st);
   }
   if (c->has_lo && r == ncclSuccess) {   // down: my raw J rows -1, 0 and my down-going particles
-    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(jrow(c, k, -1), rows2, ncclFloat, c->lower, comm, c->stream);
-    if (r == ncclSuccess) r = ncclSend(c->pmsg_send[0], mb, ncclChar, c->lower, comm, c->stream);
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(jrow(c, k, -1), rows2, ncclFloat, c->lower, comm, st);
+    if (r == ncclSuccess) r = ncclSend(c->pmsg_send[0], mb, ncclChar, c->lower, comm, st);
   }
   if (c->has_hi && r == ncclSuccess) {   // from above: the upper's rows -1, 0 and its down-going particles
-    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(c->jrup + k * rows2, rows2, ncclFloat, c->upper, comm, c->stream);
-    if (r == ncclSuccess) r = ncclRecv(c->pmsg_recv[1], mb, ncclChar, c->upper, comm, c->stream);
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(c->jrup + k * rows2, rows2, ncclFloat, c->upper, comm, st);
+    if (r == ncclSuccess) r = ncclRecv(c->pmsg_recv[1], mb, ncclChar, c->upper, comm, st);
   }
   ncclResult_t e = ncclGroupEnd();
   return r != ncclSuccess ? r : e;
@@ -311,20 +312,20 @@ ncclResult_t nccl_exchange_round1(zpic_ctx* c) {
 
 // Round 2: E, B ghost rows of buffer `b`: my row ny-1 -> the upper's guard row -1 (up); my rows
 // 0, 1 -> the lower's guard rows ny, ny+1 (down).
-ncclResult_t nccl_exchange_round2(zpic_ctx* c, int b) {
+ncclResult_t nccl_exchange_round2(zpic_ctx* c, int b, cudaStream_t st) {
   ncclComm_t comm = (ncclComm_t)c->comm;
   const GridDesc& g = c->g;
   const size_t row = g.pitch;
   float* F[2] = {c->E[b], c->B[b]};
   ncclResult_t r = ncclGroupStart();
   for (int f = 0; f < 2 && c->has_hi && r == ncclSuccess; ++f)
-    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(frow(F[f], g, k, g.ny - 1), row, ncclFloat, c->upper, comm, c->stream);
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(frow(F[f], g, k, g.ny - 1), row, ncclFloat, c->upper, comm, st);
   for (int f = 0; f < 2 && c->has_lo && r == ncclSuccess; ++f)
-    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(frow(F[f], g, k, -1), row, ncclFloat, c->lower, comm, c->stream);
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(frow(F[f], g, k, -1), row, ncclFloat, c->lower, comm, st);
   for (int f = 0; f < 2 && c->has_lo && r == ncclSuccess; ++f)
-    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(frow(F[f], g, k, 0), 2 * row, ncclFloat, c->lower, comm, c->stream);
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclSend(frow(F[f], g, k, 0), 2 * row, ncclFloat, c->lower, comm, st);
   for (int f = 0; f < 2 && c->has_hi && r == ncclSuccess; ++f)
-    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(frow(F[f], g, k, g.ny), 2 * row, ncclFloat, c->upper, comm, c->stream);
+    for (int k = 0; k < 3 && r == ncclSuccess; ++k) r = ncclRecv(frow(F[f], g, k, g.ny), 2 * row, ncclFloat, c->upper, comm, st);
   ncclResult_t e = ncclGroupEnd();
   return r != ncclSuccess ? r : e;
 }
@@ -640,6 +641,8 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
           c->comm = comm;
           c->own_comm = true;
         }
+        CUDA_OR_THROW(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+        for (auto& e : c->ev) CUDA_OR_THROW(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       }
     }
     CUDA_OR_THROW(cudaGetLastError());
@@ -873,7 +876,16 @@ struct StepState {
   PushParams p;
   int shift;
   int launches;
+  bool r1_async;   // exchange round 1 runs on the comm stream while interior Yee tiles run
 };
+
+// Overlap of the NCCL halo rounds with interior work (SURVEY.md §8(e) "Overlap"): round 2 (E/B
+// ghost rows) with the next step's K1 on tile rows 1 .. nty-2 (they read no ghost row); round 1
+// (raw J rows + particles) with the Yee tile rows whose J rows avoid 0, 1, ny-1, ny (the rows
+// the halo changes).  Round 1 stays in order when a filter needs every J row first.
+bool overlap_round1(const zpic_ctx* c) {
+  return c->slab && c->transport == ZPIC_TRANSPORT_NCCL && c->comm_stream && c->opt.filter_passes == 0;
+}
 
 StepState step_phase_a(zpic_ctx* c) {
   StepState s{};
@@ -888,7 +900,21 @@ StepState step_phase_a(zpic_ctx* c) {
     ProfScope ps(c, K_ASSEMBLE);
     CUDA_OR_THROW(cudaMemsetAsync(c->J, 0, (size_t)3 * c->g.plane * sizeof(float), c->stream));
   }
-  { ProfScope ps(c, K_PUSH); launch_push_tiles(p, c->ntiles, c->stream); ++s.launches; }
+  {
+    ProfScope ps(c, K_PUSH);
+    if (c->r2_pending) {   // the E/B ghost rows of this step are still in flight
+      const int tb = c->ntx, te = std::max(c->ntx, (c->nty - 1) * c->ntx);
+      launch_push_tiles(p, tb, te, c->stream);
+      CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
+      c->r2_pending = false;
+      launch_push_tiles(p, 0, std::min(tb, c->ntiles), c->stream);
+      launch_push_tiles(p, std::max(te, tb), c->ntiles, c->stream);
+      s.launches += 3;
+    } else {
+      launch_push_tiles(p, 0, c->ntiles, c->stream);
+      ++s.launches;
+    }
+  }
   if (p.use_mail) { ProfScope ps(c, K_MAIL); launch_mail_gather(p, c->stream); ++s.launches; }
   { ProfScope ps(c, K_INSERT); launch_insert(p, grid_small, c->stream); ++s.launches; }
   if (!p.commutative) {
@@ -910,6 +936,33 @@ StepState step_phase_a(zpic_ctx* c) {
 }
 
 void step_phase_b(zpic_ctx* c, StepState& s) {
+  YeeParams y{};
+  y.g = c->g;
+  y.E0 = c->E[c->cur]; y.B0 = c->B[c->cur]; y.J = c->J;
+  y.E1 = c->E[c->cur ^ 1]; y.B1 = c->B[c->cur ^ 1];
+  y.dt = (float)c->dt;
+  y.dtdx = (float)(c->dt / c->dx); y.dtdy = (float)(c->dt / c->dy);
+  y.hdx = (float)(0.5 * c->dt / c->dx); y.hdy = (float)(0.5 * c->dt / c->dy);
+  y.murx = (float)((c->dt - c->dx) / (c->dt + c->dx));
+  y.mury = (float)((c->dt - c->dy) / (c->dt + c->dy));
+  y.bcx = c->bcx; y.bcy = c->bcy;
+  y.shift = s.shift;
+  y.y_images = !c->slab && c->bcy == ZPIC_BC_PERIODIC;
+  y.ylo_edge = !c->slab || !c->has_lo;
+  y.yhi_edge = !c->slab || !c->has_hi;
+  y.fe_slots = c->fe_slots;
+  y.fe_scale = 0.5 * c->dx * c->dy;
+  int yee_done_to = 0;   // tile rows [1, yee_done_to) already advanced (round 1 overlap)
+  if (s.r1_async) {
+    const int hi = (c->g.ny - 2) / 32;   // rows r < hi: J rows [32 r, 32 r + 32] avoid ny - 1, ny
+    if (hi > 1) {
+      ProfScope ps(c, K_YEE);
+      launch_yee(y, c->stream, 1, hi);
+      ++s.launches;
+      yee_done_to = hi;
+    }
+    CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[1], 0));
+  }
   if (c->slab) {
     ProfScope ps(c, K_HALO);
     launch_apply_j_halo(c->J, c->g, c->jrup, c->jrdn, c->has_lo, c->has_hi, c->stream);
@@ -933,24 +986,15 @@ void step_phase_b(zpic_ctx* c, StepState& s) {
   }
   {
     ProfScope ps(c, K_YEE);
-      YeeParams y{};
-      y.g = c->g;
-      y.E0 = c->E[c->cur]; y.B0 = c->B[c->cur]; y.J = Jyee;
-      y.E1 = c->E[c->cur ^ 1]; y.B1 = c->B[c->cur ^ 1];
-      y.dt = (float)c->dt;
-      y.dtdx = (float)(c->dt / c->dx); y.dtdy = (float)(c->dt / c->dy);
-      y.hdx = (float)(0.5 * c->dt / c->dx); y.hdy = (float)(0.5 * c->dt / c->dy);
-      y.murx = (float)((c->dt - c->dx) / (c->dt + c->dx));
-      y.mury = (float)((c->dt - c->dy) / (c->dt + c->dy));
-      y.bcx = c->bcx; y.bcy = c->bcy;
-      y.shift = s.shift;
-      y.y_images = !c->slab && c->bcy == ZPIC_BC_PERIODIC;
-      y.ylo_edge = !c->slab || !c->has_lo;
-      y.yhi_edge = !c->slab || !c->has_hi;
-      y.fe_slots = c->fe_slots;
-      y.fe_scale = 0.5 * c->dx * c->dy;
+    y.J = Jyee;
+    if (yee_done_to > 1) {
+      launch_yee(y, c->stream, 0, 1);
+      launch_yee(y, c->stream, yee_done_to, -1);
+      s.launches += 2;
+    } else {
       launch_yee(y, c->stream);
       ++s.launches;
+    }
   }
 }
 
@@ -1054,7 +1098,7 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
   }
   try {
     if (c->slab && c->halo_dirty) {
-      ncclResult_t r = nccl_exchange_round2(c, c->cur);
+      ncclResult_t r = nccl_exchange_round2(c, c->cur, c->stream);
       if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL halo: ") + ncclGetErrorString(r)};
       c->halo_dirty = false;
     }
@@ -1062,17 +1106,39 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
       maybe_repack(c);
       StepState s = step_phase_a(c);
       if (c->slab) {
-        ProfScope ps(c, K_EXCHANGE);
-        ncclResult_t r = nccl_exchange_round1(c);
+        ncclResult_t r;
+        if (overlap_round1(c)) {   // round 1 on the comm stream, interior Yee rows meanwhile
+          CUDA_OR_THROW(cudaEventRecord(c->ev[0], c->stream));
+          CUDA_OR_THROW(cudaStreamWaitEvent(c->comm_stream, c->ev[0], 0));
+          r = nccl_exchange_round1(c, c->comm_stream);
+          CUDA_OR_THROW(cudaEventRecord(c->ev[1], c->comm_stream));
+          s.r1_async = true;
+        } else {
+          ProfScope ps(c, K_EXCHANGE);
+          r = nccl_exchange_round1(c, c->stream);
+        }
         if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 1: ") + ncclGetErrorString(r)};
       }
       step_phase_b(c, s);
       if (c->slab) {
-        ProfScope ps(c, K_EXCHANGE);
-        ncclResult_t r = nccl_exchange_round2(c, c->cur ^ 1);
+        ncclResult_t r;
+        if (c->comm_stream) {   // round 2 on the comm stream, the next step's interior K1 meanwhile
+          CUDA_OR_THROW(cudaEventRecord(c->ev[2], c->stream));
+          CUDA_OR_THROW(cudaStreamWaitEvent(c->comm_stream, c->ev[2], 0));
+          r = nccl_exchange_round2(c, c->cur ^ 1, c->comm_stream);
+          CUDA_OR_THROW(cudaEventRecord(c->ev[3], c->comm_stream));
+          c->r2_pending = true;
+        } else {
+          ProfScope ps(c, K_EXCHANGE);
+          r = nccl_exchange_round2(c, c->cur ^ 1, c->stream);
+        }
         if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 2: ") + ncclGetErrorString(r)};
       }
       step_phase_c(c, s);
+    }
+    if (c->r2_pending) {   // the caller's stream sees complete ghost rows after zpic_step
+      CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
+      c->r2_pending = false;
     }
   } catch (const Fail& f) {
     c->last_error = f.msg;
@@ -1314,7 +1380,11 @@ void zpic_free(zpic_ctx* c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   drop_graphs(c);
+  if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
   if (c->own_comm && c->comm) ncclCommDestroy((ncclComm_t)c->comm);
+  for (auto e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   for (void* p : c->allocations) {
     if (c->opt.free) c->opt.free(p, c->opt.alloc_user);

@@ -101,6 +101,7 @@ struct PushParams {
   int use_mail;         // 1: tile leavers go through the per-tile mailboxes (K3m), else the mover list
   MailBox mail[kMaxSpecies];
   int fx_smin;          // a tile uses the one-word int32 current when its scale exponent S >= fx_smin
+  int tile0;            // K1 launches over tiles [tile0, tile0 + grid) (the slab overlap splits it)
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
   int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
 };
@@ -117,6 +118,7 @@ struct YeeParams {
   int ylo_edge, yhi_edge;           // the slab's low / high y boundary is a domain edge
   double* fe_slots;
   double fe_scale;  // dx dy / 2
+  int row0;         // first 32-row tile row of this launch (the slab overlap splits the grid)
 };
 
 struct InjectParams {
@@ -178,6 +180,9 @@ struct zpic_ctx {
   int rank, world, lower, upper, has_lo, has_hi;
   int transport;
   void* comm;        // ncclComm_t
+  cudaStream_t comm_stream = nullptr;   // NCCL halo rounds, overlapped with interior kernels
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // phase-A end, round 1, Yee end, round 2
+  bool r2_pending = false;              // round 2 of the last step is in flight on comm_stream
   bool own_comm;
   float* jrup;       // [3][2][pitch]: the upper neighbour's raw J rows -1, 0
   float* jrdn;       // [3][2][pitch]: the lower neighbour's raw J rows ny, ny+1

@@ -318,7 +318,7 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   __shared__ float sJ[3][WJ * WJ];
   __shared__ float s_mur[4][2][2][T + 1];  // E^n on Mur node lines: [edge][component][b, b'][index]
   const GridDesc& g = p.g;
-  const int i0 = blockIdx.x * T, j0 = blockIdx.y * T;
+  const int i0 = blockIdx.x * T, j0 = (blockIdx.y + p.row0) * T;
   const int tw = min(T, g.nx - i0), th = min(T, g.ny - j0);
   const long pl = g.plane;
   // y edges of this slab that are domain edges (with a slab decomposition the others are
@@ -535,7 +535,8 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
 #undef EI
 #undef BI
 #undef JI
-  block_add_double((double)fe * p.fe_scale, p.fe_slots + ((blockIdx.y * gridDim.x + blockIdx.x) & (kEnergySlots - 1)));
+  block_add_double((double)fe * p.fe_scale,
+                   p.fe_slots + (((blockIdx.y + p.row0) * gridDim.x + blockIdx.x) & (kEnergySlots - 1)));
 }
 
 // =============================================================================================
@@ -917,10 +918,17 @@ void launch_guard_y(float* F, const GridDesc& g, int mode, int keep, cudaStream_
   const int n = 3 * (g.nx + 3);
   k_guard_y<<<(n + 255) / 256, 256, 0, st>>>(F, g, mode, keep);
 }
-void launch_yee(const YeeParams& p, cudaStream_t st) {
-  dim3 grid((p.g.nx + kYeeT - 1) / kYeeT, (p.g.ny + kYeeT - 1) / kYeeT);
-  k_yee<<<grid, kBlock, 0, st>>>(p);
+// K5 over tile rows [row_begin, row_end) (row_end < 0: to the last)
+void launch_yee(const YeeParams& p, cudaStream_t st, int row_begin, int row_end) {
+  const int nty = (p.g.ny + kYeeT - 1) / kYeeT;
+  if (row_end < 0 || row_end > nty) row_end = nty;
+  if (row_end <= row_begin) return;
+  YeeParams q = p;
+  q.row0 = row_begin;
+  dim3 grid((p.g.nx + kYeeT - 1) / kYeeT, row_end - row_begin);
+  k_yee<<<grid, kBlock, 0, st>>>(q);
 }
+int yee_tile_rows(const GridDesc& g) { return (g.ny + kYeeT - 1) / kYeeT; }
 void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4,
                      int* mc, int* sic, int* soc, int* stats, cudaStream_t st) {
   k_epilogue<<<1, kBlock, 0, st>>>(ke_slots, fe_slots, energy, nspecies, ke_scale4, mc, sic, soc, stats);

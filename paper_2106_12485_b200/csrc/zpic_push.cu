@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
   __shared__ double s_ke[kMaxSpecies];
   if (threadIdx.x < kMaxSpecies) s_ke[threadIdx.x] = 0.0;
 
-  const int t = blockIdx.x;
+  const int t = blockIdx.x + p.tile0;
   const int tx = t % p.ntx, ty = t / p.ntx;
   const int i0 = tx * T, j0 = ty * T;
   const int tw = min(T, p.g.nx - i0), th = min(T, p.g.ny - j0);
@@ -369,7 +369,11 @@ static int k1_shape() {
   return v;
 }
 
-void launch_push_tiles(const PushParams& p, int ntiles, cudaStream_t st) {
+void launch_push_tiles(const PushParams& p_in, int tile_begin, int tile_end, cudaStream_t st) {
+  if (tile_end <= tile_begin) return;
+  PushParams p = p_in;
+  p.tile0 = tile_begin;
+  const int ntiles = tile_end - tile_begin;
   switch (p.T) {
     case 8: launch_push_T<8, 128, 8>(p, ntiles, st); break;
     case 16:

@@ -124,3 +124,38 @@ def test_nccl_transport_self_ring():
     assert abs(ring.energy()[1] - ref.energy()[1]) <= 1e-6 * max(abs(ref.energy()[1]), 1e-12)
     ring.close()
     ref.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_nccl_overlapped_rounds_self_ring(name):
+    """The NCCL path overlaps round 1 (raw J rows + particles) with the Yee tile rows that need
+    no halo and round 2 (E/B ghost rows) with the next step's K1 on interior tile rows, on a
+    separate stream.  With a one-rank ring and 12 steps in one zpic_step call (every overlap in
+    play: 10 K1 tile rows, 4 Yee tile rows), the result equals the unsplit domain."""
+    z = _z()
+    if name == "C1":
+        cfg = synth.config("C1", nx=64, ny=160)
+        cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
+    else:
+        cfg = synth.config("C3", nx=96, ny=160)
+        cfg["species"][0].update(x0=0.0, x1=4.8)
+        cfg["species"][1].update(x0=4.8, x1=9.6)
+    parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
+    ref = z.Simulation(cfg, inject=False, track_ids=True, graphs=False)
+    uid = z.zpic.zpic_nccl_unique_id()
+    ring = z.Simulation(cfg, inject=False, track_ids=True,
+                        dist={"rank": 0, "world": 1, "transport": "nccl", "nccl_id": uid})
+    for s, p in enumerate(parts):
+        ref.set_particles(s, p)
+        ring.set_particles(s, p)
+    ref.step(12)
+    ring.step(12)
+    for w in (0, 1, 2):
+        assert rel_l2(ring.fields(w), ref.fields(w)) < 2e-5, w
+    for s in range(len(parts)):
+        c = compare_particles(ring.particles(s, True), ref.particles(s, True), cfg["nx"], cfg["ny"],
+                              (cfg["bc"][0] == 0, True))
+        assert c["pos_max"] < 1e-4 and c["cell_exact_frac"] >= CELL_FRAC, c
+    assert abs(ring.energy()[1] - ref.energy()[1]) <= 1e-6 * max(abs(ref.energy()[1]), 1e-12)
+    ring.close()
+    ref.close()
