@@ -470,3 +470,24 @@ def test_device_ramp_and_laser_match_generator(name):
     for got, want in ((sim.fields(0), E), (sim.fields(1), B)):
         assert np.all(np.abs(got - want) <= np.spacing(np.abs(want)) + 1e-30)
     sim.close()
+
+
+@pytest.mark.parametrize("shape", [(2, 2), (3, 5), (5, 3)])
+def test_degenerate_tiny_grids(shape):
+    """Grids smaller than a tile and than the 2-cell guard reach of the stencils (periodic images
+    of a guard land on other guards or on the cell itself): same bars as C1 over 10 steps."""
+    nx, ny = shape
+    cfg = synth.config("C1", nx=nx, ny=ny)
+    cfg["species"][0]["uth"] = (0.2, 0.2, 0.2)
+    _parity_run(cfg, 10, check_every_step=False)
+
+
+@pytest.mark.parametrize("shape", [(1, 4), (4, 1), (40000, 8)])
+def test_invalid_grids_rejected(shape):
+    """A grid one cell wide (a periodic image of the guard layer would be the cell itself twice)
+    or beyond the 16-bit packed cell index is rejected at zpic_init with ZPIC_E_INVALID."""
+    nx, ny = shape
+    cfg = synth.config("C1", nx=nx, ny=ny)
+    with pytest.raises(_z().ZpicError) as e:
+        _z().Simulation(cfg, inject=True)
+    assert e.value.status == -1
