@@ -120,7 +120,8 @@ typedef struct {
                                  polarised along y, travelling along +x, E_y = a0 w0 env(x)
                                  exp(-(y - Ly/2)^2 / W0^2) cos(w0 (x - xc)), B_z = E_y at B_z's points;
                                  env = sin^2 rise and fall of length fwhm each ending at x = start,
-                                 xc = start - fwhm (no divergence cleaning) */
+                                 xc = start - fwhm (no divergence cleaning); ZPIC_E_LASER if fwhm or
+                                 W0 <= 0 or the pulse misses the box */
   double laser_a0, laser_omega0, laser_fwhm, laser_W0, laser_start;
   int32_t no_graphs;          /* 0 (default): zpic_step replays a captured CUDA graph of two steps
                                  when it can (single domain, no moving window, profile = 0), which

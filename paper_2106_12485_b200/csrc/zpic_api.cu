@@ -32,7 +32,7 @@ void launch_guard_y(float* F, const GridDesc& g, int mode, int keep, cudaStream_
 void launch_yee(const YeeParams& p, cudaStream_t st, int row_begin = 0, int row_end = -1);
 int yee_tile_rows(const GridDesc& g);
 void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4, int* mc,
-                     int* sic, int* soc, int* stats, cudaStream_t st);
+                     int* sic, int* soc, int* stats, int64_t* d_nmove, int shifted, cudaStream_t st);
 void launch_inject(const InjectParams& q, int ntiles, cudaStream_t st);
 void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
                 const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err, const PList& loose, int s,
@@ -41,7 +41,7 @@ void launch_export(const PStore& ps, int ntiles, const int64_t* prefix, int y0, 
                    float* y, float* ux, float* uy, float* uz, uint32_t* id, cudaStream_t st);
 void launch_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
                   const float* y, int* counts, int* err, cudaStream_t st);
-void launch_inject_column(const PushParams& p, int s, int px, int py, int n_move, int ny_global, int y0, uint64_t key,
+void launch_inject_column(const PushParams& p, int s, int px, int py, const int64_t* n_move, int ny_global, int y0, uint64_t key,
                           const double* ufl, const double* uth, cudaStream_t st);
 void launch_filter_x(const float* Jin, float* Jout, const GridDesc& g, int npass, int compensated, int periodic,
                      cudaStream_t st);
@@ -566,6 +566,7 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       }
     }
     c->population = total;
+    c->d_nmove = alloc_n<int64_t>(c, 1);
     const int mcap = mover_capacity(c, total);
     c->movers = alloc_list(c, (int)mcap);
     c->spill[0] = alloc_list(c, (int)mcap);
@@ -609,8 +610,8 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       const LaserParams L{c->opt.laser_a0, c->opt.laser_omega0, c->opt.laser_fwhm, c->opt.laser_W0, c->opt.laser_start,
                           0.5 * grid->ny * grid->dy};
       if (!(L.fwhm > 0) || !(L.W0 > 0)) throw Fail{ZPIC_E_LASER, "laser: fwhm and W0 must be > 0"};
-      if (L.start - 2.0 * L.fwhm < 0.0 || L.start > grid->nx * grid->dx)
-        throw Fail{ZPIC_E_LASER, "laser: the pulse [start - 2 fwhm, start] must lie inside the box"};
+      if (L.start <= 0.0 || L.start - 2.0 * L.fwhm >= grid->nx * grid->dx)
+        throw Fail{ZPIC_E_LASER, "laser: the pulse [start - 2 fwhm, start] misses the box"};
       launch_laser(c->E[0], c->B[0], g, c->y0, grid->dx, grid->dy, L, c->stream);
       CUDA_OR_THROW(cudaGetLastError());
       refresh_field_guards(c, c->E[0], true);
@@ -1005,7 +1006,7 @@ void step_phase_c(zpic_ctx* c, StepState& s) {
       const zpic_species& sp = c->species[q];
       if (!(sp.n > 0)) continue;
       const uint64_t key = host_mix64(host_mix64(c->seed) + (uint64_t)q);
-      launch_inject_column(s.p, q, sp.ppc[0], sp.ppc[1], (int)c->n_move, c->ny_global, c->y0, key, sp.ufl, sp.uth,
+      launch_inject_column(s.p, q, sp.ppc[0], sp.ppc[1], c->d_nmove, c->ny_global, c->y0, key, sp.ufl, sp.uth,
                            c->stream);
       ++s.launches;
     }
@@ -1014,7 +1015,7 @@ void step_phase_c(zpic_ctx* c, StepState& s) {
   {
     ProfScope ps(c, K_EPI);
     launch_epilogue(c->ke_slots, c->fe_slots, c->energy, c->nspecies, c->energy + 1 + kMaxSpecies, c->movers.count,
-                    s.p.spill_in.count, s.p.spill_out.count, c->stats, c->stream);
+                    s.p.spill_in.count, s.p.spill_out.count, c->stats, c->d_nmove, s.shift, c->stream);
     ++s.launches;
     if (c->slab) {
       for (int d = 0; d < 2; ++d) CUDA_OR_THROW(cudaMemsetAsync(c->pmsg_send[d], 0, 4, c->stream));
@@ -1037,18 +1038,49 @@ zpic_status step_error(zpic_ctx* c) {
 // state only through the E/B buffer index and the loose-list parity, which both flip every step:
 // a two-step graph replayed from the same parity repeats exactly.  A graph bakes in the buffer
 // pointers, so anything that reallocates (zpic_set_particles) drops the graphs.
-static bool graphs_eligible(const zpic_ctx* c) {
-  return !c->opt.no_graphs && !c->prof && !c->slab && c->bcx != ZPIC_BC_MOVING_WINDOW;
-}
+static bool graphs_eligible(const zpic_ctx* c) { return !c->opt.no_graphs && !c->prof && !c->slab; }
 static void drop_graphs(zpic_ctx* c) {
   for (auto& g : c->graph)
     if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+  for (auto& row : c->graph1)
+    for (auto& g : row)
+      if (g) { cudaGraphExecDestroy(g); g = nullptr; }
+}
+// With a moving window the launches of a step also depend on whether the window shifts at its
+// end (a host decision, step_phase_a): one-step graphs keyed by (step parity, shift).  The column
+// injection reads n_move from the device, so the graphs stay valid as the window advances.
+static bool window_shifts(const zpic_ctx* c) {
+  return c->bcx == ZPIC_BC_MOVING_WINDOW && (double)(c->steps + 1) * c->dt > c->dx * (double)(c->n_move + 1);
 }
 static void run_step(zpic_ctx* c) {
   StepState s = step_phase_a(c);
   step_phase_b(c, s);
   step_phase_c(c, s);
 }
+static cudaGraphExec_t one_step_graph(zpic_ctx* c, int shift) {
+  const int par = (int)(c->steps & 1);
+  cudaGraphExec_t& ge = c->graph1[par][shift];
+  if (ge) return ge;
+  const int cur = c->cur, since = c->since_check;
+  const int64_t steps = c->steps, launches = c->launches, n_move = c->n_move;
+  cudaGraph_t g = nullptr;
+  CUDA_OR_THROW(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    run_step(c);
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    throw;
+  }
+  CUDA_OR_THROW(cudaStreamEndCapture(c->stream, &g));
+  c->graph1_launches[par][shift] = (int)(c->launches - launches);
+  c->cur = cur; c->steps = steps; c->launches = launches; c->n_move = n_move; c->since_check = since;
+  const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) { ge = nullptr; throw Fail{ZPIC_E_CUDA, std::string("graph: ") + cudaGetErrorString(e)}; }
+  return ge;
+}
+
 static cudaGraphExec_t two_step_graph(zpic_ctx* c) {
   cudaGraphExec_t& ge = c->graph[c->steps & 1];
   if (ge) return ge;
@@ -1075,6 +1107,25 @@ static cudaGraphExec_t two_step_graph(zpic_ctx* c) {
 
 zpic_status zpic_step(zpic_ctx* c, int32_t n) {
   if (!c || n < 0) return ZPIC_E_INVALID;
+  if (graphs_eligible(c) && n >= 2 && c->bcx == ZPIC_BC_MOVING_WINDOW) {
+    try {
+      for (int k = 0; k < n; ++k) {
+        maybe_repack(c);
+        const int shift = window_shifts(c) ? 1 : 0;
+        const int par = c->steps & 1;
+        CUDA_OR_THROW(cudaGraphLaunch(one_step_graph(c, shift), c->stream));
+        c->cur ^= 1;
+        c->steps += 1;
+        c->since_check += 1;
+        c->launches += c->graph1_launches[par][shift];
+        if (shift) c->n_move += 1;
+      }
+    } catch (const Fail& f) {
+      c->last_error = f.msg;
+      return f.st;
+    }
+    return step_error(c);
+  }
   if (graphs_eligible(c) && n >= 2) {
     try {
       int k = 0;

@@ -195,6 +195,9 @@ struct zpic_ctx {
   // CUDA graphs of two steps, by step parity (the state a two-step replay returns to)
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
   int graph_launches = 0;  // kernels in one two-step graph
+  cudaGraphExec_t graph1[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // one step, [parity][shift]
+  int graph1_launches[2][2] = {{0, 0}, {0, 0}};
+  int64_t* d_nmove = nullptr;   // the window shift count on the device (column injection ids)
   // profiling
   bool prof;
   std::vector<std::string> prof_names;

@@ -542,7 +542,8 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
 // =============================================================================================
 // Epilogue (1 CTA): reduce the energy slots of the step just taken, reset per-step counters.
 __global__ void k_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4,
-                           int* movers_count, int* spill_in_count, int* spill_out_count, int* stats) {
+                           int* movers_count, int* spill_in_count, int* spill_out_count, int* stats,
+                           int64_t* d_nmove, int shifted) {
   __shared__ double red[kBlock];
   for (int q = 0; q <= nspecies; ++q) {
     double* slots = q == 0 ? fe_slots : ke_slots + (q - 1) * kEnergySlots;
@@ -562,6 +563,7 @@ __global__ void k_epilogue(double* ke_slots, double* fe_slots, double* energy, i
     *movers_count = 0;
     *spill_in_count = 0;
     stats[1] = *spill_out_count;
+    if (shifted) *d_nmove += 1;
   }
 }
 
@@ -618,8 +620,12 @@ __global__ void __launch_bounds__(kBlock) k_inject(InjectParams q) {
 // Moving window (R15): fresh plasma in the column entering the window, ix = nx-1:
 // the ppc sub-lattice at the species density, u = ufl + uth N with the counter-based generator,
 // ids 2^31 + (n_move ny + iy) ppc + l ppc_x + k.  Inserted straight into the tiles.
-__global__ void k_inject_column(PushParams p, int s, int px, int py, int n_move, int ny_global, int y0, uint64_t key,
-                                double ufl0, double ufl1, double ufl2, double uth0, double uth1, double uth2) {
+// n_move is read from the device counter (advanced by the epilogue of every shift step), so a
+// captured step graph injects the right column ids when it is replayed.
+__global__ void k_inject_column(PushParams p, int s, int px, int py, const int64_t* d_nmove, int ny_global, int y0,
+                                uint64_t key, double ufl0, double ufl1, double ufl2, double uth0, double uth1,
+                                double uth2) {
+  const int64_t n_move = *d_nmove;
   const int ppc = px * py;
   const int n = p.g.ny * ppc;
   for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
@@ -930,8 +936,9 @@ void launch_yee(const YeeParams& p, cudaStream_t st, int row_begin, int row_end)
 }
 int yee_tile_rows(const GridDesc& g) { return (g.ny + kYeeT - 1) / kYeeT; }
 void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4,
-                     int* mc, int* sic, int* soc, int* stats, cudaStream_t st) {
-  k_epilogue<<<1, kBlock, 0, st>>>(ke_slots, fe_slots, energy, nspecies, ke_scale4, mc, sic, soc, stats);
+                     int* mc, int* sic, int* soc, int* stats, int64_t* d_nmove, int shifted, cudaStream_t st) {
+  k_epilogue<<<1, kBlock, 0, st>>>(ke_slots, fe_slots, energy, nspecies, ke_scale4, mc, sic, soc, stats, d_nmove,
+                                   shifted);
 }
 void launch_inject(const InjectParams& q, int ntiles, cudaStream_t st) { k_inject<<<ntiles, kBlock, 0, st>>>(q); }
 void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
@@ -940,7 +947,7 @@ void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t*
   const int grid = (int)std::min<long>((n + kBlock - 1) / kBlock, 148L * 32);
   if (grid > 0) k_bin<<<grid, kBlock, 0, st>>>(ps, T, ntx, y0, n, ix, iy, x, y, ux, uy, uz, id, err, loose, s);
 }
-void launch_inject_column(const PushParams& p, int s, int px, int py, int n_move, int ny_global, int y0, uint64_t key,
+void launch_inject_column(const PushParams& p, int s, int px, int py, const int64_t* n_move, int ny_global, int y0, uint64_t key,
                           const double* ufl, const double* uth, cudaStream_t st) {
   const int n = p.g.ny * px * py;
   k_inject_column<<<(n + kBlock - 1) / kBlock, kBlock, 0, st>>>(p, s, px, py, n_move, ny_global, y0, key, ufl[0], ufl[1],

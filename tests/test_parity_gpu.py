@@ -491,3 +491,22 @@ def test_invalid_grids_rejected(shape):
     with pytest.raises(_z().ZpicError) as e:
         _z().Simulation(cfg, inject=True)
     assert e.value.status == -1
+
+
+def test_cuda_graph_replay_moving_window():
+    """With a moving window zpic_step replays one-step graphs keyed by (step parity, window
+    shift) and the column injection reads the shift count from the device: particles (by id),
+    fields and the injected ids match plain launches over 40 steps (38 shifts)."""
+    out = []
+    for graphs in (True, False):
+        cfg = c4_reduced(nx=200, ny=32)
+        sim = _z().Simulation(cfg, inject=True, track_ids=True, graphs=graphs)
+        sim.step(40)
+        p = sim.particles(0, True)
+        o = np.argsort(p["id"])
+        out.append(({k: v[o] for k, v in p.items()}, sim.fields(0), sim.fields(1)))
+        sim.close()
+    (pa, Ea, Ba), (pb, Eb, Bb) = out
+    for k in pa:
+        assert np.array_equal(pa[k], pb[k]), k
+    assert np.array_equal(Ea, Eb) and np.array_equal(Ba, Bb)
