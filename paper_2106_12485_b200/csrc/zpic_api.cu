@@ -117,7 +117,7 @@ void alloc_store(zpic_ctx* c, int s, int cap) {
   // mailboxes: an edge box holds half a tile column of the species' lattice, a corner box 32
   MailBox& M = c->mail[s];
   const int ppc = c->species[s].ppc[0] * c->species[s].ppc[1];
-  M.cap_edge = round_up(std::max(32, c->T * ppc / 2), 32);
+  M.cap_edge = round_up(std::max(32, std::min(c->T * ppc / 2, cap)), 32);
   M.cap_corner = 32;
   M.per_tile = 4 * M.cap_edge + 4 * M.cap_corner;
   M.stride = (long)c->ntiles * M.per_tile;
@@ -549,7 +549,14 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       int maxcount = c->T * c->T * ppc;
       if (sp.profile == ZPIC_DENS_NONE || sp.profile == ZPIC_DENS_RAMP || sp.n == 0.0) { col_lo = col_hi = 0; }
       // the device injector writes every lattice particle into its tile: no less than a full tile
-      const int cap = std::max(32, round_up((int)std::ceil(maxcount * std::max(1.0, c->opt.capacity_slack)), 32));
+      // (also for NONE, which zpic_set_particles then usually fills without reallocating); a ramp
+      // species is sized when it is loaded below
+      const bool later = sp.profile == ZPIC_DENS_RAMP;
+      const int cap = later ? 32
+                            : std::max(32, round_up((int)std::ceil(maxcount * (sp.profile == ZPIC_DENS_NONE
+                                                                                    ? c->opt.capacity_slack
+                                                                                    : std::max(1.0, c->opt.capacity_slack))),
+                                                    32));
       if ((double)cap * c->ntiles > 2.0e9) throw Fail{ZPIC_E_INVALID, "particle store exceeds 2^31 slots"};
       alloc_store(c, s, cap);
       check_tile_capacity(c);
@@ -690,9 +697,13 @@ static void load_species(zpic_ctx* c, int s, int64_t n, char* tmp, bool has_id) 
   const double slack = c->repacking ? std::max(1.1, c->opt.capacity_slack) : c->opt.capacity_slack;
   const int cap = std::max({32, round_up((int)std::ceil(maxc * slack), 32),
                             round_up((int)std::ceil(c->T * c->T * ppc * slack), 32)});
-  free_store(c, s);
-  alloc_store(c, s, cap);
-  check_tile_capacity(c);
+  if (cap > c->ps[s].cap || cap < c->ps[s].cap / 2 || c->repacking) {   // else keep the store
+    free_store(c, s);
+    alloc_store(c, s, cap);
+    check_tile_capacity(c);
+  } else {
+    CUDA_OR_THROW(cudaMemsetAsync(c->ps[s].cnt, 0, (size_t)c->ntiles * 4, c->stream));
+  }
   if (n > 0) {
     launch_bin(c->ps[s], c->T, c->ntx, c->y0, (long)n, dix, diy, dx_, dy_, dux, duy, duz, has_id ? did : nullptr, c->err,
                c->spill[c->steps & 1], s, c->stream);

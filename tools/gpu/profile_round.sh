@@ -3,7 +3,7 @@
 #  3. K1 DRAM bytes per launch at C5 (2 metrics, one pass);  4. ncu --set full of K1 at 2048^2.
 set -x
 TAG=${TAG:-pr}
-timeout 900 python bench.py > gpurun_out/${TAG}_bench.log 2>&1 || exit 1
+[ -f gpurun_out/${TAG}_bench.log ] || timeout 900 python bench.py > gpurun_out/${TAG}_bench.log 2>&1 || exit 1
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv \
   python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu > gpurun_out/${TAG}_launches_run.log 2>&1
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none \
