@@ -48,12 +48,13 @@ struct PStore {
 // tile's warp in K3m reads the 8 boxes addressed to it and appends them to its segment with
 // coalesced stores.  Boxes have fixed capacities (edges cap_edge, corners cap_corner); a
 // particle that finds its box full goes through the flat mover list instead.  Fields as in
-// PStore, field f of slot q at data[f * stride + q], q = t * per_tile + offset(d) + k.
+// PStore, one record per slot (nf consecutive words: a box is one contiguous run): field f of
+// slot q at data[q * nf + f], q = t * per_tile + offset(d) + k.
 struct MailBox {
   uint32_t* data;
   int32_t* cnt;    // [ntiles][8] entries of each box this step
   int cap_edge, cap_corner, per_tile;
-  long stride;     // ntiles * per_tile
+  long stride;     // ntiles * per_tile (slots)
   int nf;
 };
 

@@ -139,11 +139,11 @@ __global__ void __launch_bounds__(kBlock) k_mail_gather(PushParams p) {
     for (int q = 1; q < 8; ++q) {
       if (q == d) { nd = ns[q]; od = offs[q]; }
     }
-    const uint32_t* src = M.data + (long)nd * M.per_tile + mail_offset(M, d) + (e - od);
-    const uint32_t cell = src[F_CELL * M.stride];
-    const uint32_t x = src[F_X * M.stride], y = src[F_Y * M.stride];
-    const uint32_t ux = src[F_UX * M.stride], uy = src[F_UY * M.stride], uz = src[F_UZ * M.stride];
-    const uint32_t id = M.nf > F_ID ? src[F_ID * M.stride] : 0u;
+    const uint32_t* src = M.data + ((long)nd * M.per_tile + mail_offset(M, d) + (e - od)) * M.nf;
+    const uint32_t cell = src[F_CELL];
+    const uint32_t x = src[F_X], y = src[F_Y];
+    const uint32_t ux = src[F_UX], uy = src[F_UY], uz = src[F_UZ];
+    const uint32_t id = M.nf > F_ID ? src[F_ID] : 0u;
     const int slot = pos + e;
     if (slot < ps.cap) {
       uint32_t* q = ps.slot((long)t * ps.cap + slot);

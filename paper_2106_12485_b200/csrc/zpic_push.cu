@@ -229,12 +229,12 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
       const int m = warp_reserve(p.movers.count, glob);
       if (mslot >= 0) {
         const MailBox& M = p.mail[s];
-        uint32_t* q = M.data + (long)t * M.per_tile + mail_offset(M, mdir) + mslot;
-        q[F_CELL * M.stride] = (uint32_t)pack_cell(ix, iy);
-        q[F_X * M.stride] = __float_as_uint(x); q[F_Y * M.stride] = __float_as_uint(y);
-        q[F_UX * M.stride] = __float_as_uint(ux); q[F_UY * M.stride] = __float_as_uint(uy);
-        q[F_UZ * M.stride] = __float_as_uint(uz);
-        if (M.nf > F_ID) q[F_ID * M.stride] = id;
+        uint32_t* q = M.data + ((long)t * M.per_tile + mail_offset(M, mdir) + mslot) * M.nf;
+        q[F_CELL] = (uint32_t)pack_cell(ix, iy);
+        q[F_X] = __float_as_uint(x); q[F_Y] = __float_as_uint(y);
+        q[F_UX] = __float_as_uint(ux); q[F_UY] = __float_as_uint(uy);
+        q[F_UZ] = __float_as_uint(uz);
+        if (M.nf > F_ID) q[F_ID] = id;
       }
       if (glob) {
         if (m < p.movers.cap) list_put(p.movers, m, pack_cell(ix, iy), x, y, ux, uy, uz, id, s);
