@@ -3,9 +3,10 @@
 // One CTA per tile of T x T cells.  It stages the tile's E and B (+1 guard cell each side) in
 // shared memory, pushes every particle of every species of the tile — interpolation
 // (PAPER.md:144), relativistic Boris, charge-conserving deposit
-// — and accumulates the tile's current exactly in shared memory (fixed point,
-// native integer atomics).  Then it stores the (T+3)^2 current block for K4 and fixes up the
-// tile's particle segment.
+// — and accumulates the tile's current in shared memory as fixed point with
+// native integer atomics (one int32 per node at a per-tile scale, or the exact two-word form;
+// DESIGN.md §2).  Then it stores the (T+3)^2 current block for K4 (or adds it into J:
+// current_mode 1) and fixes up the tile's particle segment.
 //
 // Divergence control: every lane deposits the first straight piece of its path in lock-step;
 // a path that crosses a cell edge is queued (start point, displacement, z weight) in a per-warp
@@ -13,9 +14,10 @@
 // active: each lane recomputes the crossings with the same arithmetic and deposits the later
 // pieces.
 // Re-sort: particles that stay in the tile are written back in place; leavers leave a hole
-// (cell = -1) and go to the mover list (K3 inserts them into their new tile).  Once per tile
-// and species, the holes below the new count are filled from the tail — no block barrier per
-// chunk, and only O(#leavers) particle moves.
+// (cell = -1) and go to this tile's mailbox for their direction of travel (K3m appends them to
+// the destination tile), or to the flat mover list when the box is full or they leave the slab
+// (K3).  Once per tile and species, the holes below the new count are filled from the tail — no
+// block barrier per chunk, and only O(#leavers) particle moves.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
