@@ -1,12 +1,17 @@
 // zpic_kernels.cu — the sm_100a kernels of the B200 EM-PIC step.
 //   K1 k_push_tiles   fused gather + Boris + charge-conserving deposit + cell update + tile
 //                     compaction, one CTA per tile, fields and current in shared memory
-//   K3 k_insert       movers -> destination tile slack (or the loose list)
+//   K3m k_mail_gather per-tile mailboxes -> destination tile segments (one warp per tile)
+//   K3 k_insert       flat mover list (full boxes, slab exits) -> destination tile slack (or the loose list)
 //   K4 k_assemble_j   per-tile current blocks -> guard-extended J grid (plain stores, no atomics)
 //   K1L k_push_loose  the loose list: same physics, global-memory fields / current
 //   K4b k_guard_x/y   ghost-current reduction and guard refresh
 //   K5 k_yee          fused B half step, E step, B half step on a 32x32 tile
-//   K0 k_inject       counter-based lattice injection
+//   K0 k_inject       counter-based lattice injection; k_ramp_rows, k_laser:
+//                     the C4 density ramp (R16) and laser fields (R17) at zpic_init
+//   k_inject_column   moving-window injection (R15); k_filter_x the compensated filter (R12)
+//   k_apply_j_halo, k_recv_insert   y-slab halo rounds (§8(e))
+//   k_charge, k_export, k_count, k_bin, k_loose_extract   diagnostics, loading and re-packing
 //   k_epilogue        energies, counters
 #include <cuda_runtime.h>
 #include <stdint.h>
