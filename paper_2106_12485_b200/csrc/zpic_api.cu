@@ -2,6 +2,7 @@
 // sequence, exports, energies, profiling.  No compute happens on the host:
 // every stage of the step is one of the kernels in zpic_kernels.cu.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <nccl.h>
 
 #include <algorithm>
@@ -106,6 +107,29 @@ T* alloc_n(zpic_ctx* c, size_t n) {
 }
 
 int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+// A 3D TMA map of one guard-extended field buffer: dims (pitch, rows, 3 components) floats, box
+// (BX, T + 2, 3) with BX = T + 5 rounded up to 4 floats (the box starts at a 16-byte aligned column
+// 4 cells left of the tile: TMA faults on an unaligned start column), zero fill outside.
+// cuTensorMapEncodeTiled is taken from the driver through the runtime (no -lcuda).
+void make_field_tmap(CUtensorMap* map, float* F, const GridDesc& g, int T) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !encode)
+      throw Fail{ZPIC_E_CUDA, "cuTensorMapEncodeTiled is not available"};
+  }
+  const int W = T + 2, BX = (T + 5 + 3) & ~3;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.pitch, (cuuint64_t)g.rows, 3};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.plane * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)BX, (cuuint32_t)W, 3};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, F, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw Fail{ZPIC_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+}
 
 void alloc_store(zpic_ctx* c, int s, int cap) {
   PStore& ps = c->ps[s];
@@ -245,6 +269,8 @@ int fx_smin() {
 
 PushParams push_params(zpic_ctx* c) {
   PushParams p{};
+  p.tmE = c->tm[0][c->cur];
+  p.tmB = c->tm[1][c->cur];
   p.g = c->g;
   p.E = c->E[c->cur];
   p.B = c->B[c->cur];
@@ -518,6 +544,10 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     }
     // fields
     for (int b = 0; b < 2; ++b) { c->E[b] = alloc_n<float>(c, 3 * g.plane); c->B[b] = alloc_n<float>(c, 3 * g.plane); }
+    for (int b = 0; b < 2; ++b) {   // TMA maps for K1's staging of a tile's fields (+1 cell halo)
+      make_field_tmap(&c->tm[0][b], c->E[b], g, c->T);
+      make_field_tmap(&c->tm[1][b], c->B[b], g, c->T);
+    }
     c->J = alloc_n<float>(c, 3 * g.plane);
     c->Jf = c->opt.filter_passes > 0 ? alloc_n<float>(c, 3 * g.plane) : nullptr;
     if (c->opt.filter_passes < 0 || c->opt.filter_passes > 64) throw Fail{ZPIC_E_INVALID, "filter_passes must be in [0, 64]"};

@@ -1,6 +1,7 @@
 // zpic_internal.h — device data layout and kernel parameter blocks of the B200 EM-PIC path.
 // Not part of the ABI (include/zpic.h is).  Layouts are documented in DESIGN.md "Data layout".
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -75,8 +76,11 @@ struct SpeciesConst {
   double ke_scale;  // q m_q dx dy
 };
 
-// Everything the particle kernels need, passed by value.
+// Everything the particle kernels need, passed by value (K1 takes it as a __grid_constant__
+// parameter: the TMA descriptors are read from parameter space).
 struct PushParams {
+  CUtensorMap tmE, tmB;   // 3D TMA maps of the current E and B buffers: (pitch, rows, 3) floats,
+                          // box (T + 4 rounded to 4, T + 2, 3); zero fill outside (K1 staging)
   GridDesc g;
   const float* E;   // current E (3 planes)
   const float* B;
@@ -154,6 +158,7 @@ struct zpic_ctx {
   int T, ntx, nty, ntiles;
   cudaStream_t stream;
   bool own_stream;
+  CUtensorMap tm[2][2];   // [E / B][buffer] TMA maps for K1's field staging
   // device buffers
   float* E[2];
   float* B[2];

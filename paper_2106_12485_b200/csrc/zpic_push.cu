@@ -54,18 +54,41 @@ __device__ __forceinline__ void drain_path(const A& acc, const PathRing& Q, int 
   if (c.di && c.dj) deposit_seg(acc, s2, jxs, jys);
 }
 
+// Shared-memory layout of K1 (bytes): the current accumulators (128 B aligned), the per-warp path
+// rings, then the repacked fields.  Before the current is zeroed and the rings are used, the
+// accumulator + ring bytes receive the TMA boxes of E and B.  A box starts 4 cells left of the
+// tile (TMA needs a 16-byte aligned start column: interior column 0 sits at padded column 4) and
+// is T + 5 cells rounded up to 4 wide, W = T + 2 rows (local cells -1 .. T).
+template <int T>
+struct K1Smem {
+  static constexpr int W = T + 2, WJ = T + 3;
+  static constexpr int BX = (T + 5 + 3) & ~3;                  // TMA box row (16 B multiple)
+  static constexpr int BOX = 3 * W * BX * 4;                   // one field's box: 3 components
+  static constexpr int BOFF = (BOX + 127) & ~127;              // B's box offset
+  static constexpr int JWORDS = (3 * WJ * WJ + 3) & ~3;        // int4-aligned
+  static constexpr int JBYTES = (2 * JWORDS * 4 + 127) & ~127;
+  static constexpr int QBYTES(int blk) { return 6 * (blk / 32) * kQRing * 4; }
+  static constexpr int FBYTES = W * W * (2 * 8 + 2 * 4);
+  static constexpr size_t bytes(int blk) { return (size_t)JBYTES + QBYTES(blk) + FBYTES; }
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 template <int T, int BLK, int MINB>
-__global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
+__global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant__ PushParams p) {
+  using L = K1Smem<T>;
   constexpr int W = T + 2, WJ = T + 3, NW = BLK / 32;
-  constexpr int JWORDS = (3 * WJ * WJ + 3) & ~3;   // int4-aligned
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* s_eb1 = reinterpret_cast<float2*>(smem_raw);
+  constexpr int JWORDS = L::JWORDS;
+  static_assert(L::BOFF + L::BOX <= L::JBYTES + L::QBYTES(BLK), "TMA landing exceeds the current + ring bytes");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  int* s_j = reinterpret_cast<int*>(smem_raw);         // int32 current, or the high words (exact form)
+  int* s_jlo = s_j + JWORDS;                           // low words (exact form only)
+  int* s_q = reinterpret_cast<int*>(smem_raw + L::JBYTES);   // 6 arrays of NW * kQRing words
+  float2* s_eb1 = reinterpret_cast<float2*>(smem_raw + L::JBYTES + L::QBYTES(BLK));
   float2* s_eb2 = s_eb1 + W * W;
   float* s_ez = reinterpret_cast<float*>(s_eb2 + W * W);
   float* s_bz = s_ez + W * W;
-  int* s_j = reinterpret_cast<int*>(s_bz + W * W);   // int32 current, or the high words (exact form)
-  int* s_jlo = s_j + JWORDS;                           // low words (exact form only)
-  int* s_q = s_jlo + JWORDS;  // 6 arrays of NW * kQRing words
+  __shared__ __align__(8) unsigned long long s_bar;
   __shared__ int s_holes[kHCap], s_hb[kHCap], s_sa[kHCap];
   __shared__ unsigned s_bits[kHCap / 32];
   __shared__ int s_cnt[4];  // holes, holes below, stayers above, hole-list overflow
@@ -82,18 +105,42 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned ltmask = lanemask_lt();
 
-  for (int k = threadIdx.x; k < W * W; k += BLK) {
-    const int gi = i0 + k % W - 1, gj = j0 + k / W - 1;
-    float ex = 0.f, ey = 0.f, ez = 0.f, bx = 0.f, by = 0.f, bz = 0.f;
-    if (gi <= p.g.nx + 1 && gj <= p.g.ny + 1) {
-      const long a = p.g.at(gi, gj);
-      ex = __ldg(p.E + a); ey = __ldg(p.E + pl + a); ez = __ldg(p.E + 2 * pl + a);
-      bx = __ldg(p.B + a); by = __ldg(p.B + pl + a); bz = __ldg(p.B + 2 * pl + a);
+  // Stage E, B on local cells [-1, T+1)^2 with two TMA box loads (cp.async.bulk.tensor, one
+  // elected thread, completion on an mbarrier), then repack into the gather's pair layout.
+  // Cells beyond the guard-extended grid come back zero (TMA out-of-bounds fill; the padding
+  // columns of a row are zero).
+  {
+    const float* landE = reinterpret_cast<const float*>(smem_raw);
+    const float* landB = reinterpret_cast<const float*>(smem_raw + L::BOFF);
+    const unsigned bar = smem_u32(&s_bar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * L::BOX) : "memory");
+      const int cx = i0 - 4 + kXOff, cy = j0;   // padded column of local cell -4 (16 B aligned), row of -1
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+          ::"r"(smem_u32(landE)), "l"(reinterpret_cast<uint64_t>(&p.tmE)), "r"(cx), "r"(cy), "r"(0), "r"(bar)
+          : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+          ::"r"(smem_u32(landB)), "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(cx), "r"(cy), "r"(0), "r"(bar)
+          : "memory");
     }
-    s_eb1[k] = make_float2(ex, by);
-    s_eb2[k] = make_float2(ey, bx);
-    s_ez[k] = ez;
-    s_bz[k] = bz;
+    __syncthreads();   // the barrier is initialised before anyone waits on it
+    asm volatile(
+        "{\n .reg .pred done;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n"
+        " @!done bra WAIT_%=;\n}" ::"r"(bar)
+        : "memory");
+    constexpr int C = W * L::BX;   // one component of a box
+    for (int k = threadIdx.x; k < W * W; k += BLK) {
+      const int q = (k / W) * L::BX + k % W + 3;   // local cell k % W - 1 sits at box column k % W + 3
+      s_eb1[k] = make_float2(landE[q], landB[C + q]);         // (Ex, By)
+      s_eb2[k] = make_float2(landE[C + q], landB[q]);         // (Ey, Bx)
+      s_ez[k] = landE[2 * C + q];
+      s_bz[k] = landB[2 * C + q];
+    }
+    __syncthreads();   // the boxes are consumed before the current is zeroed and the rings are used
   }
   // fixed-point scale of this tile's current: 2^S from the bound sum_s n_s |q_s| on |J|
   double bound = 0.0;
@@ -345,9 +392,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(PushParams p) {
 
 template <int T, int BLK, int MINB>
 static void launch_push_T(const PushParams& p, int ntiles, cudaStream_t st) {
-  constexpr int W = T + 2, WJ = T + 3;
-  constexpr size_t smem = (size_t)W * W * (2 * sizeof(float2) + 2 * sizeof(float)) +
-                          (size_t)2 * ((3 * WJ * WJ + 3) & ~3) * sizeof(int) + (size_t)6 * (BLK / 32) * kQRing * sizeof(int);
+  constexpr size_t smem = K1Smem<T>::bytes(BLK);
   // the attribute is per device: set it once for every device this process launches on
   static unsigned attr_set = 0;
   int dev = 0;
