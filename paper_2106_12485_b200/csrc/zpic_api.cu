@@ -112,7 +112,7 @@ int round_up(int v, int m) { return (v + m - 1) / m * m; }
 // (BX, T + 2, 3) with BX = T + 5 rounded up to 4 floats (the box starts at a 16-byte aligned column
 // 4 cells left of the tile: TMA faults on an unaligned start column), zero fill outside.
 // cuTensorMapEncodeTiled is taken from the driver through the runtime (no -lcuda).
-void make_field_tmap(CUtensorMap* map, float* F, const GridDesc& g, int T) {
+void make_tmap(CUtensorMap* map, float* F, const GridDesc& g, int bx, int by) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult q;
@@ -120,15 +120,17 @@ void make_field_tmap(CUtensorMap* map, float* F, const GridDesc& g, int T) {
         q != cudaDriverEntryPointSuccess || !encode)
       throw Fail{ZPIC_E_CUDA, "cuTensorMapEncodeTiled is not available"};
   }
-  const int W = T + 2, BX = (T + 5 + 3) & ~3;
   const cuuint64_t dims[3] = {(cuuint64_t)g.pitch, (cuuint64_t)g.rows, 3};
   const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.plane * 4};
-  const cuuint32_t box[3] = {(cuuint32_t)BX, (cuuint32_t)W, 3};
+  const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 3};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, F, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw Fail{ZPIC_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")"};
+}
+void make_field_tmap(CUtensorMap* map, float* F, const GridDesc& g, int T) {
+  make_tmap(map, F, g, (T + 5 + 3) & ~3, T + 2);
 }
 
 void alloc_store(zpic_ctx* c, int s, int cap) {
@@ -550,6 +552,13 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     }
     c->J = alloc_n<float>(c, 3 * g.plane);
     c->Jf = c->opt.filter_passes > 0 ? alloc_n<float>(c, 3 * g.plane) : nullptr;
+    // K5's TMA maps (boxes: zpic_kernels.cu YeeBox)
+    for (int b = 0; b < 2; ++b) {
+      make_tmap(&c->ytm[0][b], c->E[b], g, 40, 32 + 3);
+      make_tmap(&c->ytm[1][b], c->B[b], g, 40, 32 + 2);
+    }
+    make_tmap(&c->ytmJ[0], c->J, g, 36, 32 + 1);
+    if (c->Jf) make_tmap(&c->ytmJ[1], c->Jf, g, 36, 32 + 1);
     if (c->opt.filter_passes < 0 || c->opt.filter_passes > 64) throw Fail{ZPIC_E_INVALID, "filter_passes must be in [0, 64]"};
     if (c->opt.current_mode != 0 && c->opt.current_mode != 1) throw Fail{ZPIC_E_INVALID, "current_mode must be 0 or 1"};
     const int WJ = c->T + 3;
@@ -979,6 +988,9 @@ StepState step_phase_a(zpic_ctx* c) {
 
 void step_phase_b(zpic_ctx* c, StepState& s) {
   YeeParams y{};
+  y.tmE = c->ytm[0][c->cur];
+  y.tmB = c->ytm[1][c->cur];
+  y.tmJ = c->ytmJ[0];
   y.g = c->g;
   y.E0 = c->E[c->cur]; y.B0 = c->B[c->cur]; y.J = c->J;
   y.E1 = c->E[c->cur ^ 1]; y.B1 = c->B[c->cur ^ 1];
@@ -1029,6 +1041,7 @@ void step_phase_b(zpic_ctx* c, StepState& s) {
   {
     ProfScope ps(c, K_YEE);
     y.J = Jyee;
+    y.tmJ = c->ytmJ[Jyee == c->Jf ? 1 : 0];
     if (yee_done_to > 1) {
       launch_yee(y, c->stream, 0, 1);
       launch_yee(y, c->stream, yee_done_to, -1);

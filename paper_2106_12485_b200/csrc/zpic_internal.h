@@ -112,6 +112,7 @@ struct PushParams {
 };
 
 struct YeeParams {
+  CUtensorMap tmE, tmB, tmJ;   // TMA maps of E0, B0 (box 40 x (T+3|T+2) x 3) and J (36 x (T+1) x 3)
   GridDesc g;
   const float* E0; const float* B0; const float* J;
   float* E1; float* B1;
@@ -159,6 +160,8 @@ struct zpic_ctx {
   cudaStream_t stream;
   bool own_stream;
   CUtensorMap tm[2][2];   // [E / B][buffer] TMA maps for K1's field staging
+  CUtensorMap ytm[2][2];  // [E / B][buffer] TMA maps for K5's staging (boxes of YeeBox)
+  CUtensorMap ytmJ[2];    // [J / Jf] for K5
   // device buffers
   float* E[2];
   float* B[2];

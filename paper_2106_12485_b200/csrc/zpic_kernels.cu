@@ -316,12 +316,33 @@ struct RowCol {
 };
 
 constexpr int kYeeT = 32;
-__global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
-  constexpr int T = kYeeT, WE = T + 3, WB = T + 2, WJ = T + 1;
-  __shared__ float sE[3][WE * WE];
-  __shared__ float sB[3][WB * WB];
-  __shared__ float sJ[3][WJ * WJ];
+// K5's staged boxes (TMA, one elected thread, mbarrier completion): E on local rows [-1, T+2)
+// and B on [-1, T+1), both from column -4 (the 16-byte aligned padded column i0; TMA faults on an
+// unaligned start) and 40 wide; J on rows [0, T+1) from column 0, 36 wide.  Outside the
+// guard-extended grid the boxes read zero (out-of-bounds rows; the padding columns are zero).
+struct YeeBox {
+  static constexpr int T = kYeeT;
+  static constexpr int XE = 40, YE = T + 3, XB = 40, YB = T + 2, XJ = 36, YJ = T + 1;
+  static constexpr int E = 3 * YE * XE, B = 3 * YB * XB, J = 3 * YJ * XJ;   // floats
+  static constexpr int OB = (E + 31) & ~31, OJ = OB + ((B + 31) & ~31);       // 128-byte aligned boxes
+  static constexpr size_t bytes = (size_t)(OJ + J) * 4;
+};
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, int x, int y, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];"
+      ::"r"(dst), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(0), "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParams p) {
+  constexpr int T = kYeeT;
+  constexpr int WE = YeeBox::XE, WB = YeeBox::XB, WJ = YeeBox::XJ;   // row widths of the staged boxes
+  extern __shared__ __align__(128) float yee_smem[];
+  float (*sE)[YeeBox::YE * YeeBox::XE] = reinterpret_cast<float (*)[YeeBox::YE * YeeBox::XE]>(yee_smem);
+  float (*sB)[YeeBox::YB * YeeBox::XB] = reinterpret_cast<float (*)[YeeBox::YB * YeeBox::XB]>(yee_smem + YeeBox::OB);
+  float (*sJ)[YeeBox::YJ * YeeBox::XJ] = reinterpret_cast<float (*)[YeeBox::YJ * YeeBox::XJ]>(yee_smem + YeeBox::OJ);
   __shared__ float s_mur[4][2][2][T + 1];  // E^n on Mur node lines: [edge][component][b, b'][index]
+  __shared__ __align__(8) unsigned long long s_bar;
   const GridDesc& g = p.g;
   const int i0 = blockIdx.x * T, j0 = (blockIdx.y + p.row0) * T;
   const int tw = min(T, g.nx - i0), th = min(T, g.ny - j0);
@@ -330,67 +351,51 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   // interfaces whose guards come from the neighbour)
   const bool ylo_dom = p.bcy != ZPIC_BC_PERIODIC && p.ylo_edge, yhi_dom = p.bcy != ZPIC_BC_PERIODIC && p.yhi_edge;
 
-  // Staging with asynchronous global -> shared copies (cp.async, LDGSTS): every thread issues all
-  // of its copies before waiting, no registers hold the data; a node outside the guard-extended
-  // grid is zero-filled (source size 0).
-  // (plane offsets fit in 32 bits: 3 planes of <= 2^29 floats)
   {
-    RowCol<WE> rc(threadIdx.x);
-    for (int k = threadIdx.x; k < WE * WE; k += kBlock, rc.next()) {
-      const int gi = i0 + rc.c - 1, gj = j0 + rc.r - 1;
-      const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
-      const int a = in ? (int)g.at(gi, gj) : 0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) cp_async4(&sE[c][k], p.E0 + c * (int)pl + a, in);
+    const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
+                   "r"((YeeBox::E + YeeBox::B + YeeBox::J) * 4)   // the bytes the three boxes deliver
+                   : "memory");
+      // padded column of local cell -4 is i0 (kXOff = 4); padded row of local row r is j0 + r + 1
+      tma_load_3d((unsigned)__cvta_generic_to_shared(&sE[0][0]), &p.tmE, i0, j0, bar);
+      tma_load_3d((unsigned)__cvta_generic_to_shared(&sB[0][0]), &p.tmB, i0, j0, bar);
+      tma_load_3d((unsigned)__cvta_generic_to_shared(&sJ[0][0]), &p.tmJ, i0 + kXOff, j0 + 1, bar);
     }
+    __syncthreads();
+    asm volatile(
+        "{\n .reg .pred done;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n"
+        " @!done bra WAIT_%=;\n}" ::"r"(bar)
+        : "memory");
   }
-  {
-    RowCol<WB> rc(threadIdx.x);
-    for (int k = threadIdx.x; k < WB * WB; k += kBlock, rc.next()) {
-      const int gi = i0 + rc.c - 1, gj = j0 + rc.r - 1;
-      const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
-      const int a = in ? (int)g.at(gi, gj) : 0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) cp_async4(&sB[c][k], p.B0 + c * (int)pl + a, in);
-    }
-  }
-  {
-    RowCol<WJ> rc(threadIdx.x);
-    for (int k = threadIdx.x; k < WJ * WJ; k += kBlock, rc.next()) {
-      const int gi = i0 + rc.c, gj = j0 + rc.r;
-      const bool in = gi <= g.nx + 1 && gj <= g.ny + 1;
-      const int a = in ? (int)g.at(gi, gj) : 0;
-#pragma unroll
-      for (int c = 0; c < 3; ++c) cp_async4(&sJ[c][k], p.J + c * (int)pl + a, in);
-    }
-  }
-  cp_async_wait_all();
-  __syncthreads();
 
+#define EI(lx, ly) (((ly) + 1) * WE + (lx) + 4)
+#define BI(lx, ly) (((ly) + 1) * WB + (lx) + 4)
+#define JI(lx, ly) ((ly) * WJ + (lx))
   // FE(n) = 1/2 dx dy sum(E^2 + B^2) over this tile's interior cells
   float fe = 0.f;
   for (int k = threadIdx.x; k < T * T; k += kBlock) {
     const int lx = k % T, ly = k / T;
     if (lx < tw && ly < th) {
-      const int e = (ly + 1) * WE + lx + 1, b = (ly + 1) * WB + lx + 1;
+      const int e = EI(lx, ly), b = BI(lx, ly);
 #pragma unroll
       for (int c = 0; c < 3; ++c) fe += sE[c][e] * sE[c][e] + sB[c][b] * sB[c][b];
     }
   }
-#define EI(lx, ly) (((ly) + 1) * WE + (lx) + 1)
-#define BI(lx, ly) (((ly) + 1) * WB + (lx) + 1)
-#define JI(lx, ly) ((ly) * WJ + (lx))
   // B^{n+1/2} on [-1, T]^2
-  RowCol<WB> rcb(threadIdx.x);
-  for (int k = threadIdx.x; k < WB * WB; k += kBlock, rcb.next()) {
+  RowCol<T + 2> rcb(threadIdx.x);
+  for (int k = threadIdx.x; k < (T + 2) * (T + 2); k += kBlock, rcb.next()) {
     const int lx = rcb.c - 1, ly = rcb.r - 1;
+    const int bk = BI(lx, ly);
     const int gi = i0 + lx, gj = j0 + ly;
     if ((p.bcx != ZPIC_BC_PERIODIC && (gi < 0 || gi >= g.nx)) || (gj < 0 && ylo_dom) || (gj >= g.ny && yhi_dom))
       continue;   // B guards of a non-periodic axis stay 0 (only the interior is advanced)
     const float ez = sE[2][EI(lx, ly)];
-    sB[0][k] -= p.hdy * (sE[2][EI(lx, ly + 1)] - ez);
-    sB[1][k] += p.hdx * (sE[2][EI(lx + 1, ly)] - ez);
-    sB[2][k] += p.hdy * (sE[0][EI(lx, ly + 1)] - sE[0][EI(lx, ly)]) - p.hdx * (sE[1][EI(lx + 1, ly)] - sE[1][EI(lx, ly)]);
+    sB[0][bk] -= p.hdy * (sE[2][EI(lx, ly + 1)] - ez);
+    sB[1][bk] += p.hdx * (sE[2][EI(lx + 1, ly)] - ez);
+    sB[2][bk] += p.hdy * (sE[0][EI(lx, ly + 1)] - sE[0][EI(lx, ly)]) - p.hdx * (sE[1][EI(lx + 1, ly)] - sE[1][EI(lx, ly)]);
   }
   if (p.bcx == ZPIC_BC_OPEN || p.bcy == ZPIC_BC_OPEN) {   // save E^n on the Mur node lines
     for (int k = threadIdx.x; k < 4 * 2 * 2 * (T + 1); k += kBlock) {
@@ -408,13 +413,14 @@ __global__ void __launch_bounds__(kBlock) k_yee(YeeParams p) {
   }
   __syncthreads();
   // E^{n+1} on [0, T]^2
-  RowCol<WJ> rcj(threadIdx.x);
-  for (int k = threadIdx.x; k < WJ * WJ; k += kBlock, rcj.next()) {
+  RowCol<T + 1> rcj(threadIdx.x);
+  for (int k = threadIdx.x; k < (T + 1) * (T + 1); k += kBlock, rcj.next()) {
     const int lx = rcj.c, ly = rcj.r;
+    const int jk = JI(lx, ly);
     const int e = EI(lx, ly), b = BI(lx, ly);
-    sE[0][e] += p.dtdy * (sB[2][b] - sB[2][BI(lx, ly - 1)]) - p.dt * sJ[0][k];
-    sE[1][e] -= p.dtdx * (sB[2][b] - sB[2][BI(lx - 1, ly)]) + p.dt * sJ[1][k];
-    sE[2][e] += p.dtdx * (sB[1][b] - sB[1][BI(lx - 1, ly)]) - p.dtdy * (sB[0][b] - sB[0][BI(lx, ly - 1)]) - p.dt * sJ[2][k];
+    sE[0][e] += p.dtdy * (sB[2][b] - sB[2][BI(lx, ly - 1)]) - p.dt * sJ[0][jk];
+    sE[1][e] -= p.dtdx * (sB[2][b] - sB[2][BI(lx - 1, ly)]) + p.dt * sJ[1][jk];
+    sE[2][e] += p.dtdx * (sB[1][b] - sB[1][BI(lx - 1, ly)]) - p.dtdy * (sB[0][b] - sB[0][BI(lx, ly - 1)]) - p.dt * sJ[2][jk];
   }
   __syncthreads();
   // Non-periodic edges (R13, R14).  The node line on a domain edge holds: Mur-1 values for the
@@ -931,13 +937,20 @@ void launch_guard_y(float* F, const GridDesc& g, int mode, int keep, cudaStream_
 }
 // K5 over tile rows [row_begin, row_end) (row_end < 0: to the last)
 void launch_yee(const YeeParams& p, cudaStream_t st, int row_begin, int row_end) {
+  static unsigned attr_set = 0;   // per device
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 32 || !((attr_set >> dev) & 1u)) {
+    cudaFuncSetAttribute(k_yee, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YeeBox::bytes);
+    if (dev < 32) attr_set |= 1u << dev;
+  }
   const int nty = (p.g.ny + kYeeT - 1) / kYeeT;
   if (row_end < 0 || row_end > nty) row_end = nty;
   if (row_end <= row_begin) return;
   YeeParams q = p;
   q.row0 = row_begin;
   dim3 grid((p.g.nx + kYeeT - 1) / kYeeT, row_end - row_begin);
-  k_yee<<<grid, kBlock, 0, st>>>(q);
+  k_yee<<<grid, kBlock, YeeBox::bytes, st>>>(q);
 }
 int yee_tile_rows(const GridDesc& g) { return (g.ny + kYeeT - 1) / kYeeT; }
 void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4,
