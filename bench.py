@@ -28,6 +28,27 @@ K1_BYTES_PER_PARTICLE = 56
 K1_BYTES_PER_CELL = 36
 
 
+def numa_bind(device):
+    """Pin this process to the CPUs of the GPU's NUMA node (sysfs local_cpulist of its PCI
+    device), so the pinned host buffers of the end-to-end leg are allocated next to the GPU's PCIe
+    root.  No-op when the topology is not readable."""
+    try:
+        bus = subprocess.run(["nvidia-smi", "--query-gpu=pci.bus_id", "--format=csv,noheader", "-i", str(device)],
+                             capture_output=True, text=True, timeout=20).stdout.strip().lower()
+        dom, rest = bus.split(":", 1)
+        path = "/sys/bus/pci/devices/%s:%s/local_cpulist" % (dom[-4:], rest)
+        cpus = set()
+        for part in open(path).read().strip().split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return sorted(cpus)
+    except Exception:
+        pass
+    return None
+
+
 def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -256,6 +277,7 @@ def main():
         run_reference(args, world, rank)
         return
 
+    numa_bind(local)
     import torch
     import synth
     import paper_2106_12485_b200 as z

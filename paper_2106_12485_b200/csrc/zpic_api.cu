@@ -36,8 +36,8 @@ void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nsp
                      int* sic, int* soc, int* stats, int64_t* d_nmove, int shifted, cudaStream_t st);
 void launch_inject(const InjectParams& q, int ntiles, cudaStream_t st);
 void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
-                const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err, const PList& loose, int s,
-                cudaStream_t st);
+                const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err,
+                const PList& loose, int s, cudaStream_t st, int nx = 0, int ny = 0, int* bad = nullptr, long id0 = 0);
 void launch_export(const PStore& ps, int ntiles, const int64_t* prefix, int y0, int32_t* ix, int32_t* iy, float* x,
                    float* y, float* ux, float* uy, float* uz, uint32_t* id, cudaStream_t st);
 void launch_count(int T, int ntx, int nx, int ny, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
@@ -430,7 +430,7 @@ extern "C" {
 const char* zpic_last_error(const zpic_ctx* ctx) { return ctx ? ctx->last_error.c_str() : g_init_error.c_str(); }
 
 static void load_species(zpic_ctx* c, int s, int64_t n, char* tmp, bool has_id);
-static void size_lists(zpic_ctx* c);
+static void size_lists(zpic_ctx* c, int64_t extra = 0);
 
 // The one x sub-row of a ramp species (R16), in the oracle-independent arithmetic of the library:
 // ramp positions by cumulative inversion, then the regular sub-lattice from x1 on; cell index and
@@ -753,9 +753,9 @@ static void load_species(zpic_ctx* c, int s, int64_t n, char* tmp, bool has_id) 
 }
 
 // Movers / loose lists sized for the current population (the live loose list keeps its
-// contents when it grows).
-static void size_lists(zpic_ctx* c) {
-  int64_t total = 0;
+// contents when it grows); `extra` particles about to be loaded are counted in.
+static void size_lists(zpic_ctx* c, int64_t extra) {
+  int64_t total = extra;
   for (int q = 0; q < c->nspecies; ++q) {
     std::vector<int> cnt(c->ntiles);
     CUDA_OR_THROW(cudaMemcpy(cnt.data(), c->ps[q].cnt, c->ntiles * 4, cudaMemcpyDeviceToHost));
@@ -857,6 +857,12 @@ static void repack(zpic_ctx* c) {
 
 // Called between steps: re-pack when the loose list holds more than a quarter of its capacity
 // (or 4096 particles, whichever is larger).
+static void maybe_repack_now(zpic_ctx* c) {
+  int nl = 0;
+  CUDA_OR_THROW(cudaMemcpyAsync(&nl, c->spill[c->steps & 1].count, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  if (nl > std::max<int64_t>(4096, std::min<int64_t>(c->spill[0].cap / 4, c->population / 64))) repack(c);
+}
 static void maybe_repack(zpic_ctx* c) {
   if (c->since_check < kRepackCheck) return;
   c->since_check = 0;
@@ -864,6 +870,72 @@ static void maybe_repack(zpic_ctx* c) {
   CUDA_OR_THROW(cudaMemcpyAsync(&nl, c->spill[c->steps & 1].count, 4, cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
   if (nl > std::max<int64_t>(4096, std::min<int64_t>(c->spill[0].cap / 4, c->population / 64))) repack(c);
+}
+
+static void maybe_repack_now(zpic_ctx* c);
+
+// Chunked direct load: when the species' tile store already has room for n particles on average
+// (it was sized for the species' lattice at zpic_init), the host arrays are copied in chunks into
+// two device staging buffers on a copy stream while the compute stream bins the previous chunk
+// (validation inside the binning; a full tile sends the rest to the loose list, re-packed after if
+// it grew).  No full-size device copy of the input, and the upload overlaps the binning.
+constexpr int64_t kLoadChunk = 1 << 23;
+static bool load_chunked(zpic_ctx* c, int s, int64_t n, const int32_t* ix, const int32_t* iy, const float* x,
+                         const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id) {
+  PStore& ps = c->ps[s];
+  if (!ps.data || n <= kLoadChunk || (double)n > 0.9 * (double)ps.cap * c->ntiles) return false;
+  CUDA_OR_THROW(cudaMemsetAsync(ps.cnt, 0, (size_t)c->ntiles * 4, c->stream));
+  size_lists(c, n);   // loose list room for what may not fit
+  if (!c->copy_stream) CUDA_OR_THROW(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+  cudaEvent_t copied[2], binned[2];
+  for (int b = 0; b < 2; ++b) {
+    CUDA_OR_THROW(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
+    CUDA_OR_THROW(cudaEventCreateWithFlags(&binned[b], cudaEventDisableTiming));
+  }
+  char* stage = (char*)dev_alloc(c, (size_t)2 * kLoadChunk * 32);
+  int* bad = alloc_n<int>(c, 1);
+  const int64_t nchunks = (n + kLoadChunk - 1) / kLoadChunk;
+  for (int64_t k = 0; k < nchunks; ++k) {
+    const int b = (int)(k & 1);
+    const int64_t o = k * kLoadChunk, m = std::min(kLoadChunk, n - o);
+    char* buf = stage + (size_t)b * kLoadChunk * 32;
+    int32_t* dix = (int32_t*)buf;
+    int32_t* diy = dix + kLoadChunk;
+    float* dx_ = (float*)(diy + kLoadChunk);
+    float* dy_ = dx_ + kLoadChunk;
+    float* dux = dy_ + kLoadChunk;
+    float* duy = dux + kLoadChunk;
+    float* duz = duy + kLoadChunk;
+    uint32_t* did = (uint32_t*)(duz + kLoadChunk);
+    if (k >= 2) CUDA_OR_THROW(cudaStreamWaitEvent(c->copy_stream, binned[b], 0));
+    const size_t mb = (size_t)m * 4;
+    CUDA_OR_THROW(cudaMemcpyAsync(dix, ix + o, mb, cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_OR_THROW(cudaMemcpyAsync(diy, iy + o, mb, cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_OR_THROW(cudaMemcpyAsync(dx_, x + o, mb, cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_OR_THROW(cudaMemcpyAsync(dy_, y + o, mb, cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_OR_THROW(cudaMemcpyAsync(dux, ux + o, mb, cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_OR_THROW(cudaMemcpyAsync(duy, uy + o, mb, cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_OR_THROW(cudaMemcpyAsync(duz, uz + o, mb, cudaMemcpyHostToDevice, c->copy_stream));
+    if (id) CUDA_OR_THROW(cudaMemcpyAsync(did, id + o, mb, cudaMemcpyHostToDevice, c->copy_stream));
+    CUDA_OR_THROW(cudaEventRecord(copied[b], c->copy_stream));
+    CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, copied[b], 0));
+    launch_bin(ps, c->T, c->ntx, c->y0, (long)m, dix, diy, dx_, dy_, dux, duy, duz, id ? did : nullptr, c->err,
+               c->spill[c->steps & 1], s, c->stream, c->g.nx, c->g.ny, bad, (long)o);
+    CUDA_OR_THROW(cudaGetLastError());
+    CUDA_OR_THROW(cudaEventRecord(binned[b], c->stream));
+  }
+  int nbad = 0;
+  CUDA_OR_THROW(cudaMemcpyAsync(&nbad, bad, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  for (int b = 0; b < 2; ++b) { cudaEventDestroy(copied[b]); cudaEventDestroy(binned[b]); }
+  dev_free(c, stage);
+  dev_free(c, bad);
+  if (nbad) {
+    CUDA_OR_THROW(cudaMemsetAsync(ps.cnt, 0, (size_t)c->ntiles * 4, c->stream));
+    throw Fail{ZPIC_E_INVALID, "set_particles: a particle is outside the local slab or its offset is not in [0,1)"};
+  }
+  maybe_repack_now(c);
+  return true;
 }
 
 zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t* ix, const int32_t* iy, const float* x,
@@ -874,6 +946,10 @@ zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t*
   }
   drop_graphs(c);
   try {
+    if (load_chunked(c, s, n, ix, iy, x, y, ux, uy, uz, id)) {
+      size_lists(c);
+      return check_sticky(c);
+    }
     // upload, then validate + count per tile and bin on the device
     char* tmp = (char*)dev_alloc(c, (size_t)std::max<int64_t>(n, 1) * (7 * 4 + 4));
     int32_t* dix = (int32_t*)tmp;
@@ -1490,6 +1566,7 @@ void zpic_free(zpic_ctx* c) {
   for (auto e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   for (void* p : c->allocations) {
     if (c->opt.free) c->opt.free(p, c->opt.alloc_user);

@@ -190,6 +190,7 @@ struct zpic_ctx {
   int transport;
   void* comm;        // ncclComm_t
   cudaStream_t comm_stream = nullptr;   // NCCL halo rounds, overlapped with interior kernels
+  cudaStream_t copy_stream = nullptr;   // chunked host uploads (zpic_set_particles)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};   // phase-A end, round 1, Yee end, round 2
   bool r2_pending = false;              // round 2 of the last step is in flight on comm_stream
   bool own_comm;

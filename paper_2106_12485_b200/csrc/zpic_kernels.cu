@@ -759,23 +759,29 @@ __global__ void k_count(int T, int ntx, int nx, int ny, int y0, long n, const in
 }
 
 // Bin host-uploaded particles (global iy -> slab-local) into tiles.
+// bad != nullptr: also validate (a particle outside the slab or with an offset outside [0, 1) is
+// skipped and counted in *bad); id0: the id of entry 0 when no ids are given.
 __global__ void k_bin(PStore ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
                       const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err,
-                      PList loose, int s) {
+                      PList loose, int s, int nx, int ny, int* bad, long id0) {
   for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) {
     const int cx = ix[k], cy = iy[k] - y0;
+    if (bad && (cx < 0 || cx >= nx || cy < 0 || cy >= ny || !(x[k] >= 0.f && x[k] < 1.f) || !(y[k] >= 0.f && y[k] < 1.f))) {
+      atomicAdd(bad, 1);
+      continue;
+    }
     const int t = (cy / T) * ntx + cx / T;
     const int slot = atomicAdd(ps.cnt + t, 1);
     if (slot >= ps.cap) {   // tile full (capacity slack < 1): the loose list takes it
       atomicSub(ps.cnt + t, 1);
-      list_append(loose, err, pack_cell(cx, cy), x[k], y[k], ux[k], uy[k], uz[k], id ? id[k] : (uint32_t)k, s);
+      list_append(loose, err, pack_cell(cx, cy), x[k], y[k], ux[k], uy[k], uz[k], id ? id[k] : (uint32_t)(id0 + k), s);
       continue;
     }
     uint32_t* o = ps.slot((long)t * ps.cap + slot);
     o[F_CELL * 32] = (uint32_t)pack_cell(cx, cy);
     o[F_X * 32] = __float_as_uint(x[k]); o[F_Y * 32] = __float_as_uint(y[k]);
     o[F_UX * 32] = __float_as_uint(ux[k]); o[F_UY * 32] = __float_as_uint(uy[k]); o[F_UZ * 32] = __float_as_uint(uz[k]);
-    if (ps.nf > F_ID) o[F_ID * 32] = id ? id[k] : (uint32_t)k;
+    if (ps.nf > F_ID) o[F_ID * 32] = id ? id[k] : (uint32_t)(id0 + k);
   }
 }
 
@@ -961,9 +967,10 @@ void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nsp
 void launch_inject(const InjectParams& q, int ntiles, cudaStream_t st) { k_inject<<<ntiles, kBlock, 0, st>>>(q); }
 void launch_bin(const PStore& ps, int T, int ntx, int y0, long n, const int32_t* ix, const int32_t* iy, const float* x,
                 const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id, int* err,
-                const PList& loose, int s, cudaStream_t st) {
+                const PList& loose, int s, cudaStream_t st, int nx, int ny, int* bad, long id0) {
   const int grid = (int)std::min<long>((n + kBlock - 1) / kBlock, 148L * 32);
-  if (grid > 0) k_bin<<<grid, kBlock, 0, st>>>(ps, T, ntx, y0, n, ix, iy, x, y, ux, uy, uz, id, err, loose, s);
+  if (grid > 0)
+    k_bin<<<grid, kBlock, 0, st>>>(ps, T, ntx, y0, n, ix, iy, x, y, ux, uy, uz, id, err, loose, s, nx, ny, bad, id0);
 }
 void launch_inject_column(const PushParams& p, int s, int px, int py, const int64_t* n_move, int ny_global, int y0, uint64_t key,
                           const double* ufl, const double* uth, cudaStream_t st) {

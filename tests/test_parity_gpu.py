@@ -510,3 +510,26 @@ def test_cuda_graph_replay_moving_window():
     for k in pa:
         assert np.array_equal(pa[k], pb[k]), k
     assert np.array_equal(Ea, Eb) and np.array_equal(Ba, Bb)
+
+
+def test_chunked_upload_validates_and_matches_direct_load():
+    """zpic_set_particles streams a large upload (> 8 M particles) in chunks through two staging
+    buffers into the tile store: the loaded set equals the input (keyed by id), and a particle with
+    an offset outside [0, 1) anywhere in the upload is rejected with ZPIC_E_INVALID."""
+    cfg = synth.config("C1", nx=768, ny=768)          # 9.4 M particles
+    parts = synth.species_particles(cfg, 0)
+    sim = _z().Simulation(cfg, inject=False, track_ids=True)
+    sim.set_particles(0, parts)
+    g = sim.particles(0, True)
+    o = np.argsort(g["id"])
+    g = {k: v[o] for k, v in g.items()}
+    assert np.array_equal(g["id"], parts["id"])
+    for k in ("ix", "iy", "x", "y", "ux", "uy", "uz"):
+        assert np.array_equal(g[k], parts[k]), k
+    bad = dict(parts)
+    bad["x"] = parts["x"].copy()
+    bad["x"][len(bad["x"]) - 3] = 1.0
+    with pytest.raises(_z().ZpicError) as e:
+        sim.set_particles(0, bad)
+    assert e.value.status == -1
+    sim.close()
