@@ -99,6 +99,16 @@ void dev_free(zpic_ctx* c, void* p) {
   else cudaFree(p);
 }
 
+// A temporary device buffer released when the scope ends (also when a Fail unwinds it).
+struct TmpBuf {
+  zpic_ctx* c;
+  void* p;
+  TmpBuf(zpic_ctx* c_, size_t bytes) : c(c_), p(dev_alloc(c_, bytes)) {}
+  ~TmpBuf() { dev_free(c, p); }
+  TmpBuf(const TmpBuf&) = delete;
+  TmpBuf& operator=(const TmpBuf&) = delete;
+};
+
 template <class T>
 T* alloc_n(zpic_ctx* c, size_t n) {
   T* p = (T*)dev_alloc(c, n * sizeof(T));
@@ -892,8 +902,10 @@ static bool load_chunked(zpic_ctx* c, int s, int64_t n, const int32_t* ix, const
     CUDA_OR_THROW(cudaEventCreateWithFlags(&copied[b], cudaEventDisableTiming));
     CUDA_OR_THROW(cudaEventCreateWithFlags(&binned[b], cudaEventDisableTiming));
   }
-  char* stage = (char*)dev_alloc(c, (size_t)2 * kLoadChunk * 32);
-  int* bad = alloc_n<int>(c, 1);
+  TmpBuf stage_buf(c, (size_t)2 * kLoadChunk * 32), bad_buf(c, 4);
+  char* stage = (char*)stage_buf.p;
+  int* bad = (int*)bad_buf.p;
+  CUDA_OR_THROW(cudaMemsetAsync(bad, 0, 4, c->stream));
   const int64_t nchunks = (n + kLoadChunk - 1) / kLoadChunk;
   for (int64_t k = 0; k < nchunks; ++k) {
     const int b = (int)(k & 1);
@@ -928,8 +940,6 @@ static bool load_chunked(zpic_ctx* c, int s, int64_t n, const int32_t* ix, const
   CUDA_OR_THROW(cudaMemcpyAsync(&nbad, bad, 4, cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
   for (int b = 0; b < 2; ++b) { cudaEventDestroy(copied[b]); cudaEventDestroy(binned[b]); }
-  dev_free(c, stage);
-  dev_free(c, bad);
   if (nbad) {
     CUDA_OR_THROW(cudaMemsetAsync(ps.cnt, 0, (size_t)c->ntiles * 4, c->stream));
     throw Fail{ZPIC_E_INVALID, "set_particles: a particle is outside the local slab or its offset is not in [0,1)"};
