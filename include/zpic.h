@@ -149,14 +149,21 @@ typedef struct {
 
 typedef struct zpic_ctx zpic_ctx;
 
-/* Validate, allocate, inject every species (profile != NONE) and zero the fields.
- * Errors: ZPIC_E_INVALID, ZPIC_E_CFL, ZPIC_E_EMPTY_GRID, ZPIC_E_DECOMP, ZPIC_E_OOM, ZPIC_E_CUDA. */
+/* Validate, allocate, inject every species (UNIFORM / SLAB lattices with the seeded momenta, RAMP
+ * by cumulative inversion), zero the fields and, with options->laser, write the laser pulse.
+ * nx, ny in [2, 32767]; dt below the Courant limit 1/sqrt(dx^-2 + dy^-2).
+ * Errors: ZPIC_E_INVALID, ZPIC_E_CFL, ZPIC_E_EMPTY_GRID, ZPIC_E_DECOMP, ZPIC_E_LASER, ZPIC_E_OOM,
+ * ZPIC_E_CUDA, ZPIC_E_NCCL. On error *out is NULL and zpic_last_error(NULL) says why. */
 zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zpic_species* species,
                       int32_t n_species, const zpic_boundaries* bc, uint64_t seed,
                       const zpic_options* options, const zpic_dist* dist);
 
-/* Replace the particles of one species by n host particles (global ix, iy).  id may be NULL
- * (then ids are 0..n-1 if track_ids).  Particles outside the local slab are an error. */
+/* Replace the particles of one species by n host particles (global ix, iy; x, y in [0, 1)).
+ * id may be NULL (then ids are 0..n-1 if track_ids).  The arrays are copied (pinned host memory
+ * uploads at the PCIe rate; large uploads stream in chunks, overlapped with the binning on the
+ * device).  A particle outside the local slab or with an offset outside [0, 1) is an error
+ * (ZPIC_E_INVALID; the species is left empty).  Tiles without room send particles to the loose
+ * list, which is re-packed when it grows.  Synchronous.  Drops the captured step graphs. */
 zpic_status zpic_set_particles(zpic_ctx* ctx, int32_t species, int64_t n, const int32_t* ix,
                                const int32_t* iy, const float* x, const float* y, const float* ux,
                                const float* uy, const float* uz, const uint32_t* id);
@@ -164,8 +171,14 @@ zpic_status zpic_set_particles(zpic_ctx* ctx, int32_t species, int64_t n, const 
 /* Overwrite E (which=0) or B (which=1) interior values from host [comp][y][x] (laser init). */
 zpic_status zpic_set_fields(zpic_ctx* ctx, int32_t which, const float* in, size_t in_len);
 
-/* Enqueue n time steps (asynchronous w.r.t. the host).  With NCCL slabs every rank must call it
- * with the same n (the halo exchanges are collective between neighbours). */
+/* Enqueue n time steps (asynchronous w.r.t. the host, on the context's stream).  Without slabs
+ * and with profile = 0 the steps are replayed as captured CUDA graphs (two-step graphs, or one-step
+ * graphs keyed by the window shift).  Every 16 steps the host reads the loose-list count (one
+ * stream synchronisation) and re-packs the tile stores if it grew.  With NCCL slabs every rank must
+ * call it with the same n (the halo exchanges are collective between neighbours); the exchanges run
+ * on a second stream overlapped with interior tiles, and the context's stream has waited for them
+ * when zpic_step returns.  Errors raised on the device are reported by the next synchronising
+ * call. */
 zpic_status zpic_step(zpic_ctx* ctx, int32_t n);
 
 /* Step `count` loopback slab contexts (ranks 0..count-1 of one decomposition, same device and
