@@ -74,8 +74,11 @@ struct K1Smem {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
-template <int T, int BLK, int MINB>
+// NSPEC > 0: the species count is a compile-time constant (species constants become immediate
+// constant-bank operands instead of indexed reloads); 0: p.nspecies.
+template <int T, int BLK, int MINB, int NSPEC>
 __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant__ PushParams p) {
+  const int nspec = NSPEC > 0 ? NSPEC : p.nspecies;
   using L = K1Smem<T>;
   constexpr int W = T + 2, WJ = T + 3, NW = BLK / 32;
   constexpr int JWORDS = L::JWORDS;
@@ -145,7 +148,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   // fixed-point scale of this tile's current: 2^S from the bound sum_s n_s |q_s| on |J|
   double bound = 0.0;
   int ntot = 0;
-  for (int s = 0; s < p.nspecies; ++s) {
+  for (int s = 0; s < nspec; ++s) {
     const int n = p.ps[s].cnt[t];
     bound += (double)n * fabs((double)p.sc[s].q);
     ntot += n;
@@ -169,7 +172,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
                    reinterpret_cast<float*>(s_q + 4 * NW * kQRing + qo), reinterpret_cast<float*>(s_q + 5 * NW * kQRing + qo)};
 
   auto push_all = [&](const auto& A, const float fscale) {
-  for (int s = 0; s < p.nspecies; ++s) {
+  for (int s = 0; s < nspec; ++s) {
     const PStore ps = p.ps[s];
     const SpeciesConst sc = p.sc[s];
     const float jxs = sc.jx * fscale, jys = sc.jy * fscale, qs = sc.q * fscale;
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
       }
     }
     if (threadIdx.x == 0) ps.cnt[t] = n2;
-    if (s + 1 < p.nspecies) __syncthreads();   // the hole lists / counters are reused by the next species
+    if (s + 1 < nspec) __syncthreads();   // the hole lists / counters are reused by the next species
   }
   };
   if (fast) push_all(SmemCurrentI32<WJ>{s_j}, ldexpf(1.0f, S));
@@ -386,22 +389,30 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
     for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK)
       __stcg(jt + k, (float)(fma((double)s_j[k], 32768.0, (double)s_jlo[k]) * kFxInv));
   }
-  if (threadIdx.x < p.nspecies && s_ke[threadIdx.x] != 0.0)
+  if ((int)threadIdx.x < nspec && s_ke[threadIdx.x] != 0.0)
     atomicAdd(p.ke_slots + threadIdx.x * kEnergySlots + (t & (kEnergySlots - 1)), s_ke[threadIdx.x]);
 }
 
-template <int T, int BLK, int MINB>
-static void launch_push_T(const PushParams& p, int ntiles, cudaStream_t st) {
+template <int T, int BLK, int MINB, int NSPEC>
+static void launch_push_N(const PushParams& p, int ntiles, cudaStream_t st) {
   constexpr size_t smem = K1Smem<T>::bytes(BLK);
   // the attribute is per device: set it once for every device this process launches on
   static unsigned attr_set = 0;
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev >= 32 || !((attr_set >> dev) & 1u)) {
-    cudaFuncSetAttribute(k_push_tiles<T, BLK, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(k_push_tiles<T, BLK, MINB, NSPEC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (dev < 32) attr_set |= 1u << dev;
   }
-  k_push_tiles<T, BLK, MINB><<<ntiles, BLK, smem, st>>>(p);
+  k_push_tiles<T, BLK, MINB, NSPEC><<<ntiles, BLK, smem, st>>>(p);
+}
+template <int T, int BLK, int MINB>
+static void launch_push_T(const PushParams& p, int ntiles, cudaStream_t st) {
+  switch (p.nspecies) {
+    case 1: launch_push_N<T, BLK, MINB, 1>(p, ntiles, st); break;
+    case 2: launch_push_N<T, BLK, MINB, 2>(p, ntiles, st); break;
+    default: launch_push_N<T, BLK, MINB, 0>(p, ntiles, st); break;
+  }
 }
 
 // K1 launch shape for 16x16 tiles (threads per CTA, CTAs per SM the register budget is sized
