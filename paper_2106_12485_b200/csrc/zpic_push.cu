@@ -8,11 +8,10 @@
 // DESIGN.md §2).  Then it stores the (T+3)^2 current block for K4 (or adds it into J:
 // current_mode 1) and fixes up the tile's particle segment.
 //
-// Divergence control: every lane deposits the first straight piece of its path in lock-step;
-// a path that crosses a cell edge is queued (start point, displacement, z weight) in a per-warp
-// ring buffer in shared memory, and the queue is drained 32 paths at a time with all lanes
-// active: each lane recomputes the crossings with the same arithmetic and deposits the later
-// pieces.
+// Divergence control: a path inside its start cell (most of them) is deposited as one piece in
+// the main loop; a path that crosses a cell edge is queued (start point, displacement, z weight)
+// in a per-warp ring buffer in shared memory, and the queue is drained 32 paths at a time with
+// all lanes active: each lane splits its path at the crossings and deposits all 2-3 pieces.
 // Re-sort: particles that stay in the tile are written back in place; leavers leave a hole
 // (cell = -1) and go to this tile's mailbox for their direction of travel (K3m appends them to
 // the destination tile), or to the flat mover list when the box is full or they leave the slab
@@ -40,7 +39,7 @@ struct PathRing {
   }
 };
 
-// Deposit the later pieces of queued path k (the split of PAPER.md:197).
+// Deposit every piece of queued crossing path k (the split of PAPER.md:197).
 template <class A>
 __device__ __forceinline__ void drain_path(const A& acc, const PathRing& Q, int k, float jxs, float jys) {
   const int v = Q.c[k];
@@ -48,6 +47,7 @@ __device__ __forceinline__ void drain_path(const A& acc, const PathRing& Q, int 
   const float x = Q.x[k], y = Q.y[k], dxp = Q.dx[k], dyp = Q.dy[k], qvz = Q.qvz[k];
   const float x1 = __fadd_rn(x, dxp), y1 = __fadd_rn(y, dyp);
   const Crossing c = path_crossings(x, y, dxp, dyp, x1, y1);
+  deposit_seg(acc, Seg{lx, ly, x, y, c.xa, c.ya, qvz * c.t1}, jxs, jys);
   Seg s1, s2;
   later_pieces(lx, ly, x1, y1, qvz, c, s1, s2);
   deposit_seg(acc, s1, jxs, jys);
@@ -229,10 +229,11 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         qvz = qs * uz * rg;
         x0 = x; y0 = y;
         const float x1 = __fadd_rn(x, dxp), y1 = __fadd_rn(y, dyp);
-        const Crossing c = path_crossings(x, y, dxp, dyp, x1, y1);
-        deposit_seg(A, Seg{lx, ly, x, y, c.xa, c.ya, qvz * c.t1}, jxs, jys);
-        cross = c.di || c.dj;
-        int di = c.di, dj = c.dj;
+        int di = (x1 >= 1.0f) - (x1 < 0.0f), dj = (y1 >= 1.0f) - (y1 < 0.0f);
+        cross = di || dj;
+        // a path inside its start cell is one piece, deposited now; a crossing path is queued
+        // and split in the drain (the same pieces path_crossings gives, t1 = 1: fma(1, d, x) = x1)
+        if (!cross) deposit_seg(A, Seg{lx, ly, x, y, x1, y1, qvz}, jxs, jys);
         renormalise(x1, y1, di, dj, x, y);
         di -= p.shift;   // moving window: the cell index follows the shift at the end of the step
         ix += di; iy += dj;

@@ -11,7 +11,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO = os.path.join(HERE, "libzpic_b200.so")
+# ZPIC_SO: another in-tree build of the same library (same-box A/B timing of kernel variants,
+# tools/gpu/ab.sh); only a bare file name inside this package directory is accepted
+SO = os.path.join(HERE, os.path.basename(os.environ.get("ZPIC_SO", "libzpic_b200.so")))
 
 if not os.path.exists(SO):
     raise ImportError("libzpic_b200.so is not built (run `python -m paper_2106_12485_b200.build` or "
