@@ -41,10 +41,12 @@ struct PathRing {
 
 // Deposit every piece of queued crossing path k (the split of PAPER.md:197).
 template <class A>
-__device__ __forceinline__ void drain_path(const A& acc, const PathRing& Q, int k, float jxs, float jys) {
+__device__ __forceinline__ void drain_path(const A& acc, const PathRing& Q, int k, float jxs, float jys, int* err) {
   const int v = Q.c[k];
   const int lx = (v & 0xffff) - 8, ly = (v >> 16) - 8;
   const float x = Q.x[k], y = Q.y[k], dxp = Q.dx[k], dyp = Q.dy[k], qvz = Q.qvz[k];
+  // a path that stays in its cell moved less than a cell: only a queued path can move >= 1
+  if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(err, ERR_MIGRATION);
   const float x1 = __fadd_rn(x, dxp), y1 = __fadd_rn(y, dyp);
   const Crossing c = path_crossings(x, y, dxp, dyp, x1, y1);
   deposit_seg(acc, Seg{lx, ly, x, y, c.xa, c.ya, qvz * c.t1}, jxs, jys);
@@ -225,7 +227,6 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         // __fmul_rn: no contraction into x + dxp, so the drain recomputes the same end point
         dxp = __fmul_rn(ux * rg, p.dtdx);
         dyp = __fmul_rn(uy * rg, p.dtdy);
-        if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(p.err, ERR_MIGRATION);
         qvz = qs * uz * rg;
         x0 = x; y0 = y;
         const float x1 = __fadd_rn(x, dxp), y1 = __fadd_rn(y, dyp);
@@ -252,7 +253,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         qn += __popc(bal);
         __syncwarp();
         if (qn >= 32) {
-          drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys);
+          drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys, p.err);
           qh = (qh + 32) & (kQRing - 1);
           qn -= 32;
           __syncwarp();   // the drained entries are read before the next put overwrites them
@@ -294,7 +295,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         else atomicOr(p.err, ERR_OVERFLOW);
       }
     }
-    if (lane < qn) drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys);
+    if (lane < qn) drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys, p.err);
     // kinetic energy: warp reduction, one shared fp64 add per warp, one global add per CTA
     for (int o = 16; o > 0; o >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, o);
     if (lane == 0) atomicAdd(&s_ke[s], (double)ke);
