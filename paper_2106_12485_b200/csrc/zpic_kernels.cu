@@ -167,36 +167,51 @@ __global__ void __launch_bounds__(kBlock) k_mail_gather(PushParams p) {
 // K4: J grid node (i, j), -1 <= i <= nx+1, -1 <= j <= ny+1, = sum of the (at most 2 x 2) tile
 // blocks covering it.  No periodic wrap here: blocks at the domain edge land in the guards and
 // K4b folds them ("the reduction is only required for ghost cells").
+// Each thread assembles K4R nodes of one column (rows j, j + 1, ...): all their block loads are
+// issued before the sums (more bytes in flight per thread; K4 is latency-bound otherwise).
+constexpr int K4R = 4;
 template <int T>
 __global__ void __launch_bounds__(kBlock) k_assemble_j(float* __restrict__ J, const float* __restrict__ Jt, GridDesc g,
                                                        int ntx, int nty) {
   constexpr int WJ = T + 3;
   const int i = blockIdx.x * blockDim.x + threadIdx.x - 1;
-  const int j = blockIdx.y - 1;
   if (i > g.nx + 1) return;
-  int txs[2], lxs[2], nxs = 0, tys[2], lys[2], nys = 0;
-  {
-    const int th = (i + 1) / T, lh = i - th * T;
-    if (th < ntx) { txs[nxs] = th; lxs[nxs++] = lh; }
-    if (lh <= 1 && th >= 1) { txs[nxs] = th - 1; lxs[nxs++] = lh + T; }
-  }
-  {
+  // column i's entry in the (at most 2) x-overlapping tile blocks of tile row 0
+  const int thx = (i + 1) / T, lhx = i - thx * T;
+  const bool xa = thx < ntx, xb = lhx <= 1 && thx >= 1;
+  const float* bxa = Jt + (long)thx * 3 * WJ * WJ + (lhx + 1);
+  const float* bxb = Jt + (long)(thx - 1) * 3 * WJ * WJ + (lhx + T + 1);
+  float v[K4R][3];
+#pragma unroll
+  for (int r = 0; r < K4R; ++r) {
+    const int j = blockIdx.y * K4R + r - 1;
     const int th = (j + 1) / T, lh = j - th * T;
-    if (th < nty) { tys[nys] = th; lys[nys++] = lh; }
-    if (lh <= 1 && th >= 1) { tys[nys] = th - 1; lys[nys++] = lh + T; }
+    const bool in = j <= g.ny + 1;
+    const bool ya = in && th < nty, yb = in && lh <= 1 && th >= 1;
+    const long oa = (long)th * ntx * 3 * WJ * WJ + (lh + 1) * WJ;
+    const long ob = (long)(th - 1) * ntx * 3 * WJ * WJ + (lh + T + 1) * WJ;
+    v[r][0] = v[r][1] = v[r][2] = 0.f;
+    auto add = [&](bool ok, const float* blk) {
+      if (ok) {
+        v[r][0] += __ldcg(blk);
+        v[r][1] += __ldcg(blk + WJ * WJ);
+        v[r][2] += __ldcg(blk + 2 * WJ * WJ);
+      }
+    };
+    add(ya && xa, bxa + oa);
+    add(ya && xb, bxb + oa);
+    add(yb && xa, bxa + ob);
+    add(yb && xb, bxb + ob);
   }
-  float v0 = 0.f, v1 = 0.f, v2 = 0.f;
-  for (int a = 0; a < nys; ++a)
-    for (int b = 0; b < nxs; ++b) {
-      const float* blk = Jt + ((long)tys[a] * ntx + txs[b]) * 3 * WJ * WJ + (lys[a] + 1) * WJ + (lxs[b] + 1);
-      v0 += __ldcg(blk);
-      v1 += __ldcg(blk + WJ * WJ);
-      v2 += __ldcg(blk + 2 * WJ * WJ);
-    }
-  const long o = g.at(i, j);
-  J[o] = v0;
-  J[g.plane + o] = v1;
-  J[2 * g.plane + o] = v2;
+#pragma unroll
+  for (int r = 0; r < K4R; ++r) {
+    const int j = blockIdx.y * K4R + r - 1;
+    if (j > g.ny + 1) break;
+    const long o = g.at(i, j);
+    J[o] = v[r][0];
+    J[g.plane + o] = v[r][1];
+    J[2 * g.plane + o] = v[r][2];
+  }
 }
 
 // =============================================================================================
@@ -926,7 +941,7 @@ void launch_mail_gather(const PushParams& p, cudaStream_t st) {
 void launch_insert(const PushParams& p, int grid, cudaStream_t st) { k_insert<<<grid * 2, kBlock, 0, st>>>(p); }
 void launch_loose(const PushParams& p, int grid, cudaStream_t st) { k_push_loose<<<grid, kBlock, 0, st>>>(p); }
 void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st) {
-  dim3 grid((g.nx + 3 + kBlock - 1) / kBlock, g.ny + 3);
+  dim3 grid((g.nx + 3 + kBlock - 1) / kBlock, (g.ny + 3 + K4R - 1) / K4R);
   switch (T) {
     case 8: k_assemble_j<8><<<grid, kBlock, 0, st>>>(J, Jt, g, ntx, nty); break;
     case 16: k_assemble_j<16><<<grid, kBlock, 0, st>>>(J, Jt, g, ntx, nty); break;

@@ -8,7 +8,9 @@ import json, sys
 for l in open("gpurun_out/ab.log"):
     if l.startswith("{"):
         d = json.loads(l)
-        print("%-28s round %s  ms/step %.3f  K1 %.3f ms  frac %.3f" % (sys.argv[1], sys.argv[2], d["ms_per_step"], d["roofline"]["avg_launch_ms"], d["roofline"]["frac"]))
+        k = d["kernel_ms_per_step"]
+        print("%-28s round %s  ms/step %.3f  K1 %.3f ms  frac %.3f  | %s" % (sys.argv[1], sys.argv[2], d["ms_per_step"], d["roofline"]["avg_launch_ms"], d["roofline"]["frac"],
+              " ".join("%s %.3f" % (n[2:], v) for n, v in sorted(k.items()) if n != "k_push_tiles" and v > 0.05)))
 PY
   done
 done
