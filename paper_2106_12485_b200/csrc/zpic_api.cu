@@ -564,11 +564,11 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     c->Jf = c->opt.filter_passes > 0 ? alloc_n<float>(c, 3 * g.plane) : nullptr;
     // K5's TMA maps (boxes: zpic_kernels.cu YeeBox)
     for (int b = 0; b < 2; ++b) {
-      make_tmap(&c->ytm[0][b], c->E[b], g, 40, 32 + 3);
-      make_tmap(&c->ytm[1][b], c->B[b], g, 40, 32 + 2);
+      make_tmap(&c->ytm[0][b], c->E[b], g, kYeeTX + 8, kYeeTY + 3);
+      make_tmap(&c->ytm[1][b], c->B[b], g, kYeeTX + 8, kYeeTY + 2);
     }
-    make_tmap(&c->ytmJ[0], c->J, g, 36, 32 + 1);
-    if (c->Jf) make_tmap(&c->ytmJ[1], c->Jf, g, 36, 32 + 1);
+    make_tmap(&c->ytmJ[0], c->J, g, kYeeTX + 4, kYeeTY + 1);
+    if (c->Jf) make_tmap(&c->ytmJ[1], c->Jf, g, kYeeTX + 4, kYeeTY + 1);
     if (c->opt.filter_passes < 0 || c->opt.filter_passes > 64) throw Fail{ZPIC_E_INVALID, "filter_passes must be in [0, 64]"};
     if (c->opt.current_mode != 0 && c->opt.current_mode != 1) throw Fail{ZPIC_E_INVALID, "current_mode must be 0 or 1"};
     const int WJ = c->T + 3;
@@ -1094,7 +1094,7 @@ void step_phase_b(zpic_ctx* c, StepState& s) {
   y.fe_scale = 0.5 * c->dx * c->dy;
   int yee_done_to = 0;   // tile rows [1, yee_done_to) already advanced (round 1 overlap)
   if (s.r1_async) {
-    const int hi = (c->g.ny - 2) / 32;   // rows r < hi: J rows [32 r, 32 r + 32] avoid ny - 1, ny
+    const int hi = (c->g.ny - 2) / kYeeTY;   // tile rows r < hi: J rows [TY r, TY r + TY] avoid ny - 1, ny
     if (hi > 1) {
       ProfScope ps(c, K_YEE);
       launch_yee(y, c->stream, 1, hi);

@@ -17,6 +17,8 @@ constexpr int kXOff = 4;          // interior column 0 sits at column 4 of a pad
 constexpr int kEnergySlots = 256; // fp64 partial-sum slots (spread the atomics), per quantity
 constexpr int kBlock = 256;       // threads per CTA of the particle kernels
 constexpr int kSMin = 22;         // smallest tile scale exponent of the one-word int32 current
+constexpr int kYeeTX = 32;        // K5 tile: columns
+constexpr int kYeeTY = 32;        // K5 tile: rows
 
 // A guard-extended field grid: 3 planes of `rows` x `pitch` floats; interior cell (i, j) of a
 // plane is at (j + 1) * pitch + (i + kXOff), valid for -1 <= i <= nx + 1, -1 <= j <= ny + 1

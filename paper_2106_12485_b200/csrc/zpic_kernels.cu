@@ -330,14 +330,14 @@ struct RowCol {
   }
 };
 
-constexpr int kYeeT = 32;
-// K5's staged boxes (TMA, one elected thread, mbarrier completion): E on local rows [-1, T+2)
-// and B on [-1, T+1), both from column -4 (the 16-byte aligned padded column i0; TMA faults on an
-// unaligned start) and 40 wide; J on rows [0, T+1) from column 0, 36 wide.  Outside the
+// K5 tile TX x TY.  Its staged boxes (TMA, one elected thread, mbarrier completion): E on local
+// rows [-1, TY+2) and B on [-1, TY+1), both from column -4 (the 16-byte aligned padded column i0;
+// TMA faults on an unaligned start) and TX + 8 wide; J on rows [0, TY+1) from column 0, TX + 4
+// wide.  Outside the
 // guard-extended grid the boxes read zero (out-of-bounds rows; the padding columns are zero).
 struct YeeBox {
-  static constexpr int T = kYeeT;
-  static constexpr int XE = 40, YE = T + 3, XB = 40, YB = T + 2, XJ = 36, YJ = T + 1;
+  static constexpr int TX = kYeeTX, TY = kYeeTY;
+  static constexpr int XE = TX + 8, YE = TY + 3, XB = TX + 8, YB = TY + 2, XJ = TX + 4, YJ = TY + 1;
   static constexpr int E = 3 * YE * XE, B = 3 * YB * XB, J = 3 * YJ * XJ;   // floats
   static constexpr int OB = (E + 31) & ~31, OJ = OB + ((B + 31) & ~31);       // 128-byte aligned boxes
   static constexpr size_t bytes = (size_t)(OJ + J) * 4;
@@ -350,17 +350,17 @@ __device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map
 }
 
 __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParams p) {
-  constexpr int T = kYeeT;
+  constexpr int TX = kYeeTX, TY = kYeeTY, TM = (TX > TY ? TX : TY) + 1;
   constexpr int WE = YeeBox::XE, WB = YeeBox::XB, WJ = YeeBox::XJ;   // row widths of the staged boxes
   extern __shared__ __align__(128) float yee_smem[];
   float (*sE)[YeeBox::YE * YeeBox::XE] = reinterpret_cast<float (*)[YeeBox::YE * YeeBox::XE]>(yee_smem);
   float (*sB)[YeeBox::YB * YeeBox::XB] = reinterpret_cast<float (*)[YeeBox::YB * YeeBox::XB]>(yee_smem + YeeBox::OB);
   float (*sJ)[YeeBox::YJ * YeeBox::XJ] = reinterpret_cast<float (*)[YeeBox::YJ * YeeBox::XJ]>(yee_smem + YeeBox::OJ);
-  __shared__ float s_mur[4][2][2][T + 1];  // E^n on Mur node lines: [edge][component][b, b'][index]
+  __shared__ float s_mur[4][2][2][TM];  // E^n on Mur node lines: [edge][component][b, b'][index]
   __shared__ __align__(8) unsigned long long s_bar;
   const GridDesc& g = p.g;
-  const int i0 = blockIdx.x * T, j0 = (blockIdx.y + p.row0) * T;
-  const int tw = min(T, g.nx - i0), th = min(T, g.ny - j0);
+  const int i0 = blockIdx.x * TX, j0 = (blockIdx.y + p.row0) * TY;
+  const int tw = min(TX, g.nx - i0), th = min(TY, g.ny - j0);
   const long pl = g.plane;
   // y edges of this slab that are domain edges (with a slab decomposition the others are
   // interfaces whose guards come from the neighbour)
@@ -391,17 +391,17 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
 #define JI(lx, ly) ((ly) * WJ + (lx))
   // FE(n) = 1/2 dx dy sum(E^2 + B^2) over this tile's interior cells
   float fe = 0.f;
-  for (int k = threadIdx.x; k < T * T; k += kBlock) {
-    const int lx = k % T, ly = k / T;
+  for (int k = threadIdx.x; k < TX * TY; k += kBlock) {
+    const int lx = k % TX, ly = k / TX;
     if (lx < tw && ly < th) {
       const int e = EI(lx, ly), b = BI(lx, ly);
 #pragma unroll
       for (int c = 0; c < 3; ++c) fe += sE[c][e] * sE[c][e] + sB[c][b] * sB[c][b];
     }
   }
-  // B^{n+1/2} on [-1, T]^2
-  RowCol<T + 2> rcb(threadIdx.x);
-  for (int k = threadIdx.x; k < (T + 2) * (T + 2); k += kBlock, rcb.next()) {
+  // B^{n+1/2} on [-1, TX] x [-1, TY]
+  RowCol<TX + 2> rcb(threadIdx.x);
+  for (int k = threadIdx.x; k < (TX + 2) * (TY + 2); k += kBlock, rcb.next()) {
     const int lx = rcb.c - 1, ly = rcb.r - 1;
     const int bk = BI(lx, ly);
     const int gi = i0 + lx, gj = j0 + ly;
@@ -413,8 +413,8 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
     sB[2][bk] += p.hdy * (sE[0][EI(lx, ly + 1)] - sE[0][EI(lx, ly)]) - p.hdx * (sE[1][EI(lx + 1, ly)] - sE[1][EI(lx, ly)]);
   }
   if (p.bcx == ZPIC_BC_OPEN || p.bcy == ZPIC_BC_OPEN) {   // save E^n on the Mur node lines
-    for (int k = threadIdx.x; k < 4 * 2 * 2 * (T + 1); k += kBlock) {
-      const int idx = k % (T + 1), node = (k / (T + 1)) % 2, comp = (k / (2 * (T + 1))) % 2, edge = k / (4 * (T + 1));
+    for (int k = threadIdx.x; k < 4 * 2 * 2 * TM; k += kBlock) {
+      const int idx = k % TM, node = (k / TM) % 2, comp = (k / (2 * TM)) % 2, edge = k / (4 * TM);
       float v = 0.f;
       if (edge < 2 && p.bcx == ZPIC_BC_OPEN && idx <= th) {
         const int bn = edge ? tw : 0, bp = edge ? tw - 1 : 1;
@@ -427,9 +427,9 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
     }
   }
   __syncthreads();
-  // E^{n+1} on [0, T]^2
-  RowCol<T + 1> rcj(threadIdx.x);
-  for (int k = threadIdx.x; k < (T + 1) * (T + 1); k += kBlock, rcj.next()) {
+  // E^{n+1} on [0, TX] x [0, TY]
+  RowCol<TX + 1> rcj(threadIdx.x);
+  for (int k = threadIdx.x; k < (TX + 1) * (TY + 1); k += kBlock, rcj.next()) {
     const int lx = rcj.c, ly = rcj.r;
     const int jk = JI(lx, ly);
     const int e = EI(lx, ly), b = BI(lx, ly);
@@ -475,9 +475,9 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
     }
   }
   __syncthreads();
-  // B^{n+1} on [0, T)^2 and the stores
-  for (int k = threadIdx.x; k < T * T; k += kBlock) {
-    const int lx = k % T, ly = k / T;
+  // B^{n+1} on [0, TX) x [0, TY) and the stores
+  for (int k = threadIdx.x; k < TX * TY; k += kBlock) {
+    const int lx = k % TX, ly = k / TX;
     if (lx >= tw || ly >= th) continue;
     const int e = EI(lx, ly), b = BI(lx, ly);
     const float ez = sE[2][e];
@@ -965,15 +965,15 @@ void launch_yee(const YeeParams& p, cudaStream_t st, int row_begin, int row_end)
     cudaFuncSetAttribute(k_yee, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)YeeBox::bytes);
     if (dev < 32) attr_set |= 1u << dev;
   }
-  const int nty = (p.g.ny + kYeeT - 1) / kYeeT;
+  const int nty = (p.g.ny + kYeeTY - 1) / kYeeTY;
   if (row_end < 0 || row_end > nty) row_end = nty;
   if (row_end <= row_begin) return;
   YeeParams q = p;
   q.row0 = row_begin;
-  dim3 grid((p.g.nx + kYeeT - 1) / kYeeT, row_end - row_begin);
+  dim3 grid((p.g.nx + kYeeTX - 1) / kYeeTX, row_end - row_begin);
   k_yee<<<grid, kBlock, YeeBox::bytes, st>>>(q);
 }
-int yee_tile_rows(const GridDesc& g) { return (g.ny + kYeeT - 1) / kYeeT; }
+int yee_tile_rows(const GridDesc& g) { return (g.ny + kYeeTY - 1) / kYeeTY; }
 void launch_epilogue(double* ke_slots, double* fe_slots, double* energy, int nspecies, const double* ke_scale4,
                      int* mc, int* sic, int* soc, int* stats, int64_t* d_nmove, int shifted, cudaStream_t st) {
   k_epilogue<<<1, kBlock, 0, st>>>(ke_slots, fe_slots, energy, nspecies, ke_scale4, mc, sic, soc, stats, d_nmove,
