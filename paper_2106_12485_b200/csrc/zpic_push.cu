@@ -215,7 +215,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         if (has_id) nid = __ldcs(qn_ + F_ID * 32);
       }
       bool cross = false, stay = false, move = false;
-      int ix = 0, iy = 0, lx = 0, ly = 0, mdir = -1;
+      int mdir = -1;
+      // set on valid lanes only; read only under cross / stay / move, which are false elsewhere
+      // (no initialisers: no per-chunk register zeroing)
+      int ix, iy, lx, ly;
       float x0 = 0.f, y0 = 0.f, dxp = 0.f, dyp = 0.f, qvz = 0.f;
       if (valid) {
         ix = cell_ix(cell); iy = cell_iy(cell);
