@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
   float (*sB)[YeeBox::YB * YeeBox::XB] = reinterpret_cast<float (*)[YeeBox::YB * YeeBox::XB]>(yee_smem + YeeBox::OB);
   float (*sJ)[YeeBox::YJ * YeeBox::XJ] = reinterpret_cast<float (*)[YeeBox::YJ * YeeBox::XJ]>(yee_smem + YeeBox::OJ);
   __shared__ float s_mur[4][2][2][TM];  // E^n on Mur node lines: [edge][component][b, b'][index]
-  __shared__ __align__(8) unsigned long long s_bar;
+  __shared__ __align__(8) unsigned long long s_bar[2];   // [0] the E and B boxes, [1] the J box
   const GridDesc& g = p.g;
   const int i0 = blockIdx.x * TX, j0 = (blockIdx.y + p.row0) * TY;
   const int tw = min(TX, g.nx - i0), th = min(TY, g.ny - j0);
@@ -366,18 +366,20 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
   // interfaces whose guards come from the neighbour)
   const bool ylo_dom = p.bcy != ZPIC_BC_PERIODIC && p.ylo_edge, yhi_dom = p.bcy != ZPIC_BC_PERIODIC && p.yhi_edge;
 
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar[0]);
+  const unsigned barj = (unsigned)__cvta_generic_to_shared(&s_bar[1]);
   {
-    const unsigned bar = (unsigned)__cvta_generic_to_shared(&s_bar);
     if (threadIdx.x == 0) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(barj) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar),
-                   "r"((YeeBox::E + YeeBox::B + YeeBox::J) * 4)   // the bytes the three boxes deliver
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((YeeBox::E + YeeBox::B) * 4)
                    : "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(barj), "r"(YeeBox::J * 4) : "memory");
       // padded column of local cell -4 is i0 (kXOff = 4); padded row of local row r is j0 + r + 1
       tma_load_3d((unsigned)__cvta_generic_to_shared(&sE[0][0]), &p.tmE, i0, j0, bar);
       tma_load_3d((unsigned)__cvta_generic_to_shared(&sB[0][0]), &p.tmB, i0, j0, bar);
-      tma_load_3d((unsigned)__cvta_generic_to_shared(&sJ[0][0]), &p.tmJ, i0 + kXOff, j0 + 1, bar);
+      tma_load_3d((unsigned)__cvta_generic_to_shared(&sJ[0][0]), &p.tmJ, i0 + kXOff, j0 + 1, barj);
     }
     __syncthreads();
     asm volatile(
@@ -427,6 +429,11 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
     }
   }
   __syncthreads();
+  // the J box (its own barrier: its transfer overlaps the B half step)
+  asm volatile(
+      "{\n .reg .pred done;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n"
+      " @!done bra WAIT_%=;\n}" ::"r"(barj)
+      : "memory");
   // E^{n+1} on [0, TX] x [0, TY]
   RowCol<TX + 1> rcj(threadIdx.x);
   for (int k = threadIdx.x; k < (TX + 1) * (TY + 1); k += kBlock, rcj.next()) {
