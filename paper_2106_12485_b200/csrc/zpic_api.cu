@@ -51,6 +51,8 @@ void launch_apply_j_halo(float* J, const GridDesc& g, const float* rup, const fl
 size_t particle_msg_bytes(int cap);
 PList particle_msg_list(void* buf, int cap);
 void launch_recv_insert(const PushParams& p, const PList& lo, const PList& hi, cudaStream_t st);
+void launch_sort_tiles(const PStore& src, uint32_t* dst, int T, int ntx, int ntiles, cudaStream_t st);
+int sort_max_cap();
 }  // namespace zpic
 
 using namespace zpic;
@@ -176,6 +178,7 @@ void check_tile_capacity(zpic_ctx* c) {
 void free_store(zpic_ctx* c, int s) {
   PStore& ps = c->ps[s];
   dev_free(c, ps.data); dev_free(c, ps.cnt);
+  if (c->sort_buf[s]) { dev_free(c, c->sort_buf[s]); c->sort_buf[s] = nullptr; }
   ps = PStore{};
   dev_free(c, c->mail[s].data); dev_free(c, c->mail[s].cnt);
   c->mail[s] = MailBox{};
@@ -231,11 +234,13 @@ void refresh_field_guards(zpic_ctx* c, float* F, bool is_E) {
 }
 
 // ---- profiling ---------------------------------------------------------------------------
+constexpr int kSortEveryDefault = 0;   // steps between K2s re-sorts (ZPIC_SORT_EVERY overrides; 0 = off)
 enum KId { K_PUSH = 0, K_INSERT, K_ASSEMBLE, K_LOOSE, K_FOLD, K_HALO, K_FILTER, K_YEE, K_WINDOW, K_EPI, K_EXCHANGE,
-           K_MAIL, K_COUNT };
+           K_MAIL, K_SORT, K_COUNT };
 const char* kNames[K_COUNT] = {"k_push_tiles", "k_insert",        "k_assemble_j", "k_push_loose",
                                "k_guard_fold", "k_apply_halo",    "k_filter_x",   "k_yee",
-                               "k_inject_column", "k_epilogue",   "halo_exchange", "k_mail_gather"};
+                               "k_inject_column", "k_epilogue",   "halo_exchange", "k_mail_gather",
+                               "k_sort_tiles"};
 
 struct ProfScope {
   zpic_ctx* c;
@@ -513,6 +518,10 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     if (c->opt.stream) { c->stream = (cudaStream_t)c->opt.stream; c->own_stream = false; }
     else { CUDA_OR_THROW(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking)); c->own_stream = true; }
     c->prof = c->opt.profile != 0;
+    {
+      const char* e = getenv("ZPIC_SORT_EVERY");   // read per context
+      c->sort_every = e ? atoi(e) : kSortEveryDefault;
+    }
     c->prof_ms.assign(K_COUNT, 0.0);
     c->prof_count.assign(K_COUNT, 0);
     if (dist) c->dist = *dist; else c->dist = zpic_dist{0, 1, nullptr, 0, nullptr, ZPIC_TRANSPORT_NCCL};
@@ -884,6 +893,28 @@ static void maybe_repack(zpic_ctx* c) {
 
 static void maybe_repack_now(zpic_ctx* c);
 
+// K2s every sort_every steps (ZPIC_SORT_EVERY; 0 = never): each species' tiles re-sorted into a
+// second store of the same shape, which then becomes the store (the graphs hold the old pointer:
+// they are dropped and re-captured).
+static void maybe_sort(zpic_ctx* c) {
+  if (c->sort_every <= 0 || c->steps - c->last_sort < c->sort_every) return;
+  c->last_sort = c->steps;
+  for (int s = 0; s < c->nspecies; ++s) {
+    PStore& ps = c->ps[s];
+    if (ps.cap > sort_max_cap() || !ps.data) continue;
+    if (!c->sort_buf[s]) c->sort_buf[s] = (uint32_t*)dev_alloc(c, (size_t)ps.cap * c->ntiles * ps.nf * sizeof(uint32_t));
+    {
+      ProfScope pr(c, K_SORT);
+      launch_sort_tiles(ps, c->sort_buf[s], c->T, c->ntx, c->ntiles, c->stream);
+      CUDA_OR_THROW(cudaGetLastError());
+    }
+    c->launches += 1;
+    std::swap(ps.data, c->sort_buf[s]);
+  }
+  c->sorts += 1;
+  drop_graphs(c);
+}
+
 // Chunked direct load: when the species' tile store already has room for n particles on average
 // (it was sized for the species' lattice at zpic_init), the host arrays are copied in chunks into
 // two device staging buffers on a copy stream while the compute stream bins the previous chunk
@@ -1251,6 +1282,7 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
     try {
       for (int k = 0; k < n; ++k) {
         maybe_repack(c);
+        maybe_sort(c);
         const int shift = window_shifts(c) ? 1 : 0;
         const int par = c->steps & 1;
         CUDA_OR_THROW(cudaGraphLaunch(one_step_graph(c, shift), c->stream));
@@ -1271,12 +1303,13 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
       int k = 0;
       for (; k + 2 <= n; k += 2) {
         maybe_repack(c);
+        maybe_sort(c);
         CUDA_OR_THROW(cudaGraphLaunch(two_step_graph(c), c->stream));
         c->steps += 2;
         c->since_check += 2;
         c->launches += c->graph_launches;
       }
-      if (k < n) { maybe_repack(c); run_step(c); }
+      if (k < n) { maybe_repack(c); maybe_sort(c); run_step(c); }
     } catch (const Fail& f) {
       c->last_error = f.msg;
       return f.st;
@@ -1295,6 +1328,7 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
     }
     for (int k = 0; k < n; ++k) {
       maybe_repack(c);
+      maybe_sort(c);
       StepState s = step_phase_a(c);
       if (c->slab) {
         ncclResult_t r;

@@ -215,6 +215,124 @@ __global__ void __launch_bounds__(kBlock) k_assemble_j(float* __restrict__ J, co
 }
 
 // =============================================================================================
+// K2s: periodic in-tile particle re-sort, out of place into `dst` (same layout).  K1 writes a
+// particle back into its own slot, so a warp's 32 slots, which the injection fills with 32
+// consecutive cells, drift towards random cells as particles cross edges and holes are refilled:
+// the shared-memory gather and current atomics of K1 then hit ~2.5x more bank conflicts
+// ("order decay").  The re-sort restores the injection order: rank-major,
+// cell-minor (the first particle of every cell in cell order, then the second, ...), computed
+// as the rank of a unique key = rank_in_cell * T^2 + cell in a bitmap (ranks past the bitmap go
+// to the end in arbitrary order).  One CTA per tile; writes are coalesced, reads are in-tile
+// gathers (L1 / L2).
+constexpr int kSortBlock = 256;
+// key bitmap bits: ranks below kSortBits / T^2 are placed exactly (64 per cell at T = 16, 512 at
+// T = 8), the rest go to the end in arbitrary order
+template <int T>
+constexpr int kSortBits = T == 16 ? 16384 : 32768;
+template <int T>
+__global__ void __launch_bounds__(kSortBlock) k_sort_tiles(PStore src, uint32_t* __restrict__ dst, int ntx) {
+  constexpr int NC = T * T, RMAX = kSortBits<T> / NC, NW = kSortBits<T> / 32;
+  extern __shared__ __align__(16) int sort_smem[];
+  __shared__ int s_cnt[NC];
+  __shared__ unsigned s_bits[NW];
+  __shared__ int s_pre[NW];
+  __shared__ int s_wsum[kSortBlock / 32];
+  __shared__ int s_ovf;
+  const int t = blockIdx.x;
+  const int n = min(src.cnt[t], src.cap);
+  int* keys = sort_smem;                                                   // [cap]
+  unsigned short* sidx = reinterpret_cast<unsigned short*>(sort_smem + src.cap);   // [cap]
+  const int i0 = (t % ntx) * T, j0 = (t / ntx) * T;
+  const long base = (long)t * src.cap;
+  // word offsets inside the tile's segment (32-bit): slot i, field f at (i / 32) * 32 nf + 32 f + i % 32;
+  // a thread's slots i = tid + 256 k advance by 256 nf words
+  const int nf = src.nf, wstep = kSortBlock * nf;
+  const int off0 = (threadIdx.x >> 5) * 32 * nf + (threadIdx.x & 31);
+  const uint32_t* tsrc = src.data + (base >> 5) * (32L * nf);
+  uint32_t* tdst = dst + (base >> 5) * (32L * nf);
+  for (int k = threadIdx.x; k < NC; k += kSortBlock) s_cnt[k] = 0;
+  for (int k = threadIdx.x; k < NW; k += kSortBlock) s_bits[k] = 0u;
+  if (threadIdx.x == 0) s_ovf = 0;
+  __syncthreads();
+  int off = off0 + F_CELL * 32;
+#pragma unroll 4
+  for (int i = threadIdx.x; i < n; i += kSortBlock, off += wstep) {
+    const int cell = (int)__ldg(tsrc + off);
+    const int lc = (cell_ix(cell) - i0) + (cell_iy(cell) - j0) * T;
+    const int r = atomicAdd(&s_cnt[lc], 1);
+    const int key = r < RMAX ? r * NC + lc : -1;
+    if (key >= 0) atomicOr(&s_bits[key >> 5], 1u << (key & 31));
+    keys[i] = key;
+  }
+  __syncthreads();
+  // exclusive prefix of the bitmap's popcounts (NW words, NW / kSortBlock per thread)
+  constexpr int PER = NW / kSortBlock;
+  int loc[PER], sum = 0;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) {
+    loc[q] = sum;
+    sum += __popc(s_bits[threadIdx.x * PER + q]);
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = sum;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) s_wsum[warp] = incl;
+  __syncthreads();
+  int wbase = 0, nk = 0;
+  for (int w = 0; w < kSortBlock / 32; ++w) {
+    wbase += w < warp ? s_wsum[w] : 0;
+    nk += s_wsum[w];
+  }
+  const int excl = wbase + incl - sum;
+#pragma unroll
+  for (int q = 0; q < PER; ++q) s_pre[threadIdx.x * PER + q] = excl + loc[q];
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += kSortBlock) {
+    const int key = keys[i];
+    const int slot = key >= 0 ? s_pre[key >> 5] + __popc(s_bits[key >> 5] & ((1u << (key & 31)) - 1u))
+                              : nk + atomicAdd(&s_ovf, 1);
+    sidx[slot] = (unsigned short)i;
+  }
+  // the permutation, one field at a time through shared memory (the key array's bytes): coalesced
+  // loads of field f in slot order, coalesced stores in sorted order, the gather in shared memory
+  uint32_t* buf = reinterpret_cast<uint32_t*>(keys);
+  for (int f = 0; f < nf; ++f) {
+    __syncthreads();   // the slots (first pass) or the previous field are consumed
+    int o = off0 + f * 32;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < n; i += kSortBlock, o += wstep) buf[i] = __ldcs(tsrc + o);
+    __syncthreads();
+    o = off0 + f * 32;
+#pragma unroll 4
+    for (int k = threadIdx.x; k < n; k += kSortBlock, o += wstep) __stcs(tdst + o, buf[sidx[k]]);
+  }
+}
+
+void launch_sort_tiles(const PStore& src, uint32_t* dst, int T, int ntx, int ntiles, cudaStream_t st) {
+  const size_t smem = (size_t)src.cap * 6;
+  switch (T) {
+    case 8:
+      cudaFuncSetAttribute(k_sort_tiles<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_sort_tiles<8><<<ntiles, kSortBlock, smem, st>>>(src, dst, ntx);
+      break;
+    case 16:
+      cudaFuncSetAttribute(k_sort_tiles<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_sort_tiles<16><<<ntiles, kSortBlock, smem, st>>>(src, dst, ntx);
+      break;
+    case 32:
+      cudaFuncSetAttribute(k_sort_tiles<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      k_sort_tiles<32><<<ntiles, kSortBlock, smem, st>>>(src, dst, ntx);
+      break;
+  }
+}
+// the largest tile capacity the re-sort handles (16-bit slot indices, shared memory)
+int sort_max_cap() { return 30000; }
+
+// =============================================================================================
 // K1L: loose particles (those that found no tile slack): global-memory gather, global atomics
 // into the assembled J grid (guard-extended, folded afterwards), then re-insertion.
 __global__ void __launch_bounds__(kBlock) k_push_loose(PushParams p) {
