@@ -162,6 +162,11 @@ def run_reference(args, world, rank):
         return
     import synth
     from oracle.sim import from_config
+    # bound the run to a few minutes: ~3 s per oracle step on a 1024^2 patch, so past 50 steps the
+    # patch shrinks with the step count (a multiple of 64 cells per side)
+    tot = max(1, args.steps + args.warmup)
+    if tot > 50:
+        args.cpu_cells = max(64, int(args.cpu_cells * (50.0 / tot) ** 0.5) // 64 * 64)
     cfg = synth.config(args.config, nx=args.cpu_cells, ny=args.cpu_cells)
     sim = from_config(cfg)
     n = sum(len(s["ix"]) for s in sim.species)
