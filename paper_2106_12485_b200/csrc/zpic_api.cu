@@ -51,8 +51,7 @@ void launch_apply_j_halo(float* J, const GridDesc& g, const float* rup, const fl
 size_t particle_msg_bytes(int cap);
 PList particle_msg_list(void* buf, int cap);
 void launch_recv_insert(const PushParams& p, const PList& lo, const PList& hi, cudaStream_t st);
-void launch_sort_tiles(const PStore& src, uint32_t* dst, int T, int ntx, int ntiles, cudaStream_t st);
-int sort_max_cap();
+void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, cudaStream_t st);
 }  // namespace zpic
 
 using namespace zpic;
@@ -178,7 +177,6 @@ void check_tile_capacity(zpic_ctx* c) {
 void free_store(zpic_ctx* c, int s) {
   PStore& ps = c->ps[s];
   dev_free(c, ps.data); dev_free(c, ps.cnt);
-  if (c->sort_buf[s]) { dev_free(c, c->sort_buf[s]); c->sort_buf[s] = nullptr; }
   ps = PStore{};
   dev_free(c, c->mail[s].data); dev_free(c, c->mail[s].cnt);
   c->mail[s] = MailBox{};
@@ -893,26 +891,19 @@ static void maybe_repack(zpic_ctx* c) {
 
 static void maybe_repack_now(zpic_ctx* c);
 
-// K2s every sort_every steps (ZPIC_SORT_EVERY; 0 = never): each species' tiles re-sorted into a
-// second store of the same shape, which then becomes the store (the graphs hold the old pointer:
-// they are dropped and re-captured).
+// K2s every sort_every steps (ZPIC_SORT_EVERY; 0 = never): each species' tiles re-sorted in
+// place (the store pointer does not change: the captured graphs stay valid).
 static void maybe_sort(zpic_ctx* c) {
   if (c->sort_every <= 0 || c->steps - c->last_sort < c->sort_every) return;
   c->last_sort = c->steps;
   for (int s = 0; s < c->nspecies; ++s) {
-    PStore& ps = c->ps[s];
-    if (ps.cap > sort_max_cap() || !ps.data) continue;
-    if (!c->sort_buf[s]) c->sort_buf[s] = (uint32_t*)dev_alloc(c, (size_t)ps.cap * c->ntiles * ps.nf * sizeof(uint32_t));
-    {
-      ProfScope pr(c, K_SORT);
-      launch_sort_tiles(ps, c->sort_buf[s], c->T, c->ntx, c->ntiles, c->stream);
-      CUDA_OR_THROW(cudaGetLastError());
-    }
+    if (!c->ps[s].data) continue;
+    ProfScope pr(c, K_SORT);
+    launch_sort_tiles(c->ps[s], c->T, c->ntx, c->ntiles, c->stream);
+    CUDA_OR_THROW(cudaGetLastError());
     c->launches += 1;
-    std::swap(ps.data, c->sort_buf[s]);
   }
   c->sorts += 1;
-  drop_graphs(c);
 }
 
 // Chunked direct load: when the species' tile store already has room for n particles on average

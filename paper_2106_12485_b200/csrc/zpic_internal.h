@@ -210,11 +210,10 @@ struct zpic_ctx {
   cudaGraphExec_t graph1[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // one step, [parity][shift]
   int graph1_launches[2][2] = {{0, 0}, {0, 0}};
   int64_t* d_nmove = nullptr;   // the window shift count on the device (column injection ids)
-  // periodic in-tile re-sort (K2s): every sort_every steps into the second store, then swapped
+  // periodic in-tile re-sort (K2s, in place) every sort_every steps
   int sort_every = 0;
   int64_t last_sort = 0;
   int64_t sorts = 0;
-  uint32_t* sort_buf[zpic::kMaxSpecies] = {nullptr, nullptr, nullptr, nullptr};
   // profiling
   bool prof;
   std::vector<std::string> prof_names;

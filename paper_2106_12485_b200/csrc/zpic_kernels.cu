@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "zpic_device.cuh"
 
 namespace zpic {
@@ -215,63 +217,85 @@ __global__ void __launch_bounds__(kBlock) k_assemble_j(float* __restrict__ J, co
 }
 
 // =============================================================================================
-// K2s: periodic in-tile particle re-sort, out of place into `dst` (same layout).  K1 writes a
-// particle back into its own slot, so a warp's 32 slots, which the injection fills with 32
-// consecutive cells, drift towards random cells as particles cross edges and holes are refilled:
-// the shared-memory gather and current atomics of K1 then hit ~2.5x more bank conflicts
-// ("order decay").  The re-sort restores the injection order: rank-major,
-// cell-minor (the first particle of every cell in cell order, then the second, ...), computed
-// as the rank of a unique key = rank_in_cell * T^2 + cell in a bitmap (ranks past the bitmap go
-// to the end in arbitrary order).  One CTA per tile; writes are coalesced, reads are in-tile
-// gathers (L1 / L2).
-constexpr int kSortBlock = 256;
-// key bitmap bits: ranks below kSortBits / T^2 are placed exactly (64 per cell at T = 16, 512 at
-// T = 8), the rest go to the end in arbitrary order
+// K2s: periodic in-tile particle re-sort, in place.  K1 writes a particle back into its own slot,
+// so a warp's 32 slots, which the injection fills with 32 consecutive cells, drift towards random
+// cells as particles cross edges and holes are refilled: the shared-memory gather and current
+// atomics of K1 then hit ~2.5x more bank conflicts ("order decay").  The re-sort
+// restores the injection order: rank-major, cell-minor (the first particle of every cell in cell
+// order, then the second, ...), i.e. the rank of the unique key rank_in_cell * T^2 + cell in a
+// shared-memory bitmap (ranks past the bitmap go to the end in arbitrary order).  One CTA per
+// tile stages the tile's particles in shared memory (all loads in flight at once), then stores
+// them back in sorted order (coalesced).  The cell word is rebuilt from the local cell, so only
+// the other fields are staged; a tile with more than `nstage` particles is left as it is.
+constexpr int kSortBlock = 512;
+constexpr int kSortK = 9;   // particles per thread: nstage <= kSortBlock * kSortK
+// key bitmap bits: ranks below kSortBits / T^2 are placed exactly (64 per cell at T = 16)
 template <int T>
 constexpr int kSortBits = T == 16 ? 16384 : 32768;
 template <int T>
-__global__ void __launch_bounds__(kSortBlock) k_sort_tiles(PStore src, uint32_t* __restrict__ dst, int ntx) {
-  constexpr int NC = T * T, RMAX = kSortBits<T> / NC, NW = kSortBits<T> / 32;
-  extern __shared__ __align__(16) int sort_smem[];
+__global__ void __launch_bounds__(kSortBlock, 2) k_sort_tiles(PStore ps, int ntx, int nstage) {
+  constexpr int NC = T * T, RMAX = kSortBits<T> / NC, NW = kSortBits<T> / 32, PER = NW / kSortBlock > 0 ? NW / kSortBlock : 1;
+  extern __shared__ __align__(16) uint32_t sort_smem[];
   __shared__ int s_cnt[NC];
   __shared__ unsigned s_bits[NW];
   __shared__ int s_pre[NW];
   __shared__ int s_wsum[kSortBlock / 32];
   __shared__ int s_ovf;
   const int t = blockIdx.x;
-  const int n = min(src.cnt[t], src.cap);
-  int* keys = sort_smem;                                                   // [cap]
-  unsigned short* sidx = reinterpret_cast<unsigned short*>(sort_smem + src.cap);   // [cap]
+  const int n = min(ps.cnt[t], ps.cap);
+  if (n > nstage) return;   // CTA-uniform: this tile stays unsorted
+  const int nf = ps.nf;
+  uint32_t* stage = sort_smem;                                                        // [nf - 1][nstage]
+  unsigned short* sidx = reinterpret_cast<unsigned short*>(sort_smem + (nf - 1) * nstage);   // [nstage]
+  unsigned short* lcs = sidx + nstage;                                                // [nstage]
   const int i0 = (t % ntx) * T, j0 = (t / ntx) * T;
-  const long base = (long)t * src.cap;
-  // word offsets inside the tile's segment (32-bit): slot i, field f at (i / 32) * 32 nf + 32 f + i % 32;
-  // a thread's slots i = tid + 256 k advance by 256 nf words
-  const int nf = src.nf, wstep = kSortBlock * nf;
-  const int off0 = (threadIdx.x >> 5) * 32 * nf + (threadIdx.x & 31);
-  const uint32_t* tsrc = src.data + (base >> 5) * (32L * nf);
-  uint32_t* tdst = dst + (base >> 5) * (32L * nf);
+  uint32_t* seg = ps.data + ((long)t * ps.cap >> 5) * (32L * nf);   // the tile's segment (cap is a multiple of 32)
+  const int wstep = kSortBlock * nf;
+  const int off0 = (threadIdx.x >> 5) * 32 * nf + (threadIdx.x & 31);   // slot tid, field 0
   for (int k = threadIdx.x; k < NC; k += kSortBlock) s_cnt[k] = 0;
   for (int k = threadIdx.x; k < NW; k += kSortBlock) s_bits[k] = 0u;
   if (threadIdx.x == 0) s_ovf = 0;
   __syncthreads();
-  int off = off0 + F_CELL * 32;
-#pragma unroll 4
-  for (int i = threadIdx.x; i < n; i += kSortBlock, off += wstep) {
-    const int cell = (int)__ldg(tsrc + off);
-    const int lc = (cell_ix(cell) - i0) + (cell_iy(cell) - j0) * T;
-    const int r = atomicAdd(&s_cnt[lc], 1);
-    const int key = r < RMAX ? r * NC + lc : -1;
-    if (key >= 0) atomicOr(&s_bits[key >> 5], 1u << (key & 31));
-    keys[i] = key;
+  // 1. stage: the non-cell fields of this thread's slots go global -> shared with cp.async (no
+  // registers, every copy in flight at once); the cell words come to registers for the keys
+  int key[kSortK];
+  uint32_t cellv[kSortK];
+#pragma unroll
+  for (int q = 0; q < kSortK; ++q) {
+    const int i = threadIdx.x + q * kSortBlock;
+    cellv[q] = 0u;
+    if (i < n) {
+      const uint32_t* src = seg + off0 + q * wstep;
+      for (int f = 1; f < nf; ++f)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(stage + (f - 1) * nstage + i)), "l"(src + f * 32)
+                     : "memory");
+      cellv[q] = __ldcs(src + F_CELL * 32);
+    }
   }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll
+  for (int q = 0; q < kSortK; ++q) {
+    const int i = threadIdx.x + q * kSortBlock;
+    key[q] = -2;
+    if (i < n) {
+      const int cell = (int)cellv[q];
+      const int lc = (cell_ix(cell) - i0) + (cell_iy(cell) - j0) * T;
+      lcs[i] = (unsigned short)lc;
+      const int r = atomicAdd(&s_cnt[lc], 1);
+      key[q] = r < RMAX ? r * NC + lc : -1;
+      if (key[q] >= 0) atomicOr(&s_bits[key[q] >> 5], 1u << (key[q] & 31));
+    }
+  }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");   // this thread's copies landed (the barrier publishes them)
   __syncthreads();
-  // exclusive prefix of the bitmap's popcounts (NW words, NW / kSortBlock per thread)
-  constexpr int PER = NW / kSortBlock;
+  // 2. exclusive prefix of the bitmap's popcounts
   int loc[PER], sum = 0;
 #pragma unroll
   for (int q = 0; q < PER; ++q) {
+    const int w = threadIdx.x * PER + q;
     loc[q] = sum;
-    sum += __popc(s_bits[threadIdx.x * PER + q]);
+    sum += w < NW ? __popc(s_bits[w]) : 0;
   }
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int incl = sum;
@@ -289,48 +313,54 @@ __global__ void __launch_bounds__(kSortBlock) k_sort_tiles(PStore src, uint32_t*
   }
   const int excl = wbase + incl - sum;
 #pragma unroll
-  for (int q = 0; q < PER; ++q) s_pre[threadIdx.x * PER + q] = excl + loc[q];
+  for (int q = 0; q < PER; ++q)
+    if (threadIdx.x * PER + q < NW) s_pre[threadIdx.x * PER + q] = excl + loc[q];
   __syncthreads();
-  for (int i = threadIdx.x; i < n; i += kSortBlock) {
-    const int key = keys[i];
-    const int slot = key >= 0 ? s_pre[key >> 5] + __popc(s_bits[key >> 5] & ((1u << (key & 31)) - 1u))
-                              : nk + atomicAdd(&s_ovf, 1);
+  // 3. destination slot of every staged particle
+#pragma unroll
+  for (int q = 0; q < kSortK; ++q) {
+    const int i = threadIdx.x + q * kSortBlock, k = key[q];
+    if (k == -2) continue;
+    const int slot = k >= 0 ? s_pre[k >> 5] + __popc(s_bits[k >> 5] & ((1u << (k & 31)) - 1u)) : nk + atomicAdd(&s_ovf, 1);
     sidx[slot] = (unsigned short)i;
   }
-  // the permutation, one field at a time through shared memory (the key array's bytes): coalesced
-  // loads of field f in slot order, coalesced stores in sorted order, the gather in shared memory
-  uint32_t* buf = reinterpret_cast<uint32_t*>(keys);
-  for (int f = 0; f < nf; ++f) {
-    __syncthreads();   // the slots (first pass) or the previous field are consumed
-    int o = off0 + f * 32;
-#pragma unroll 4
-    for (int i = threadIdx.x; i < n; i += kSortBlock, o += wstep) buf[i] = __ldcs(tsrc + o);
-    __syncthreads();
-    o = off0 + f * 32;
-#pragma unroll 4
-    for (int k = threadIdx.x; k < n; k += kSortBlock, o += wstep) __stcs(tdst + o, buf[sidx[k]]);
+  __syncthreads();
+  // 4. store back in sorted order (coalesced); the cell word from the local cell
+#pragma unroll
+  for (int q = 0; q < kSortK; ++q) {
+    const int s = threadIdx.x + q * kSortBlock;
+    if (s < n) {
+      const int i = sidx[s], lc = lcs[i];
+      uint32_t* d = seg + off0 + q * wstep;
+      __stcs(d + F_CELL * 32, (uint32_t)pack_cell(i0 + lc % T, j0 + lc / T));
+      for (int f = 1; f < nf; ++f) __stcs(d + f * 32, stage[(f - 1) * nstage + i]);
+    }
   }
 }
 
-void launch_sort_tiles(const PStore& src, uint32_t* dst, int T, int ntx, int ntiles, cudaStream_t st) {
-  const size_t smem = (size_t)src.cap * 6;
+// particles of one tile the re-sort can stage (two CTAs per SM), 0 if it cannot run
+int sort_stage_capacity(int nf) {
+  const int per = 4 * (nf - 1) + 4;   // staged fields + slot index + local cell
+  return std::min(kSortBlock * kSortK, (int)((104 * 1024) / per) / 32 * 32);   // 2 x (dyn + static + 1 KB) <= 228 KB
+}
+void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, cudaStream_t st) {
+  const int nstage = sort_stage_capacity(ps.nf);
+  const size_t smem = (size_t)nstage * (4 * (ps.nf - 1) + 4);
   switch (T) {
     case 8:
       cudaFuncSetAttribute(k_sort_tiles<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_sort_tiles<8><<<ntiles, kSortBlock, smem, st>>>(src, dst, ntx);
+      k_sort_tiles<8><<<ntiles, kSortBlock, smem, st>>>(ps, ntx, nstage);
       break;
     case 16:
       cudaFuncSetAttribute(k_sort_tiles<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_sort_tiles<16><<<ntiles, kSortBlock, smem, st>>>(src, dst, ntx);
+      k_sort_tiles<16><<<ntiles, kSortBlock, smem, st>>>(ps, ntx, nstage);
       break;
     case 32:
       cudaFuncSetAttribute(k_sort_tiles<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_sort_tiles<32><<<ntiles, kSortBlock, smem, st>>>(src, dst, ntx);
+      k_sort_tiles<32><<<ntiles, kSortBlock, smem, st>>>(ps, ntx, nstage);
       break;
   }
 }
-// the largest tile capacity the re-sort handles (16-bit slot indices, shared memory)
-int sort_max_cap() { return 30000; }
 
 // =============================================================================================
 // K1L: loose particles (those that found no tile slack): global-memory gather, global atomics
