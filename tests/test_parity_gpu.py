@@ -535,8 +535,8 @@ def test_chunked_upload_validates_and_matches_direct_load():
     sim.close()
 
 
-@pytest.mark.parametrize("graphs", [False, True])
-def test_periodic_resort_is_invisible(graphs, monkeypatch):
+@pytest.mark.parametrize("graphs,tile", [(False, 16), (True, 16), (False, 8)])
+def test_periodic_resort_is_invisible(graphs, tile, monkeypatch):
     """K2s (the periodic in-tile re-sort) only permutes the slots of a tile: with a re-sort every
     step the fields (an exact integer current per tile) and every particle (by id) are
     bit-identical to a run without it, with and without CUDA-graph replay."""
@@ -547,7 +547,7 @@ def test_periodic_resort_is_invisible(graphs, monkeypatch):
     out = []
     for every in ("1", "0"):
         monkeypatch.setenv("ZPIC_SORT_EVERY", every)
-        g = _z().Simulation(cfg, inject=False, track_ids=True, tile=16, capacity_slack=1.5, graphs=graphs)
+        g = _z().Simulation(cfg, inject=False, track_ids=True, tile=tile, capacity_slack=1.5, graphs=graphs)
         for s, p in enumerate(parts):
             g.set_particles(s, p)
         g.step(5)
@@ -567,3 +567,35 @@ def test_periodic_resort_is_invisible(graphs, monkeypatch):
             assert np.array_equal(pa[s][k], pb[s][k]), (s, k)
     # KE is an fp32 sum in storage order: equal to fp32 accuracy
     assert ea[2][0] == pytest.approx(eb[2][0], rel=1e-6)
+
+
+def test_resort_rank_overflow_and_crowded_cells(monkeypatch):
+    """K2s with more particles in one cell than its key bitmap ranks (64 per cell at T = 16): the
+    extra ranks go to the end of the tile in arbitrary order.  A cold cluster of 200 particles in
+    one cell plus a thermal background; fields and particles (by id) bit-identical to no re-sort,
+    and every particle survives."""
+    cfg = synth.config("C1", nx=64, ny=64)
+    cfg["species"][0]["uth"] = (0.2, 0.2, 0.2)
+    bg = synth.species_particles(cfg, 0)
+    rng = np.random.default_rng(7)
+    k = 200
+    cl = {"ix": np.full(k, 37, np.int32), "iy": np.full(k, 21, np.int32),
+          "x": rng.random(k, dtype=np.float32), "y": rng.random(k, dtype=np.float32),
+          "ux": np.zeros(k, np.float32), "uy": np.zeros(k, np.float32), "uz": np.zeros(k, np.float32),
+          "id": (np.arange(k) + len(bg["x"])).astype(np.uint32)}
+    parts = {f: np.concatenate([bg[f], cl[f]]) for f in bg}
+    out = []
+    for every in ("1", "0"):
+        monkeypatch.setenv("ZPIC_SORT_EVERY", every)
+        g = _z().Simulation(cfg, inject=False, track_ids=True, tile=16, capacity_slack=1.5)
+        g.set_particles(0, parts)
+        g.step(6)
+        p = g.particles(0, True)
+        o = np.argsort(p["id"])
+        out.append(({f: v[o] for f, v in p.items()}, g.fields(0), g.fields(1)))
+        g.close()
+    (pa, Ea, Ba), (pb, Eb, Bb) = out
+    assert len(pa["id"]) == len(parts["x"]) and np.array_equal(pa["id"], np.sort(parts["id"]))
+    assert np.array_equal(Ea, Eb) and np.array_equal(Ba, Bb)
+    for f in pa:
+        assert np.array_equal(pa[f], pb[f]), f
