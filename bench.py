@@ -138,6 +138,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
+def host_info():
+    """The host the oracle ran on: logical CPUs and the CPU model."""
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
 def cpu_baseline(args):
     """The oracle, as it stands, on a bounded sample of the same workload: the C5 physics on a
     1024 x 1024-cell periodic patch (16 ppc, 16.8 M particles), `steps` steps, one host core."""
@@ -153,7 +167,7 @@ def cpu_baseline(args):
     return {"value": n * args.cpu_steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
             "sample": "%s physics on a %dx%d-cell periodic patch (%d particles), %d steps, fp64 serial oracle"
                       % (args.config, args.cpu_cells, args.cpu_cells, n, args.cpu_steps),
-            "seconds": dt}
+            "seconds": dt, **host_info()}
 
 
 def run_reference(args, world, rank):
@@ -316,12 +330,23 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(sim.torch_stream)
-    sim.step(args.steps)
+    step_ev = []
+    if args.graphs:
+        sim.step(args.steps)
+    else:   # one event per step (the same launches): per-step statistics beside the total
+        for _ in range(args.steps):
+            sim.step(1)
+            step_ev.append(torch.cuda.Event(enable_timing=True))
+            step_ev[-1].record(sim.torch_stream)
     e1.record(sim.torch_stream)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     ms = e0.elapsed_time(e1)
+    per_step, prev = [], e0
+    for ev in step_ev:
+        per_step.append(prev.elapsed_time(ev))
+        prev = ev
     clk = clocks.stop()
     sim.sync()
     kt = sim.kernel_times()
@@ -341,6 +366,7 @@ def main():
     k1_bytes = K1_BYTES_PER_PARTICLE * cnt["particles"] + K1_BYTES_PER_CELL * n_cells // max(world, 1)
     peak, peak_kind = measured_peaks()
     achieved = k1_bytes / k1_avg_s / 1e9 if k1_n else None
+    traffic = k1_traffic(args.config, cfg["nx"], cfg["ny"]) if world == 1 else None
     value = n_particles * args.steps / (ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -354,12 +380,20 @@ def main():
         "k1_pushes_per_s": cnt["particles"] / k1_avg_s if k1_n else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak if k1_n else None,
-                     "traffic": k1_traffic(args.config, cfg["nx"], cfg["ny"]) if world == 1 else None,
+                     "traffic": traffic,
+                     # the same time against the ncu DRAM bytes, and the nominal 8 TB/s
+                     "achieved_dram": traffic / k1_avg_s / 1e9 if (traffic and k1_n) else None,
+                     "frac_dram": traffic / k1_avg_s / 1e9 / peak if (traffic and k1_n) else None,
+                     "frac_nominal_8tbs": achieved / 8000.0 if k1_n else None,
                      "traffic_source": "profiles/r1_k1_traffic_c5.json (ncu dram__bytes_read+write, C5)",
                      "kernel": "k_push_tiles", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg_s * 1e3 if k1_n else None,
                      **({"note": "--graphs: CUDA-graph replay, no per-kernel events"} if args.graphs else {})},
         "kernel_ms_per_step": {k: v[0] / max(v[1], 1) for k, v in kt.items() if v[1]},
+        # per-step times (CUDA events between the steps, this rank): the first / last steps show the
+        # in-tile order decay
+        **({"step_ms": {"mean": statistics.mean(per_step), "std": statistics.pstdev(per_step), "min": min(per_step),
+                        "max": max(per_step), "first": per_step[0], "last": per_step[-1]}} if per_step else {}),
         "gpu_launches": launches,
         "cuda_graphs": bool(args.graphs),
         "clocks": clk,
