@@ -200,7 +200,8 @@ def run_reference(args, world, rank):
                                                                                            args.cpu_cells, n)},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": "%dx%d-cell periodic patch of %s, %d particles, %d steps"
-                                       % (args.cpu_cells, args.cpu_cells, args.config, n, args.steps)},
+                                       % (args.cpu_cells, args.cpu_cells, args.config, n, args.steps),
+                             **host_info()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
