@@ -126,6 +126,7 @@ class ClockSampler:
         os.unlink(self.f.name)
         sm = [float(r[1]) for r in rows if len(r) >= 9 and r[1].strip().replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if len(r) >= 9 and r[2].strip().replace(".", "").isdigit()]
+        pw = [float(r[3]) for r in rows if len(r) >= 9 and r[3].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
         for r in rows:
@@ -135,7 +136,8 @@ class ClockSampler:
                 if "Active" in r[5 + k] and "Not" not in r[5 + k]:
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+                "reasons": sorted(reasons), "samples": len(rows),
+                "power_w": statistics.median(pw) if pw else None}
 
 
 def host_info():
