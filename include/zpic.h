@@ -63,7 +63,10 @@ typedef struct {
 typedef enum {
   ZPIC_BC_PERIODIC = 0,
   ZPIC_BC_OPEN = 1,          /* particles removed at the edge; Mur-1 on tangential E (R13) */
-  ZPIC_BC_MOVING_WINDOW = 2  /* x only: window moves at c; fresh plasma injected (R14, R15) */
+  ZPIC_BC_MOVING_WINDOW = 2  /* x only: window moves at c; fresh plasma injected (R14, R15): the
+                                entering column gets the profile's density beyond the box, so a
+                                species must be uniform or a ramp ending inside the box (x1 <= nx dx);
+                                a slab profile is rejected at zpic_init (ZPIC_E_INVALID) */
 } zpic_bc;
 
 typedef struct {

@@ -36,6 +36,7 @@ class OracleSim:
         self.species = []
         for sp in species:
             s = {k: sp[k] for k in ("m_q", "n", "ppc", "ufl", "uth")}
+            s.update({k: sp[k] for k in ("profile", "x0", "x1") if k in sp})
             # per-particle charge q_s = sign(m_q) n_s / (ppc_x ppc_y)  (R8)
             s["q"] = (1.0 if sp["m_q"] > 0 else -1.0) * sp["n"] / (sp["ppc"][0] * sp["ppc"][1])
             for k in ("ix", "iy"):
@@ -129,11 +130,20 @@ class OracleSim:
         self.n_move += 1
 
     def _inject_column(self, si, s):
-        """Fresh plasma in column nx-1: the ppc sub-lattice at density n (the profile is uniform
-        beyond the ramp, which is the only region the window reaches in C4; R15).  Momenta from
-        the shared seeded generator (synth), keyed by id = 2^31 + (n_move*ny + iy)*ppc + l*ppc_x + k."""
+        """Fresh plasma in column nx-1 (R15): density = the species profile at the column's
+        absolute position x = (nx - 1 + n_move + 1) dx, i.e. beyond the initial box.  Readings
+        (DESIGN.md §2): a uniform profile gives n there; a ramp that ends inside the initial box
+        (x1 <= nx dx: C4, P-LWFA) gives n for every injected column; a slab profile, or a ramp
+        reaching past the box, is not a supported moving-window input (the library rejects it at
+        zpic_init).  Density n > 0 -> the ppc sub-lattice; n = 0 -> nothing.  Momenta from the
+        shared seeded generator (synth), keyed by id = 2^31 + (n_move*ny + iy)*ppc + l*ppc_x + k."""
         from synth.generate import momenta
         nx, ny = self.nx, self.ny
+        prof = s.get("profile", "uniform")
+        if prof == "slab" or (prof == "ramp" and s["x1"] > nx * self.dx):
+            raise ValueError("moving-window injection needs a uniform profile or a ramp inside the box (R15)")
+        if not s["n"] > 0:
+            return None
         px, py = s["ppc"]
         l, k = np.divmod(np.arange(px * py), px)
         iy = np.repeat(np.arange(ny), px * py)

@@ -306,7 +306,8 @@ void orc_filter_x(double* J, int nx, int ny, int bcx, int bcy, int n_pass, int c
  * right after the interior E update with saved E^n values:
  *   E^{n+1}_b = E^n_{b'} + k (E^{n+1}_{b'} - E^n_b),  k = (dt - d)/(dt + d),
  *   low edge b = 0, b' = 1; high edge b = n (first high guard), b' = n-1.
- * x edges act on (Ey, Ez) (curl update skipped at node 0), y edges on (Ex, Ez).
+ * x edges act on (Ey, Ez) (curl update skipped at node 0), y edges on (Ex, Ez).  A node on two
+ * open edges (Ez at the four corners) takes the y-edge Mur, from its y neighbour (R13 corner rule).
  * save: scratch of 4*(max(nx,ny)+3) doubles per component pair (caller-provided). */
 static void b_half(double* B, const double* E, int nx, int ny, double h, double dx, double dy) {
   for (int j = 0; j < ny; ++j)
@@ -370,7 +371,7 @@ void orc_yee_advance(double* E, double* B, const double* J, int nx, int ny, doub
     for (int k = 0; k < 2; ++k) {
       int c = (k == 0) ? 1 : 2;
       for (int j = 0; j < ny; ++j) {
-        if (c == 2 && bcy == BC_OPEN && j == 0) continue;  /* corner node: handled by y Mur */
+        if (c == 2 && bcy == BC_OPEN && j == 0) continue;  /* corner node: the y Mur below (R13) */
         E[fidx(nx, ny, c, 0, j)] = sxlo[(2 * k + 1) * L + j] + kx * (E[fidx(nx, ny, c, 1, j)] - sxlo[(2 * k + 0) * L + j]);
         E[fidx(nx, ny, c, nx, j)] = sxhi[(2 * k + 1) * L + j] + kx * (E[fidx(nx, ny, c, nx - 1, j)] - sxhi[(2 * k + 0) * L + j]);
       }
@@ -380,7 +381,11 @@ void orc_yee_advance(double* E, double* B, const double* J, int nx, int ny, doub
     double ky = (dt - dy) / (dt + dy);
     for (int k = 0; k < 2; ++k) {
       int c = (k == 0) ? 0 : 2;
-      for (int i = 0; i < nx; ++i) {
+      /* corner rule (R13): a node on two open edges (Ez at (0,0), (nx,0), (0,ny),
+       * (nx,ny)) follows the y-edge Mur, so the y node line of Ez runs over i = 0 .. nx when x is
+       * open too (Ex node nx lies outside the box: held at 0) */
+      int iend = (c == 2 && bcx == BC_OPEN) ? nx : nx - 1;
+      for (int i = 0; i <= iend; ++i) {
         E[fidx(nx, ny, c, i, 0)] = sylo[(2 * k + 1) * L + i] + ky * (E[fidx(nx, ny, c, i, 1)] - sylo[(2 * k + 0) * L + i]);
         E[fidx(nx, ny, c, i, ny)] = syhi[(2 * k + 1) * L + i] + ky * (E[fidx(nx, ny, c, i, ny - 1)] - syhi[(2 * k + 0) * L + i]);
       }

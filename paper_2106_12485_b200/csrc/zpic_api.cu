@@ -489,6 +489,14 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       if (sp.uth[k] < 0) { g_init_error = "species " + std::to_string(s) + ": uth >= 0"; return ZPIC_E_INVALID; }
   }
   if (bc->y == ZPIC_BC_MOVING_WINDOW) { g_init_error = "moving window is x only"; return ZPIC_E_INVALID; }
+  if (bc->x == ZPIC_BC_MOVING_WINDOW)   // R15: the injected column takes the profile beyond its end
+    for (int s = 0; s < n_species; ++s)
+      if (species[s].profile == ZPIC_DENS_SLAB ||
+          (species[s].profile == ZPIC_DENS_RAMP && species[s].x1 > grid->nx * grid->dx)) {
+        g_init_error = "species " + std::to_string(s) +
+                       ": a moving window needs a uniform profile or a ramp that ends inside the box (R15)";
+        return ZPIC_E_INVALID;
+      }
   if (dist) {
     if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world) { g_init_error = "bad rank / world"; return ZPIC_E_DECOMP; }
     if (grid->ny % dist->world != 0 || grid->ny / dist->world < 2) {

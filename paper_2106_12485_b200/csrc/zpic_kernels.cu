@@ -605,10 +605,9 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
       const bool row_out = yhi && gj == g.ny;   // guard row of an open y axis
       if (p.bcx == ZPIC_BC_OPEN && !row_out) {
         sE[1][EI(bn, ly)] = s_mur[hiE][0][1][ly] + p.murx * (sE[1][EI(bp, ly)] - s_mur[hiE][0][0][ly]);
+        // a corner node of two open edges (Ez at (0, 0), (nx, 0)) takes the y-edge Mur (R13 corner rule)
         if (!(ylo && p.bcy == ZPIC_BC_OPEN && gj == 0))
           sE[2][EI(bn, ly)] = s_mur[hiE][1][1][ly] + p.murx * (sE[2][EI(bp, ly)] - s_mur[hiE][1][0][ly]);
-        else if (hiE)
-          sE[2][EI(bn, ly)] = 0.f;   // corner node (nx, 0) of two open edges: never Mur-updated
         if (hiE) sE[0][EI(bn, ly)] = 0.f;
       } else if (hiE) {
         sE[0][EI(bn, ly)] = 0.f; sE[1][EI(bn, ly)] = 0.f; sE[2][EI(bn, ly)] = 0.f;
@@ -621,11 +620,15 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
       const int lx = k % (tw + 1), hiE = k / (tw + 1);
       if (!(hiE ? yhi : ylo)) continue;
       const int gi = i0 + lx, bn = hiE ? th : 0, bp = hiE ? th - 1 : 1;
-      if (p.bcx != ZPIC_BC_PERIODIC && gi == g.nx) continue;   // corner column: set by the x pass
+      // column nx of a non-periodic x axis: guards set by the x pass, except Ez on two open edges,
+      // whose corner nodes (nx, 0) and (nx, ny) follow the y-edge Mur (R13 corner rule)
+      const bool corner = p.bcx != ZPIC_BC_PERIODIC && gi == g.nx;
+      if (corner && p.bcx != ZPIC_BC_OPEN) continue;
       if (p.bcy == ZPIC_BC_OPEN) {
-        sE[0][EI(lx, bn)] = s_mur[2 + hiE][0][1][lx] + p.mury * (sE[0][EI(lx, bp)] - s_mur[2 + hiE][0][0][lx]);
+        if (!corner)
+          sE[0][EI(lx, bn)] = s_mur[2 + hiE][0][1][lx] + p.mury * (sE[0][EI(lx, bp)] - s_mur[2 + hiE][0][0][lx]);
         sE[2][EI(lx, bn)] = s_mur[2 + hiE][1][1][lx] + p.mury * (sE[2][EI(lx, bp)] - s_mur[2 + hiE][1][0][lx]);
-        if (hiE) sE[1][EI(lx, bn)] = 0.f;
+        if (hiE && !corner) sE[1][EI(lx, bn)] = 0.f;
       }
     }
   }
@@ -697,6 +700,8 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
     }
   }
   if (p.bcy == ZPIC_BC_OPEN && yhi) {
+    if (p.bcx == ZPIC_BC_OPEN && xhi && threadIdx.x == 0)   // corner node (nx, ny): Ez only
+      p.E1[2 * pl + g.at(g.nx, g.ny)] = sE[2][EI(tw, th)];
     for (int lx = threadIdx.x; lx < tw; lx += kBlock) {
       const int gi = i0 + lx - p.shift;
       if (gi < 0 || (p.shift && gi == g.nx - 1)) continue;

@@ -80,3 +80,43 @@ def test_ctypes_structs_match_the_header(tmp_path):
         assert int(got["%s size" % name]) == ctypes.sizeof(cls), name
         for f in cls._fields_:
             assert int(got["%s.%s" % (name, f[0])]) == getattr(cls, f[0]).offset, (name, f[0])
+
+
+def _init_status(cfg, profile_override=None):
+    """zpic_init's status for a config; the argument checks run before any device call, so this
+    needs no GPU (a config that passes them would go on to touch the device: not used here)."""
+    _build_module().build()
+    import paper_2106_12485_b200 as z
+    zz = z.zpic
+    sps = []
+    for s in cfg["species"]:
+        prof = {"uniform": zz.DENS_UNIFORM, "slab": zz.DENS_SLAB, "ramp": zz.DENS_RAMP}[s.get("profile", "uniform")]
+        sps.append(zz.zpic_species(s["m_q"], (ctypes.c_int32 * 2)(*s["ppc"]), s["n"], prof, s.get("x0", 0.0),
+                                   s.get("x1", 0.0), (ctypes.c_double * 3)(*s["ufl"]), (ctypes.c_double * 3)(*s["uth"])))
+    ctx = ctypes.c_void_p()
+    arr = (zz.zpic_species * len(sps))(*sps)
+    return zz._lib.zpic_init(ctypes.byref(ctx), ctypes.byref(zz.zpic_grid(cfg["nx"], cfg["ny"], cfg["dx"], cfg["dy"])),
+                             cfg["dt"], arr, len(sps), ctypes.byref(zz.zpic_boundaries(*cfg["bc"])), 1, None, None)
+
+
+def test_init_rejects_invalid_configs_before_touching_the_device():
+    """zpic_init's documented errors (include/zpic.h): CFL, bad grid, bad species, and the
+    moving-window injection reading R15 (a slab profile, or a ramp reaching past the box, has no
+    defined density for the entering columns)."""
+    import synth
+    c4 = synth.config("C4")
+    slab = synth.config("C4")
+    slab["species"][0].update(profile="slab", x0=1.0, x1=50.0)
+    far = synth.config("C4")
+    far["species"][0].update(x0=70.0, x1=90.0)            # ends beyond Lx = 80
+    cfl = synth.config("C1", dt=0.0708)                    # 1/sqrt(2)/10 = 0.07071
+    tiny = synth.config("C1", nx=1)
+    bad_ppc = synth.config("C1")
+    bad_ppc["species"][0]["ppc"] = (0, 4)
+    import paper_2106_12485_b200 as z
+    assert _init_status(slab) == -1 and "R15" in z.zpic_last_error()
+    assert _init_status(far) == -1 and "R15" in z.zpic_last_error()
+    assert _init_status(cfl) == -2
+    assert _init_status(tiny) == -1
+    assert _init_status(bad_ppc) == -1
+    assert c4["species"][0]["x1"] <= c4["nx"] * c4["dx"]   # the configs themselves satisfy R15

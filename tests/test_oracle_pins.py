@@ -598,3 +598,187 @@ def test_energy_conventions():
     sim.step()
     assert sim.ke[0][0] == pytest.approx(dx * dy * (math.sqrt(1 + 0.09) - 1), rel=1e-12)
     assert sim.fe[0] == 0.0
+
+
+# ---------------------------------------------------------------------------------------
+# P9 Mur-1 on y edges and with dx != dy (R13; C4 has dx = 0.02, dy = 0.1 and absorbing y edges)
+def _pulse_energy_left(nx, ny, dx, dy, dt, bc, comp, axis, steps):
+    E = L.grid(nx, ny)
+    B = L.grid(nx, ny)
+    if axis == "y":
+        prof = np.exp(-((np.arange(ny) * dy - 0.5 * ny * dy) / 1.0) ** 2)[:, None]
+    else:
+        prof = np.exp(-((np.arange(nx) * dx - 0.5 * nx * dx) / 1.0) ** 2)[None, :]
+    E[comp, 1:ny + 1, 1:nx + 1] = prof     # splits into two pulses running into both edges
+    L.refresh_guards(E, *bc, True)
+    L.refresh_guards(B, *bc, False)
+    J = L.grid(nx, ny)
+    e0 = L.field_energy(E, B, dx, dy)
+    for _ in range(steps):
+        L.yee_advance(E, B, J, dt, dx, dy, *bc)
+    return L.field_energy(E, B, dx, dy) / e0
+
+
+@pytest.mark.parametrize("comp", [0, 2])
+def test_mur_y_edges_absorb_at_c4_spacing(comp):
+    """A pulse of Ex (TE) or Ez (TM) running along y into both open y edges of a box with C4's
+    cells (dx = 0.02, dy = 0.1, dt = 0.019): a first-order Mur boundary absorbs a smooth normally
+    incident pulse to well below 1e-4 of its energy.  The y edges use kappa_y = (dt - dy)/(dt + dy);
+    taking dx there instead leaves ~0.4 of the energy, so this pins the y branch."""
+    left = _pulse_energy_left(4, 400, 0.02, 0.1, 0.019, (0, 1), comp, "y", int(30 / 0.019))
+    assert left < 1e-4, left
+
+
+@pytest.mark.parametrize("comp", [1, 2])
+def test_mur_x_edges_absorb_with_unequal_cells(comp):
+    """The same on the x edges with dy != dx (kappa_x = (dt - dx)/(dt + dx))."""
+    left = _pulse_energy_left(400, 4, 0.1, 0.02, 0.019, (1, 0), comp, "x", int(30 / 0.019))
+    assert left < 1e-4, left
+
+
+def _open_box_state(nx, ny, rng):
+    """Random E, B on every node an open-open box evolves (interior, plus the Mur node lines of
+    tangential E at x = nx (Ey, Ez) and y = ny (Ex, Ez)); zero elsewhere."""
+    E = L.grid(nx, ny)
+    B = L.grid(nx, ny)
+    E[0, 1:ny + 2, 1:nx + 1] = rng.normal(size=(ny + 1, nx))        # Ex: i < nx, j <= ny
+    E[1, 1:ny + 1, 1:nx + 2] = rng.normal(size=(ny, nx + 1))        # Ey: i <= nx, j < ny
+    E[2, 1:ny + 2, 1:nx + 2] = rng.normal(size=(ny + 1, nx + 1))    # Ez: i <= nx, j <= ny
+    B[:, 1:ny + 1, 1:nx + 1] = rng.normal(size=(3, ny, nx))
+    L.refresh_guards(E, 1, 1, True)
+    L.refresh_guards(B, 1, 1, False)
+    return E, B
+
+
+def _mirror(E, B, nx, ny, axis):
+    """The reflection x -> Lx - x (or y -> Ly - y) of a Yee state: node index i -> n - i,
+    half-node index i -> n - 1 - i; E is a polar vector, B a pseudovector."""
+    E2, B2 = np.zeros_like(E), np.zeros_like(B)
+    n = nx if axis == "x" else ny
+    def node(F, c, sign):       # index k of the axis (guard-extended position k + 1)
+        src = F[c]
+        dst = np.zeros_like(src)
+        ax = 1 if axis == "x" else 0
+        for k in range(0, n + 1):
+            sl_d = [slice(None), slice(None)]; sl_s = [slice(None), slice(None)]
+            sl_d[ax] = k + 1; sl_s[ax] = n - k + 1
+            dst[tuple(sl_d)] = sign * src[tuple(sl_s)]
+        return dst
+    def half(F, c, sign):
+        src = F[c]
+        dst = np.zeros_like(src)
+        ax = 1 if axis == "x" else 0
+        for k in range(0, n):
+            sl_d = [slice(None), slice(None)]; sl_s = [slice(None), slice(None)]
+            sl_d[ax] = k + 1; sl_s[ax] = n - 1 - k + 1
+            dst[tuple(sl_d)] = sign * src[tuple(sl_s)]
+        return dst
+    if axis == "x":   # x-staggered: Ex, By, Bz; polar flips Ex; pseudo flips By, Bz
+        E2[0], E2[1], E2[2] = half(E, 0, -1), node(E, 1, 1), node(E, 2, 1)
+        B2[0], B2[1], B2[2] = node(B, 0, 1), half(B, 1, -1), half(B, 2, -1)
+    else:             # y-staggered: Ey, Bx, Bz; polar flips Ey; pseudo flips Bx, Bz
+        E2[0], E2[1], E2[2] = node(E, 0, 1), half(E, 1, -1), node(E, 2, 1)
+        B2[0], B2[1], B2[2] = half(B, 0, -1), node(B, 1, 1), half(B, 2, -1)
+    return E2, B2
+
+
+@pytest.mark.parametrize("axis", ["x", "y"])
+def test_open_box_mirror_symmetry_and_corner_rule(axis):
+    """Maxwell's equations and R13 treat the low and high edge of an open axis alike, so the
+    discrete evolution of an open-open box commutes with the reflection of the box: evolving
+    the mirror image of a random state equals the mirror image of the evolved state, to
+    roundoff.  This pins every Mur node line, the guard placement of the high edges and the
+    corner rule (all four corner nodes of Ez take the y-edge Mur; a corner handled differently
+    from its mirror breaks the symmetry).  B's normal component on the edge line (Bx at x = 0,
+    By at y = 0) feeds only Mur-overwritten E nodes and has no mirror partner; it is excluded."""
+    nx, ny, dx, dy, dt = 13, 11, 0.1, 0.08, 0.045
+    rng = np.random.default_rng(21)
+    E, B = _open_box_state(nx, ny, rng)
+    Em, Bm = _mirror(E, B, nx, ny, axis)
+    J = L.grid(nx, ny)
+    for _ in range(40):
+        L.yee_advance(E, B, J, dt, dx, dy, 1, 1)
+        L.yee_advance(Em, Bm, J, dt, dx, dy, 1, 1)
+    Er, Br = _mirror(E, B, nx, ny, axis)
+    if axis == "x":
+        Br[0, :, [1, nx + 1]] = Bm[0, :, [1, nx + 1]] = 0.0     # Bx on the x = 0 line and its image
+    else:
+        Br[1, [1, ny + 1], :] = Bm[1, [1, ny + 1], :] = 0.0     # By on the y = 0 line and its image
+    scale = max(np.max(np.abs(Em)), np.max(np.abs(Bm)))
+    assert np.max(np.abs(Em - Er)) <= 1e-12 * scale
+    assert np.max(np.abs(Bm - Br)) <= 1e-12 * scale
+    # the corner nodes carry field (they are advanced, not held)
+    for (i, j) in ((0, 0), (nx, 0), (0, ny), (nx, ny)):
+        assert E[2, j + 1, i + 1] != 0.0
+
+
+# ---------------------------------------------------------------------------------------
+# P7 filter with zero guards (C4: window x axis, R12/R14)
+@pytest.mark.parametrize("bcx", [1, 2])
+def test_filter_zero_guards_is_zero_padded_convolution(bcx):
+    nx, ny = 23, 4
+    rng = np.random.default_rng(22)
+    A = rng.normal(size=(3, ny, nx))
+    for n, comp in ((1, False), (4, True)):
+        J = L.grid(nx, ny)
+        J[:, 1:ny + 1, 1:nx + 1] = A
+        L.refresh_guards(J, bcx, 0, False)
+        L.filter_x(J, bcx, 0, n, comp)
+        want = A.copy()
+        kernels = [np.array([0.25, 0.5, 0.25])] * n
+        if comp:
+            kernels.append(np.array([-n / 4, 1 + n / 2, -n / 4]))
+        for k in kernels:   # numpy's own convolution of each row, zero outside the box
+            want = np.stack([np.stack([np.convolve(r, k, mode="same") for r in c]) for c in want])
+        assert np.allclose(J[:, 1:ny + 1, 1:nx + 1], want, rtol=0, atol=1e-14)
+
+
+# ---------------------------------------------------------------------------------------
+# a5 particle removal on open edges (SPEC.md:174; C3 x, C4 y)
+@pytest.mark.parametrize("axis", ["x", "y"])
+def test_open_edge_removal_counts(axis):
+    """Particles near both open edges of an axis, drifting at known speeds in a field-free box:
+    exactly those whose straight path X + u/gamma dt/d leaves [0, n) are removed after one step,
+    and the survivors keep their ids."""
+    nx, ny, dx, dy, dt = 16, 12, 0.1, 0.08, 0.05
+    rng = np.random.default_rng(23)
+    N = 400
+    n, d = (nx, dx) if axis == "x" else (ny, dy)
+    lo = rng.random(N) < 0.5
+    cell = np.where(lo, 0, n - 1).astype(np.int32)
+    off = rng.random(N)
+    u = rng.uniform(0.05, 3.0, N) * np.where(lo, -1.0, 1.0)   # outward at both edges
+    u[rng.random(N) < 0.25] *= -1.0                             # some move inward
+    other = rng.integers(2, (ny if axis == "x" else nx) - 2, N).astype(np.int32)
+    z = np.zeros(N)
+    sp = dict(m_q=-1.0, n=1.0, ppc=(1, 1), ufl=(0, 0, 0), uth=(0, 0, 0), id=np.arange(N),
+              ix=cell if axis == "x" else other, iy=other if axis == "x" else cell,
+              x=off if axis == "x" else rng.random(N), y=rng.random(N) if axis == "x" else off,
+              ux=u if axis == "x" else z, uy=z if axis == "x" else u, uz=z)
+    bc = (1, 0) if axis == "x" else (0, 1)
+    sim = OracleSim(nx, ny, dx, dy, dt, [sp], bc=bc)
+    X = cell + off + u / np.sqrt(1 + u * u) * dt / d
+    gone = (X < 0) | (X >= n)
+    assert 0 < np.count_nonzero(gone) < N
+    sim.step()
+    s = sim.species[0]
+    assert np.array_equal(np.sort(s["id"]), np.arange(N)[~gone])
+
+
+def test_window_injection_follows_the_profile_beyond_the_box():
+    """R15: the entering column takes the species' density beyond the box: the
+    ppc lattice for n > 0 (uniform, or a ramp that ends inside the box), nothing for n = 0; a slab
+    profile or a ramp reaching past the box is rejected."""
+    nx, ny = 10, 3
+    base = dict(m_q=-1.0, ppc=(2, 1), ufl=(0, 0, 0), uth=(0, 0, 0), ix=np.zeros(0, np.int32),
+                iy=np.zeros(0, np.int32), x=np.zeros(0), y=np.zeros(0), ux=np.zeros(0), uy=np.zeros(0),
+                uz=np.zeros(0), id=np.zeros(0, np.int64))
+    sps = [dict(base, n=1.0), dict(base, n=0.0), dict(base, n=2.0, profile="ramp", x0=0.2, x1=0.6)]
+    sim = OracleSim(nx, ny, 0.1, 0.1, 0.05, sps, bc=(2, 1))
+    sim._shift_window()
+    assert [len(s["ix"]) for s in sim.species] == [2 * ny, 0, 2 * ny]
+    assert np.all(sim.species[2]["ix"] == nx - 1)
+    for bad in (dict(base, n=1.0, profile="slab", x0=0.0, x1=0.5), dict(base, n=1.0, profile="ramp", x0=0.5, x1=1.5)):
+        sim = OracleSim(nx, ny, 0.1, 0.1, 0.05, [bad], bc=(2, 1))
+        with pytest.raises(ValueError):
+            sim._shift_window()
