@@ -129,6 +129,14 @@ typedef struct {
   int32_t no_graphs;          /* 0 (default): zpic_step replays a captured CUDA graph of two steps
                                  when it can (single domain, no moving window, profile = 0), which
                                  removes the per-launch host cost of small grids; 1 = plain launches */
+  int32_t current_precision;  /* accumulation of the tile current, both order-independent:
+                                 0 = auto (default): one int32 fixed-point atomic per node at the
+                                     tile's scale 2^S, the largest S that the tile's bound |J_node| <=
+                                     (particles in any 4 x 4 cell window) * max|q| keeps below 2^31
+                                     (rounding <= 2^-(S+1) per contribution, ~2^-27 at 16 ppc);
+                                     tiles with S < 22 take the exact form;
+                                 1 = exact: every tile accumulates contributions scaled by 2^32 as
+                                     int64 split into two int32 atomics (error <= 2^-33 each). */
 } zpic_options;
 
 /* y-slab decomposition (the paper's row-band regions).

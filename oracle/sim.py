@@ -50,7 +50,6 @@ class OracleSim:
         self.fe = []          # FE(n), n = 0 .. steps-1
         self.ke = []          # [KE_s(n)]
         self.bad_moves = 0
-        self.pushed = None    # positions after the push, before boundaries (continuity, R21)
 
     # ---------------------------------------------------------------------------------
     def step(self):
@@ -58,7 +57,6 @@ class OracleSim:
         # 1. J <- 0, including guards
         self.J[...] = 0.0
         ke = []
-        self.pushed = []
         # 2. every particle: interpolate (A1) -> Boris (A2) -> deposit + cell update (A3)
         for s in self.species:
             Ep, Bp = lib.interpolate(self.E, self.B, s["ix"], s["iy"], s["x"], s["y"])
@@ -66,7 +64,6 @@ class OracleSim:
             ke.append(s["q"] * s["m_q"] * dx * dy * k)
             self.bad_moves += lib.advance_deposit(s["ix"], s["iy"], s["x"], s["y"], s["ux"], s["uy"], s["uz"],
                                                   s["q"], dt, dx, dy, self.J)
-            self.pushed.append((s["ix"].copy(), s["iy"].copy(), s["x"].copy(), s["y"].copy()))
         # 3. particle boundaries (a5): periodic wrap, or removal on an open axis.  A moving-window
         #    x axis is handled after the window shift (step 7).
         for s in self.species:
@@ -95,6 +92,8 @@ class OracleSim:
 
     # ---------------------------------------------------------------------------------
     def _keep(self, s, m):
+        if m.all():    # nothing removed (bookkeeping only: skip the copies)
+            return
         for k in ("ix", "iy", "x", "y", "ux", "uy", "uz", "id"):
             s[k] = np.ascontiguousarray(s[k][m])
 

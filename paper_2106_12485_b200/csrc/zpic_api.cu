@@ -52,6 +52,7 @@ size_t particle_msg_bytes(int cap);
 PList particle_msg_list(void* buf, int cap);
 void launch_recv_insert(const PushParams& p, const PList& lo, const PList& hi, cudaStream_t st);
 void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, cudaStream_t st);
+void launch_occupancy(const PushParams& p, cudaStream_t st);
 }  // namespace zpic
 
 using namespace zpic;
@@ -295,7 +296,10 @@ PushParams push_params(zpic_ctx* c) {
   static const int mail = [] { const char* e = getenv("ZPIC_MAIL"); return e ? atoi(e) : 1; }();
   p.use_mail = mail;
   for (int s = 0; s < c->nspecies; ++s) p.mail[s] = c->mail[s];
-  p.fx_smin = fx_smin();
+  p.fx_smin = c->opt.current_precision == 1 ? 99 : fx_smin();
+  p.occ = c->occ;
+  p.qmax = 0.f;
+  for (int s = 0; s < c->nspecies; ++s) p.qmax = std::max(p.qmax, std::fabs(c->sc[s].q));
   p.T = c->T; p.ntx = c->ntx; p.nty = c->nty;
   p.nspecies = c->nspecies;
   for (int s = 0; s < c->nspecies; ++s) { p.sc[s] = c->sc[s]; p.ps[s] = c->ps[s]; }
@@ -593,6 +597,9 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     c->energy = alloc_n<double>(c, 1 + 2 * kMaxSpecies);
     c->err = alloc_n<int>(c, 1);
     c->stats = alloc_n<int>(c, 4);
+    c->occ = alloc_n<int32_t>(c, (size_t)c->ntiles);
+    if (c->opt.current_precision != 0 && c->opt.current_precision != 1)
+      throw Fail{ZPIC_E_INVALID, "current_precision must be 0 or 1"};
     {
       double kes[kMaxSpecies] = {0, 0, 0, 0};
       for (int s = 0; s < n_species; ++s) kes[s] = c->sc[s].ke_scale;
@@ -733,6 +740,7 @@ static void drop_graphs(zpic_ctx* c);
 // Bin n particles held on the device (SoA block `tmp`: ix, iy (global), x, y, ux, uy, uz, id, n
 // entries each) into species s's tile store, sized anew for the largest tile; frees `tmp`.
 static void load_species(zpic_ctx* c, int s, int64_t n, char* tmp, bool has_id) {
+  c->occ_stale = true;   // the occupancy bound of the fixed-point current is recomputed before the next step
   int32_t* dix = (int32_t*)tmp;
   int32_t* diy = dix + n;
   float* dx_ = (float*)(diy + n);
@@ -902,6 +910,12 @@ static void maybe_repack_now(zpic_ctx* c);
 // K2s every sort_every steps (ZPIC_SORT_EVERY; 0 = never): each species' tiles re-sorted in
 // place (the store pointer does not change: the captured graphs stay valid).
 static void maybe_sort(zpic_ctx* c) {
+  if (c->occ_stale) {   // particles (re)loaded: the fixed-point current's occupancy bound, from scratch
+    launch_occupancy(push_params(c), c->stream);
+    CUDA_OR_THROW(cudaGetLastError());
+    c->launches += 1;
+    c->occ_stale = false;
+  }
   if (c->sort_every <= 0 || c->steps - c->last_sort < c->sort_every) return;
   c->last_sort = c->steps;
   for (int s = 0; s < c->nspecies; ++s) {
@@ -924,6 +938,7 @@ static bool load_chunked(zpic_ctx* c, int s, int64_t n, const int32_t* ix, const
                          const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id) {
   PStore& ps = c->ps[s];
   if (!ps.data || n <= kLoadChunk || (double)n > 0.9 * (double)ps.cap * c->ntiles) return false;
+  c->occ_stale = true;
   CUDA_OR_THROW(cudaMemsetAsync(ps.cnt, 0, (size_t)c->ntiles * 4, c->stream));
   size_lists(c, n);   // loose list room for what may not fit
   if (!c->copy_stream) CUDA_OR_THROW(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
@@ -1387,6 +1402,7 @@ zpic_status zpic_step_group(zpic_ctx** cs, int32_t count, int32_t n) {
       for (int r = 0; r < count; ++r) cs[r]->halo_dirty = false;
     }
     for (int k = 0; k < n; ++k) {
+      for (int r = 0; r < count; ++r) maybe_sort(cs[r]);
       std::vector<StepState> st(count);
       for (int r = 0; r < count; ++r) st[r] = step_phase_a(cs[r]);
       loop_exchange_round1(cs, count);

@@ -106,6 +106,7 @@ __device__ __forceinline__ void insert_particle(const PushParams& p, int s, int 
   const int slot = atomicAdd(ps.cnt + t, 1);
   const int cell = pack_cell(ix, iy);
   if (slot < ps.cap) {
+    atomicAdd(p.occ + t, 1);   // the tile's occupancy bound grows with every arrival
     uint32_t* q = ps.slot((long)t * ps.cap + slot);
     q[F_CELL * 32] = (uint32_t)cell;
     q[F_X * 32] = __float_as_uint(x); q[F_Y * 32] = __float_as_uint(y);
@@ -117,4 +118,21 @@ __device__ __forceinline__ void insert_particle(const PushParams& p, int s, int 
   }
 }
 
+// Largest particle count of a 4 x 4 cell window of a tile (h: T x T per-cell counts, row width T;
+// tw x th: the tile's cells; windows clipped to a smaller tile).  Node (i, k) of a tile's current
+// block only receives from particles that start in cells [i-2, i+1] x [k-2, k+1] (a path moves less
+// than a cell and its pieces touch the two nodes of their cell per axis), so this bounds the
+// number of particles adding into any node.  Per-thread partial maximum over a block-stride.
+__device__ __forceinline__ int window_max_4x4(const int* h, int T, int tw, int th) {
+  const int wx = min(4, tw), wy = min(4, th), na = tw - wx + 1, nb = th - wy + 1;
+  int m = 0;
+  for (int k = threadIdx.x; k < na * nb; k += blockDim.x) {
+    const int a = k % na, b = k / na;
+    int sum = 0;
+    for (int y = b; y < b + wy; ++y)
+      for (int x = a; x < a + wx; ++x) sum += h[y * T + x];
+    m = max(m, sum);
+  }
+  return m;
+}
 }  // namespace zpic

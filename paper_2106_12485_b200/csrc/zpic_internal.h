@@ -108,6 +108,12 @@ struct PushParams {
   int use_mail;         // 1: tile leavers go through the per-tile mailboxes (K3m), else the mover list
   MailBox mail[kMaxSpecies];
   int fx_smin;          // a tile uses the one-word int32 current when its scale exponent S >= fx_smin
+  // Per-tile occupancy bound (DESIGN.md §2 "fixed-point current"): occ[t] >= the number of particles
+  // (all species) in any 4 x 4 cell window of tile t at the start of K1 — K1 writes the window
+  // maximum of its stayers' end cells, every insertion into the tile (K3m, K3, loose re-insertion,
+  // halo receive, window injection) adds to it; -1 = unknown (the tile count bounds it).
+  int32_t* occ;
+  float qmax;           // max_s |q_s|
   int tile0;            // K1 launches over tiles [tile0, tile0 + grid) (the slab overlap splits it)
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
   int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
@@ -178,6 +184,8 @@ struct zpic_ctx {
   double* energy;  // [1 + kMaxSpecies] last finished step: FE, KE_s
   int* err;
   int* stats;      // [0] movers of last step, [1] spill count
+  int32_t* occ = nullptr;   // [ntiles] occupancy bound of the fixed-point current (PushParams::occ)
+  bool occ_stale = true;    // the particles were (re)loaded: recompute occ before the next step
   int cur;         // index of the current E/B buffer
   int64_t steps;
   int64_t repacks;

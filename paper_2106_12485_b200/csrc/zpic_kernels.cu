@@ -74,6 +74,7 @@ __global__ void __launch_bounds__(kBlock) k_insert(PushParams p) {
       }
       const PStore& ps = p.ps[sp[u]];
       if (slot[u] < ps.cap) {
+        atomicAdd(p.occ + t[u], 1);   // occupancy bound of the destination tile
         uint32_t* q = ps.slot((long)t[u] * ps.cap + slot[u]);
         q[F_CELL * 32] = (uint32_t)cell[u];
         q[F_X * 32] = __float_as_uint(x[u]); q[F_Y * 32] = __float_as_uint(y[u]);
@@ -162,7 +163,10 @@ __global__ void __launch_bounds__(kBlock) k_mail_gather(PushParams p) {
                   __uint_as_float(uy), __uint_as_float(uz), id, s);
     }
   }
-  if (lane == 0) ps.cnt[t] = min(pos + total, ps.cap);
+  if (lane == 0) {
+    ps.cnt[t] = min(pos + total, ps.cap);
+    if (total > 0) atomicAdd(p.occ + t, min(total, max(ps.cap - pos, 0)));   // arrivals: occupancy bound
+  }
 }
 
 // =============================================================================================
@@ -1183,4 +1187,37 @@ void launch_export(const PStore& ps, int ntiles, const int64_t* prefix, int y0, 
   k_export<<<ntiles, kBlock, 0, st>>>(ps, prefix, y0, ix, iy, x, y, ux, uy, uz, id);
 }
 
+}  // namespace zpic
+
+namespace zpic {
+// =============================================================================================
+// Occupancy bound of the fixed-point tile current after a (re)load (PushParams::occ): one CTA per
+// tile histograms the cells of every species' particles and takes the largest 4 x 4 window sum.
+__global__ void __launch_bounds__(kBlock) k_occupancy(PushParams p) {
+  __shared__ int h[32 * 32];
+  __shared__ int s_max;
+  const int t = blockIdx.x, T = p.T;
+  const int tx = t % p.ntx, ty = t / p.ntx, i0 = tx * T, j0 = ty * T;
+  const int tw = min(T, p.g.nx - i0), th = min(T, p.g.ny - j0);
+  for (int k = threadIdx.x; k < T * T; k += blockDim.x) h[k] = 0;
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  for (int s = 0; s < p.nspecies; ++s) {
+    const PStore& ps = p.ps[s];
+    const int n = min(ps.cnt[t], ps.cap);
+    for (int k = threadIdx.x; k < n; k += blockDim.x) {
+      const int c = (int)*ps.slot((long)t * ps.cap + k);
+      const int lx = cell_ix(c) - i0, ly = cell_iy(c) - j0;
+      if ((unsigned)lx < (unsigned)tw && (unsigned)ly < (unsigned)th) atomicAdd(&h[ly * T + lx], 1);
+    }
+  }
+  __syncthreads();
+  const int m = window_max_4x4(h, T, tw, th);
+  atomicMax(&s_max, m);
+  __syncthreads();
+  if (threadIdx.x == 0) p.occ[t] = s_max;
+}
+void launch_occupancy(const PushParams& p, cudaStream_t st) {
+  k_occupancy<<<p.ntx * p.nty, kBlock, 0, st>>>(p);
+}
 }  // namespace zpic

@@ -100,6 +100,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   __shared__ int s_mbc[8];  // mailbox fill per direction (this species)
   __shared__ int s_wsum[2][NW];
   __shared__ double s_ke[kMaxSpecies];
+  __shared__ int s_hist[T * T];   // stayers per end cell (the occupancy bound of the next step)
+  __shared__ int s_occ;
   if (threadIdx.x < kMaxSpecies) s_ke[threadIdx.x] = 0.0;
 
   const int t = blockIdx.x + p.tile0;
@@ -132,6 +134,11 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
           ::"r"(smem_u32(landB)), "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(cx), "r"(cy), "r"(0), "r"(bar)
           : "memory");
     }
+    for (int k = threadIdx.x; k < T * T; k += BLK) s_hist[k] = 0;
+    if (threadIdx.x == 32) {   // this step's occupancy bound; the slot collects the next step's
+      s_occ = p.occ[t];
+      p.occ[t] = 0;
+    }
     __syncthreads();   // the barrier is initialised before anyone waits on it
     asm volatile(
         "{\n .reg .pred done;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n"
@@ -147,7 +154,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
     }
     __syncthreads();   // the boxes are consumed before the current is zeroed and the rings are used
   }
-  // fixed-point scale of this tile's current: 2^S from the bound sum_s n_s |q_s| on |J|
+  // fixed-point scale of this tile's current: 2^S from a bound on |J| at any node of the block.
+  // Every particle adds at most |q_s| to any node (|v| < 1, the weights of its pieces sum to 1), and
+  // only the particles of a 4 x 4 cell window reach a node: |J_node| <= occ * max_s |q_s| with occ
+  // the tile's occupancy bound (else the tile count: sum_s n_s |q_s|).  DESIGN.md §2.
   double bound = 0.0;
   int ntot = 0;
   for (int s = 0; s < nspec; ++s) {
@@ -155,15 +165,15 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
     bound += (double)n * fabs((double)p.sc[s].q);
     ntot += n;
   }
-  const int S = fx_scale_exponent(bound, ntot);
-  // CTA-uniform choice: one int32 atomic per node, else the exact two-word form.  A node sums
-  // about nnode = 4 ntot / (tw th) particles' contributions: its rounding noise grows like
-  // sqrt(nnode) 2^-S while the current's own shot noise shrinks like 1 / sqrt(nnode) (q = n / ppc),
-  // so the threshold rises by one bit per doubling of nnode above 80 (16 ppc + 25 % fluctuation):
-  // the noise-to-signal ratio never exceeds that of a 16-ppc tile at S = fx_smin.
-  const int nnode = 4 * ntot / (tw * th);
-  const int smin = p.fx_smin + (nnode > 80 ? 32 - __clz((nnode - 1) / 80) : 0);
-  const bool fast = S >= smin;
+  int npart = ntot;
+  if (s_occ >= 0 && s_occ < ntot) {
+    bound = fmin(bound, (double)s_occ * (double)p.qmax);
+    npart = s_occ;
+  }
+  const int S = fx_scale_exponent(bound, npart);
+  // CTA-uniform choice: one int32 atomic per node at scale 2^S, else (S below the floor: a tile so
+  // dense that 2^-S would be coarse, or current_precision = exact) the exact two-word form
+  const bool fast = S >= p.fx_smin;
   for (int k = threadIdx.x; k < (fast ? 1 : 2) * JWORDS / 4; k += BLK)
     reinterpret_cast<int4*>(s_j)[k] = make_int4(0, 0, 0, 0);
 
@@ -264,6 +274,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
       }
       if (valid) {
         if (stay) {
+          atomicAdd(&s_hist[(iy - j0) * T + (ix - i0)], 1);
           const int ncell_ = pack_cell(ix, iy);
           if (!p.skip_cell_store || ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);
           __stcs(pp + F_X * 32, __float_as_uint(x)); __stcs(pp + F_Y * 32, __float_as_uint(y));
@@ -396,6 +407,10 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   }
   if ((int)threadIdx.x < nspec && s_ke[threadIdx.x] != 0.0)
     atomicAdd(p.ke_slots + threadIdx.x * kEnergySlots + (t & (kEnergySlots - 1)), s_ke[threadIdx.x]);
+  // the next step's occupancy bound: the largest 4 x 4 window of this tile's stayers (the histogram
+  // is complete: every species' loop ended at a barrier); arrivals add to it after this kernel
+  const int m = __reduce_max_sync(0xffffffffu, window_max_4x4(s_hist, T, tw, th));
+  if (lane == 0 && m > 0) atomicMax(p.occ + t, m);
 }
 
 template <int T, int BLK, int MINB, int NSPEC>

@@ -54,7 +54,8 @@ class zpic_options(ctypes.Structure):
                 ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", ctypes.c_void_p),
                 ("current_mode", ctypes.c_int32), ("laser", ctypes.c_int32), ("laser_a0", ctypes.c_double),
                 ("laser_omega0", ctypes.c_double), ("laser_fwhm", ctypes.c_double), ("laser_W0", ctypes.c_double),
-                ("laser_start", ctypes.c_double), ("no_graphs", ctypes.c_int32)]
+                ("laser_start", ctypes.c_double), ("no_graphs", ctypes.c_int32),
+                ("current_precision", ctypes.c_int32)]
 
 
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
@@ -246,7 +247,7 @@ class Simulation:
     PyTorch's current CUDA stream when torch_plumbing is True."""
 
     def __init__(self, cfg, inject=True, track_ids=False, tile=16, profile=False, capacity_slack=1.25,
-                 torch_plumbing=True, stream=None, dist=None, current_mode=0, graphs=True):
+                 torch_plumbing=True, stream=None, dist=None, current_mode=0, graphs=True, current_precision=0):
         """dist: None (whole domain) or {"rank", "world", "transport": "nccl" | "loopback",
         "nccl_id": 128 bytes | "nccl_comm": ncclComm_t address} (y-slab decomposition)."""
         self.cfg = cfg
@@ -273,6 +274,7 @@ class Simulation:
         opt.profile = int(profile)
         opt.current_mode = int(current_mode)
         opt.no_graphs = 0 if graphs else 1
+        opt.current_precision = {"auto": 0, "exact": 1}.get(current_precision, current_precision)
         if inject and "laser" in cfg:     # the laser initial fields (R17) on the device
             las = cfg["laser"]
             if las.get("polarization", "y") != "y":

@@ -9,7 +9,8 @@ momentum depends only on (seed, species index, particle id) and not on the decom
     U_j      = ((r >> 11) + 0.5) * 2^-53                                  in (0, 1)
     N_k      = sqrt(-2 ln U_{2k}) * cos(2 pi U_{2k+1}),  k = 0, 1, 2       (Box-Muller)
     u_k      = fp32(ufl_k + uth_k * N_k)       (fp64 multiply, then fp64 add, then round)
-The CUDA injector implements the same generator independently (csrc/zpic_init.cu).
+The CUDA injector implements the same generator independently (K0 `k_inject` in
+paper_2106_12485_b200/csrc/zpic_kernels.cu).
 
 Particle ids (SURVEY.md §8(c) "Initial state"): the global sub-lattice index
     id = ((iy * nx + ix) * ppc_y + l) * ppc_x + k
