@@ -56,6 +56,26 @@ def dist_env():
     return world, rank, local
 
 
+def launch_ranks(args, argv):
+    """`--gpus N` without a launcher: re-run this script under torch.distributed.run, one rank per
+    GPU of this node (rendezvous on 127.0.0.1).  Under a launcher WORLD_SIZE must equal --gpus."""
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world:
+        if world != args.gpus:
+            sys.exit("bench.py: --gpus %d but WORLD_SIZE=%d" % (args.gpus, world))
+        return False
+    if args.gpus <= 1:
+        return False
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + argv
+    sys.exit(subprocess.call(cmd))
+
+
 def k1_traffic(config, nx, ny):
     """DRAM bytes per K1 launch from the committed ncu capture of the same workload
     (profiles/r1_k1_traffic_c5.json), else None."""
@@ -155,21 +175,36 @@ def host_info():
 
 
 def cpu_baseline(args):
-    """The oracle, as it stands, on a bounded sample of the same workload: the C5 physics on a
-    1024 x 1024-cell periodic patch (16 ppc, 16.8 M particles), `steps` steps, one host core."""
+    """The oracle, as it stands, on a bounded sample of the same workload: the
+    physics of the benchmarked config on a cpu_cells^2 periodic patch, `cpu_steps` steps, pinned to
+    one host core (sched_setaffinity, the taskset equivalent), repeated `cpu_reps` times; the mean
+    and the spread of the repetitions are reported."""
     import synth
     from oracle.sim import from_config
     cfg = synth.config(args.config, nx=args.cpu_cells, ny=args.cpu_cells)
-    sim = from_config(cfg)
-    n = sum(len(s["ix"]) for s in sim.species)
-    t0 = time.perf_counter()
-    for _ in range(args.cpu_steps):
-        sim.step()
-    dt = time.perf_counter() - t0
-    return {"value": n * args.cpu_steps / dt, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": "%s physics on a %dx%d-cell periodic patch (%d particles), %d steps, fp64 serial oracle"
-                      % (args.config, args.cpu_cells, args.cpu_cells, n, args.cpu_steps),
-            "seconds": dt, **host_info()}
+    if any(sp.get("profile", "uniform") != "uniform" for sp in cfg["species"]):
+        cfg = synth.config("C5", nx=args.cpu_cells, ny=args.cpu_cells)
+    old = os.sched_getaffinity(0)
+    core = min(old)
+    os.sched_setaffinity(0, {core})
+    rates = []
+    try:
+        for _ in range(args.cpu_reps):
+            sim = from_config(cfg)
+            n = sum(len(s["ix"]) for s in sim.species)
+            t0 = time.perf_counter()
+            for _ in range(args.cpu_steps):
+                sim.step()
+            rates.append(n * args.cpu_steps / (time.perf_counter() - t0))
+            del sim
+    finally:
+        os.sched_setaffinity(0, old)
+    return {"value": statistics.mean(rates), "unit": UNIT, "cores": 1, "kind": "oracle", "core": core,
+            "std": statistics.pstdev(rates), "repetitions": len(rates),
+            "sample": "%s physics on a %dx%d-cell periodic patch (%d particles), %d steps x %d repetitions, fp64 "
+                      "serial oracle pinned to core %d" % (cfg["name"], args.cpu_cells, args.cpu_cells, n,
+                                                          args.cpu_steps, args.cpu_reps, core),
+            **host_info()}
 
 
 def run_reference(args, world, rank):
@@ -217,7 +252,7 @@ def e2e_run(args, cfg, torch, z, dist_kw=None, world=1):
         from paper_2106_12485_b200.dist import nccl_id_broadcast
         dist_kw = dict(dist_kw, nccl_id=nccl_id_broadcast())
     import synth
-    src = z.Simulation(cfg, inject=True, dist=dist_kw, tile=args.tile)
+    src = z.Simulation(cfg, inject=True, dist=dist_kw, tile=args.tile, current_precision=args.current_precision)
     host = []
     for s in range(len(cfg["species"])):
         p = src.particles(s)
@@ -234,7 +269,7 @@ def e2e_run(args, cfg, torch, z, dist_kw=None, world=1):
     if dist_kw is not None:   # a fresh communicator for the second context
         from paper_2106_12485_b200.dist import nccl_id_broadcast
         dist_kw = dict(dist_kw, nccl_id=nccl_id_broadcast())
-    sim = z.Simulation(cfg, inject=False, dist=dist_kw, tile=args.tile)
+    sim = z.Simulation(cfg, inject=False, dist=dist_kw, tile=args.tile, current_precision=args.current_precision)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -285,8 +320,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
     ap.add_argument("--tile", type=int, default=0, help="tile size (0 = the library's auto choice)")
-    ap.add_argument("--cpu-cells", type=int, default=1024)
+    ap.add_argument("--cpu-cells", type=int, default=512)
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--cpu-reps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--nx", type=int, default=0, help="override the grid (profiling runs only)")
@@ -295,8 +331,16 @@ def main():
                     help="time zpic_step with CUDA-graph replay (no per-kernel events: no roofline / kernel times)")
     ap.add_argument("--current-mode", type=int, default=0, choices=[0, 1],
                     help="0 = tile-block reduction (K4), 1 = commutative global atomics (SURVEY.md NEXT-4)")
+    ap.add_argument("--current-precision", default="auto", choices=["auto", "exact"],
+                    help="fixed-point tile current: auto (one int32 per node at the tile's scale) or exact (two words)")
+    ap.add_argument("--weak", default=None, choices=["P-COLD", "P-WARM", "P-WEIBEL"],
+                    help="weak scaling (SURVEY.md NEXT-2, PAPER.md:397-399): this config's grid per GPU, "
+                         "the global grid grows along y with the GPU count")
     args = ap.parse_args()
+    launch_ranks(args, sys.argv[1:])
     world, rank, local = dist_env()
+    if args.weak:
+        args.config = args.weak
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
@@ -309,7 +353,12 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.weak:
+        args.config = args.weak
     cfg = synth.config(args.config)
+    if args.weak:   # fixed work per GPU: the slab of every rank is the config's grid
+        cfg["ny"] *= world
+        cfg["name"] += "-weak-%dgpu" % world
     if args.nx:
         cfg["nx"], cfg["ny"] = args.nx, args.ny or args.nx
         cfg["name"] += "-resized-%dx%d" % (cfg["nx"], cfg["ny"])
@@ -318,7 +367,7 @@ def main():
         from paper_2106_12485_b200.dist import nccl_id_broadcast
         dist_kw = {"rank": rank, "world": world, "transport": "nccl", "nccl_id": nccl_id_broadcast(), "device": local}
     sim = z.Simulation(cfg, inject=True, profile=not args.graphs, tile=args.tile, dist=dist_kw,
-                       current_mode=args.current_mode)
+                       current_mode=args.current_mode, current_precision=args.current_precision)
     n_particles = sim.counters()["particles"]
     n_cells = cfg["nx"] * cfg["ny"]
     sim.step(args.warmup)
@@ -373,10 +422,12 @@ def main():
     value = n_particles * args.steps / (ms * 1e-3)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
+        "vs_baseline": None,
         "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(args.config, cfg, n_particles),
                    "tile": cnt["tile"], "current_mode": ["reduction", "commutative"][args.current_mode],
+                   "current_precision": args.current_precision,
                    "l2": "inputs larger than L2 (particle store %.1f GB)" % (n_particles * 24 / 1e9),
                    "parallelism": "y-slabs x%d" % world},
         "cell_updates_per_s": n_cells * args.steps / (ms * 1e-3),

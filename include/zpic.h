@@ -137,6 +137,9 @@ typedef struct {
                                      tiles with S < 22 take the exact form;
                                  1 = exact: every tile accumulates contributions scaled by 2^32 as
                                      int64 split into two int32 atomics (error <= 2^-33 each). */
+  int32_t halo_particles;     /* y-slabs: particle records per halo message and direction (0 = auto:
+                                 a quarter of a boundary row at the nominal density, >= 4096); more
+                                 crossers in one step stop the run with ZPIC_E_OVERFLOW */
 } zpic_options;
 
 /* y-slab decomposition (the paper's row-band regions).

@@ -18,7 +18,8 @@ namespace zpic {
 void launch_push_tiles(const PushParams& p, int tile_begin, int tile_end, cudaStream_t st);
 void launch_insert(const PushParams& p, int grid, cudaStream_t st);
 void launch_mail_gather(const PushParams& p, cudaStream_t st);
-void launch_charge(const PushParams& p, float* rho, int wrap_y, cudaStream_t st);
+void launch_charge(const PushParams& p, double* rho, int wrap_y, cudaStream_t st);
+void launch_to_float(const double* a, float* b, long n, cudaStream_t st);
 void launch_ramp_rows(long n, int n_row, int py, int y0, const int32_t* ixr, const float* xr, uint64_t key,
                       const double* ufl, const double* uth, int32_t* ix, int32_t* iy, float* x, float* y, float* ux,
                       float* uy, float* uz, uint32_t* id, cudaStream_t st);
@@ -435,6 +436,11 @@ zpic_status check_sticky(zpic_ctx* c) {
                     std::to_string(c->movers.cap) + " err " + std::to_string(err) + " steps " + std::to_string(c->steps);
     return ZPIC_E_OVERFLOW;
   }
+  if (err & ERR_HALO) {
+    c->last_error = "slab halo particle message full: more than " + std::to_string(c->pcap) +
+                    " particles crossed a slab edge in one step (raise zpic_options.halo_particles)";
+    return ZPIC_E_OVERFLOW;
+  }
   if (err & ERR_MIGRATION) { c->last_error = "a particle moved >= 1 cell in one step"; return ZPIC_E_MIGRATION; }
   return ZPIC_OK;
 }
@@ -696,13 +702,18 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       refresh_field_guards(c, c->B[0], false);
     }
     if (c->slab) {
-      // halo buffers: raw J rows from both neighbours; particle messages sized for two rows of
-      // cells at 2x the densest species sum (a particle crosses at most one row per step)
+      // halo buffers: raw J rows from both neighbours; particle messages (a count header and
+      // `pcap` records, all sent every step) sized to the traffic: only particles of the boundary
+      // row can cross, and a quarter of that row at the nominal density is ~9x
+      // the thermal crossing rate of C5 (u_th = 0.1: 2.8 % per step and direction) — 1 MB per
+      // direction at C5 instead of a whole-row bound; more crossers than that stop the run with
+      // ZPIC_E_OVERFLOW (ERR_HALO; zpic_options.halo_particles raises the capacity)
       c->jrup = alloc_n<float>(c, (size_t)3 * 2 * g.pitch);
       c->jrdn = alloc_n<float>(c, (size_t)3 * 2 * g.pitch);
       int ppc_sum = 0;
       for (int s = 0; s < n_species; ++s) ppc_sum += species[s].ppc[0] * species[s].ppc[1];
-      c->pcap = std::max(4096, round_up(4 * g.nx * std::max(ppc_sum, 1), 32));
+      c->pcap = c->opt.halo_particles > 0 ? round_up(c->opt.halo_particles, 32)
+                                          : std::max(4096, round_up(g.nx * std::max(ppc_sum, 1) / 4, 32));
       for (int d = 0; d < 2; ++d) {
         c->pmsg_send[d] = alloc_n<char>(c, particle_msg_bytes(c->pcap));
         c->pmsg_recv[d] = alloc_n<char>(c, particle_msg_bytes(c->pcap));
@@ -1559,13 +1570,16 @@ zpic_status zpic_get_charge(zpic_ctx* c, float* out, size_t out_len) {
   const GridDesc& g = c->g;
   if (out_len < (size_t)g.nx * g.ny) { c->last_error = "get_charge: buffer too small"; return ZPIC_E_BUFSIZE; }
   try {
-    float* rho = alloc_n<float>(c, (size_t)g.nx * g.ny);   // zeroed
-    const PushParams p = push_params(c);                    // spill_in = the live loose list
+    double* rho = alloc_n<double>(c, (size_t)g.nx * g.ny);   // zeroed
+    float* rhof = alloc_n<float>(c, (size_t)g.nx * g.ny);
+    const PushParams p = push_params(c);                      // spill_in = the live loose list
     launch_charge(p, rho, !c->slab && c->bcy == ZPIC_BC_PERIODIC ? 1 : 0, c->stream);
+    launch_to_float(rho, rhof, (long)g.nx * g.ny, c->stream);
     CUDA_OR_THROW(cudaGetLastError());
-    CUDA_OR_THROW(cudaMemcpyAsync(out, rho, (size_t)g.nx * g.ny * 4, cudaMemcpyDeviceToHost, c->stream));
+    CUDA_OR_THROW(cudaMemcpyAsync(out, rhof, (size_t)g.nx * g.ny * 4, cudaMemcpyDeviceToHost, c->stream));
     CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
     dev_free(c, rho);
+    dev_free(c, rhof);
   } catch (const Fail& f) {
     c->last_error = f.msg;
     return f.st;

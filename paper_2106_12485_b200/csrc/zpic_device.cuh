@@ -88,10 +88,10 @@ __device__ __forceinline__ void list_put(const PList& L, int k, int cell, float 
 }
 
 __device__ __forceinline__ void list_append(const PList& L, int* err, int cell, float x, float y, float ux, float uy,
-                                            float uz, uint32_t id, int s) {
+                                            float uz, uint32_t id, int s, int err_bit = ERR_OVERFLOW) {
   const int k = atomicAdd(L.count, 1);
   if (k < L.cap) list_put(L, k, cell, x, y, ux, uy, uz, id, s);
-  else atomicOr(err, ERR_OVERFLOW);
+  else atomicOr(err, err_bit);
 }
 
 // Insert one particle into its tile's slack, else into the loose list; a particle outside the
@@ -99,8 +99,8 @@ __device__ __forceinline__ void list_append(const PList& L, int* err, int cell, 
 // already in the neighbour's local rows (equal slabs).
 __device__ __forceinline__ void insert_particle(const PushParams& p, int s, int ix, int iy, float x, float y, float ux,
                                                 float uy, float uz, uint32_t id) {
-  if (iy < 0) { list_append(p.send[0], p.err, pack_cell(ix, iy + p.g.ny), x, y, ux, uy, uz, id, s); return; }
-  if (iy >= p.g.ny) { list_append(p.send[1], p.err, pack_cell(ix, iy - p.g.ny), x, y, ux, uy, uz, id, s); return; }
+  if (iy < 0) { list_append(p.send[0], p.err, pack_cell(ix, iy + p.g.ny), x, y, ux, uy, uz, id, s, ERR_HALO); return; }
+  if (iy >= p.g.ny) { list_append(p.send[1], p.err, pack_cell(ix, iy - p.g.ny), x, y, ux, uy, uz, id, s, ERR_HALO); return; }
   const int t = (iy / p.T) * p.ntx + (ix / p.T);
   const PStore& ps = p.ps[s];
   const int slot = atomicAdd(ps.cnt + t, 1);

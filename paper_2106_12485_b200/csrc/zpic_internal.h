@@ -148,7 +148,7 @@ struct LaserParams {
   double a0, omega0, fwhm, W0, start, yc;
 };
 
-enum ErrBits { ERR_OVERFLOW = 1, ERR_MIGRATION = 2 };
+enum ErrBits { ERR_OVERFLOW = 1, ERR_MIGRATION = 2, ERR_HALO = 8 };   // 4: k_count's out-of-slab upload
 
 }  // namespace zpic
 

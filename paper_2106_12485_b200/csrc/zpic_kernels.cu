@@ -1020,7 +1020,7 @@ void launch_laser(float* E, float* B, const GridDesc& g, int y0, double dx, doub
 // Diagnostic charge density (zpic_get_charge): one CTA per tile (and one grid-stride pass over
 // the loose list), fp32 global atomics into an [ny][nx] node grid, indices wrapped (x, and y
 // unless a slab), nodes outside dropped.
-__device__ __forceinline__ void charge_add(float* rho, int nx, int ny, bool wrap_y, int i, int j, float v) {
+__device__ __forceinline__ void charge_add(double* rho, int nx, int ny, bool wrap_y, int i, int j, double v) {
   if (i >= nx) i -= nx;
   if (j >= ny) {
     if (!wrap_y) return;
@@ -1028,14 +1028,17 @@ __device__ __forceinline__ void charge_add(float* rho, int nx, int ny, bool wrap
   }
   atomicAdd(rho + (long)j * nx + i, v);
 }
-__device__ __forceinline__ void charge_particle(float* rho, int nx, int ny, bool wrap_y, int c, float x, float y, float q) {
+__device__ __forceinline__ void charge_particle(double* rho, int nx, int ny, bool wrap_y, int c, float x, float y, float q) {
   const int i = cell_ix(c), j = cell_iy(c);
-  charge_add(rho, nx, ny, wrap_y, i, j, q * (1.f - x) * (1.f - y));
-  charge_add(rho, nx, ny, wrap_y, i + 1, j, q * x * (1.f - y));
-  charge_add(rho, nx, ny, wrap_y, i, j + 1, q * (1.f - x) * y);
-  charge_add(rho, nx, ny, wrap_y, i + 1, j + 1, q * x * y);
+  // fp64 weights and sums: the diagnostic resolves the fp32 state to ~1e-16 (its continuity
+  // check is not limited by the summation of the node charge)
+  const double X = x, Y = y, Q = q;
+  charge_add(rho, nx, ny, wrap_y, i, j, Q * (1.0 - X) * (1.0 - Y));
+  charge_add(rho, nx, ny, wrap_y, i + 1, j, Q * X * (1.0 - Y));
+  charge_add(rho, nx, ny, wrap_y, i, j + 1, Q * (1.0 - X) * Y);
+  charge_add(rho, nx, ny, wrap_y, i + 1, j + 1, Q * X * Y);
 }
-__global__ void k_charge(PushParams p, float* rho, int wrap_y) {
+__global__ void k_charge(PushParams p, double* rho, int wrap_y) {
   const int t = blockIdx.x;
   if (t < p.ntx * p.nty) {
     for (int s = 0; s < p.nspecies; ++s) {
@@ -1054,7 +1057,13 @@ __global__ void k_charge(PushParams p, float* rho, int wrap_y) {
                       p.sc[p.spill_in.species[k]].q);
   }
 }
-void launch_charge(const PushParams& p, float* rho, int wrap_y, cudaStream_t st) {
+__global__ void k_to_float(const double* a, float* b, long n) {
+  for (long k = blockIdx.x * (long)blockDim.x + threadIdx.x; k < n; k += (long)gridDim.x * blockDim.x) b[k] = (float)a[k];
+}
+void launch_to_float(const double* a, float* b, long n, cudaStream_t st) {
+  k_to_float<<<148 * 4, kBlock, 0, st>>>(a, b, n);
+}
+void launch_charge(const PushParams& p, double* rho, int wrap_y, cudaStream_t st) {
   k_charge<<<p.ntx * p.nty + 148, kBlock, 0, st>>>(p, rho, wrap_y);
 }
 

@@ -55,7 +55,7 @@ class zpic_options(ctypes.Structure):
                 ("current_mode", ctypes.c_int32), ("laser", ctypes.c_int32), ("laser_a0", ctypes.c_double),
                 ("laser_omega0", ctypes.c_double), ("laser_fwhm", ctypes.c_double), ("laser_W0", ctypes.c_double),
                 ("laser_start", ctypes.c_double), ("no_graphs", ctypes.c_int32),
-                ("current_precision", ctypes.c_int32)]
+                ("current_precision", ctypes.c_int32), ("halo_particles", ctypes.c_int32)]
 
 
 TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1

@@ -60,3 +60,27 @@ def test_slab_layout_validation():
         zd.slab_layout(10, 4, 0)
     with pytest.raises(ValueError):
         zd.slab_layout(6, 4, 0)
+
+
+def test_bench_spawns_one_rank_per_gpu():
+    """`bench.py --gpus 2` without a launcher re-runs itself under torch.distributed.run (two
+    ranks, rendezvous on 127.0.0.1); with the reference arm (CPU only) rank 0 prints the single
+    JSON line with n_gpus = 2 and the other rank exits cleanly.  A launcher whose WORLD_SIZE
+    disagrees with --gpus is an error, not a silent 1-GPU run."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0", "--cpu-cells", "64"], capture_output=True, text=True,
+                       env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    bad = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "4",
+                          "--steps", "1", "--warmup", "0", "--cpu-cells", "64"], capture_output=True, text=True,
+                         env=dict(env, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0"), timeout=600)
+    assert bad.returncode != 0 and "WORLD_SIZE" in bad.stderr

@@ -20,10 +20,12 @@ from parity_util import CONT_TOL, ENERGY_TOL, FIELD_TOL, continuity_residual, en
 
 pytestmark = pytest.mark.gpu
 
-# Final-map bar (reading): fp32 roundoff grows over a long run; the paper's own
-# fp32 implementations differ by ~1e-4 in the final B map.  The runs here are
-# required to stay within 1e-2 relative L2 of the fp64 oracle, and the measured values are reported.
-FINAL_MAP_TOL = 1e-2
+# Final-map bars (reading): fp32 roundoff grows over a long run; the paper's own
+# fp32 implementations differ by ~1e-4 in the final B map.  Here the final B map
+# must stay within 1e-3 relative L2 of the fp64 oracle (measured: C2 after 500 Weibel steps 1.2e-4,
+# C1-C5 <= 8e-5) and E within 1e-2 (E is ~100x weaker than B in the Weibel run: 8e-4 measured).
+FINAL_B_TOL = 1e-3
+FINAL_E_TOL = 1e-2
 
 
 def _z():
@@ -96,6 +98,7 @@ def test_full_run_parity(name, precision, cont_every, oracle_run):
     # R21 continuity, every checked step
     rec["continuity_max"] = max(r for _, r in cont)
     rec["continuity_checked_steps"] = len(cont)
+    rec["continuity"] = cont
     # R22 energy histories
     rec["fe_agreement"] = energy_agreement(fe, o["fe"])
     rec["ke_agreement"] = [energy_agreement(ke[:, s], o["ke"][:, s]) for s in range(ke.shape[1])]
@@ -112,7 +115,7 @@ def test_full_run_parity(name, precision, cont_every, oracle_run):
     assert rec["fe_agreement"] <= ENERGY_TOL and max(rec["ke_agreement"]) <= ENERGY_TOL, rec
     assert rec["total_agreement"] <= ENERGY_TOL, rec
     assert rec["E10_rel_l2"] <= FIELD_TOL and rec["B10_rel_l2"] <= FIELD_TOL, rec
-    assert rec["B_final_rel_l2"] <= FINAL_MAP_TOL and rec["E_final_rel_l2"] <= FINAL_MAP_TOL, rec
+    assert rec["B_final_rel_l2"] <= FINAL_B_TOL and rec["E_final_rel_l2"] <= FINAL_E_TOL, rec
     assert rec["particles"][0] == rec["particles"][1], rec
 
 
@@ -166,4 +169,4 @@ def test_c5_full_run_sampled_patches(precision, oracle_run):
     for pr in rec["patches"]:
         assert pr[10]["E_rel_l2"] <= FIELD_TOL and pr[10]["B_rel_l2"] <= FIELD_TOL, pr
         assert all(pr[n]["fe_rel"] <= ENERGY_TOL for n in F.C5_SNAPS), pr
-        assert pr[F.C5_STEPS]["E_rel_l2"] <= FINAL_MAP_TOL and pr[F.C5_STEPS]["B_rel_l2"] <= FINAL_MAP_TOL, pr
+        assert pr[F.C5_STEPS]["E_rel_l2"] <= FINAL_E_TOL and pr[F.C5_STEPS]["B_rel_l2"] <= FINAL_B_TOL, pr
