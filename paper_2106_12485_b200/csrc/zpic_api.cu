@@ -597,7 +597,8 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     if (c->opt.filter_passes < 0 || c->opt.filter_passes > 64) throw Fail{ZPIC_E_INVALID, "filter_passes must be in [0, 64]"};
     if (c->opt.current_mode != 0 && c->opt.current_mode != 1) throw Fail{ZPIC_E_INVALID, "current_mode must be 0 or 1"};
     const int WJ = c->T + 3;
-    c->Jt = c->opt.current_mode == 1 ? nullptr : alloc_n<float>(c, (size_t)c->ntiles * 3 * WJ * WJ);
+    (void)WJ;   // ring buffer: 12 T nodes x 3 components per tile (TileRing, zpic_kernels.cuh)
+    c->Jt = c->opt.current_mode == 1 ? nullptr : alloc_n<float>(c, (size_t)c->ntiles * 3 * 12 * c->T);
     c->ke_slots = alloc_n<double>(c, kMaxSpecies * kEnergySlots);
     c->fe_slots = alloc_n<double>(c, kEnergySlots);
     c->energy = alloc_n<double>(c, 1 + 2 * kMaxSpecies);

@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   using L = K1Smem<T>;
   constexpr int W = T + 2, WJ = T + 3, NW = BLK / 32;
   constexpr int JWORDS = L::JWORDS;
+  static_assert(2 * kHCap * 4 <= L::QBYTES(BLK), "hole lists exceed the path rings");
   static_assert(L::BOFF + L::BOX <= L::JBYTES + L::QBYTES(BLK), "TMA landing exceeds the current + ring bytes");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   int* s_j = reinterpret_cast<int*>(smem_raw);         // int32 current, or the high words (exact form)
@@ -94,7 +95,11 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   float* s_ez = reinterpret_cast<float*>(s_eb2 + W * W);
   float* s_bz = s_ez + W * W;
   __shared__ __align__(8) unsigned long long s_bar;
-  __shared__ int s_holes[kHCap], s_hb[kHCap], s_sa[kHCap];
+  __shared__ int s_holes[kHCap];
+  // the hole fill's lists live in the path rings: it runs after every warp drained its ring and
+  // before the next species' loop (a barrier), so the static shared memory stays at 8 CTAs / SM
+  int* s_hb = reinterpret_cast<int*>(smem_raw + L::JBYTES);
+  int* s_sa = s_hb + kHCap;
   __shared__ unsigned s_bits[kHCap / 32];
   __shared__ int s_cnt[4];  // holes, holes below, stayers above, hole-list overflow
   __shared__ int s_mbc[8];  // mailbox fill per direction (this species)
@@ -396,14 +401,20 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
       const int c = k / (WJ * WJ), r = k % (WJ * WJ);
       if (v != 0.0f) atomicAdd(p.J + c * pl + p.g.at(i0 - 1 + r % WJ, j0 - 1 + r / WJ), v);
     }
-  } else if (fast) {
-    float* jt = p.Jt + (long)t * 3 * WJ * WJ;
-    const float finv = ldexpf(1.0f, -S);
-    for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) __stcg(jt + k, (float)s_j[k] * finv);
   } else {
-    float* jt = p.Jt + (long)t * 3 * WJ * WJ;
-    for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK)
-      __stcg(jt + k, (float)(fma((double)s_j[k], 32768.0, (double)s_jlo[k]) * kFxInv));
+    // the block's exclusive nodes straight into J, its ring to the ring buffer (K4 sums the rings)
+    using R = TileRing<T>;
+    float* jr = p.Jt + (long)t * 3 * R::N;
+    const float finv = ldexpf(1.0f, -S);
+    for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) {
+      const float v = fast ? (float)s_j[k] * finv : (float)(fma((double)s_j[k], 32768.0, (double)s_jlo[k]) * kFxInv);
+      const int c = k / (WJ * WJ), r = k - c * (WJ * WJ), b = r / WJ - 1, a = r - (b + 1) * WJ - 1;
+      if (R::exclusive(a, b)) {
+        if (i0 + a <= p.g.nx + 1 && j0 + b <= p.g.ny + 1) __stcg(p.J + c * pl + p.g.at(i0 + a, j0 + b), v);
+      } else {
+        __stcg(jr + c * R::N + R::slot(a, b), v);
+      }
+    }
   }
   if ((int)threadIdx.x < nspec && s_ke[threadIdx.x] != 0.0)
     atomicAdd(p.ke_slots + threadIdx.x * kEnergySlots + (t & (kEnergySlots - 1)), s_ke[threadIdx.x]);
