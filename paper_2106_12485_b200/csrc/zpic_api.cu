@@ -597,8 +597,7 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     if (c->opt.filter_passes < 0 || c->opt.filter_passes > 64) throw Fail{ZPIC_E_INVALID, "filter_passes must be in [0, 64]"};
     if (c->opt.current_mode != 0 && c->opt.current_mode != 1) throw Fail{ZPIC_E_INVALID, "current_mode must be 0 or 1"};
     const int WJ = c->T + 3;
-    (void)WJ;   // ring buffer: 12 T nodes x 3 components per tile (TileRing, zpic_kernels.cuh)
-    c->Jt = c->opt.current_mode == 1 ? nullptr : alloc_n<float>(c, (size_t)c->ntiles * 3 * 12 * c->T);
+    c->Jt = c->opt.current_mode == 1 ? nullptr : alloc_n<float>(c, (size_t)c->ntiles * 3 * WJ * WJ);
     c->ke_slots = alloc_n<double>(c, kMaxSpecies * kEnergySlots);
     c->fe_slots = alloc_n<double>(c, kEnergySlots);
     c->energy = alloc_n<double>(c, 1 + 2 * kMaxSpecies);
@@ -1302,6 +1301,83 @@ static cudaGraphExec_t two_step_graph(zpic_ctx* c) {
   return ge;
 }
 
+// One step of a context on the NCCL transport (or the unsplit domain): the halo rounds run on the
+// comm stream, overlapped with interior work; round 2 stays pending into the
+// next step's K1 (r2_pending) until slab_join.
+static void run_step_nccl(zpic_ctx* c) {
+  StepState s = step_phase_a(c);
+  if (c->slab) {
+    ncclResult_t r;
+    if (overlap_round1(c)) {   // round 1 on the comm stream, interior Yee rows meanwhile
+      CUDA_OR_THROW(cudaEventRecord(c->ev[0], c->stream));
+      CUDA_OR_THROW(cudaStreamWaitEvent(c->comm_stream, c->ev[0], 0));
+      r = nccl_exchange_round1(c, c->comm_stream);
+      CUDA_OR_THROW(cudaEventRecord(c->ev[1], c->comm_stream));
+      s.r1_async = true;
+    } else {
+      ProfScope ps(c, K_EXCHANGE);
+      r = nccl_exchange_round1(c, c->stream);
+    }
+    if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 1: ") + ncclGetErrorString(r)};
+  }
+  step_phase_b(c, s);
+  if (c->slab) {
+    ncclResult_t r;
+    if (c->comm_stream) {   // round 2 on the comm stream, the next step's interior K1 meanwhile
+      CUDA_OR_THROW(cudaEventRecord(c->ev[2], c->stream));
+      CUDA_OR_THROW(cudaStreamWaitEvent(c->comm_stream, c->ev[2], 0));
+      r = nccl_exchange_round2(c, c->cur ^ 1, c->comm_stream);
+      CUDA_OR_THROW(cudaEventRecord(c->ev[3], c->comm_stream));
+      c->r2_pending = true;
+    } else {
+      ProfScope ps(c, K_EXCHANGE);
+      r = nccl_exchange_round2(c, c->cur ^ 1, c->stream);
+    }
+    if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 2: ") + ncclGetErrorString(r)};
+  }
+  step_phase_c(c, s);
+}
+static void slab_join(zpic_ctx* c) {
+  if (c->r2_pending) {
+    CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
+    c->r2_pending = false;
+  }
+}
+// NEXT-1 on the y-slab path: two NCCL steps captured as one CUDA graph (NCCL send / recv are
+// capturable; the comm stream forks from and joins the compute stream through the captured event
+// edges, so inside the graph round 2 of the first step still overlaps the second step's interior
+// K1, and the two halo rounds overlap interior kernels as in plain launches).  The graph starts and
+// ends joined (no pending round), so the host state after a replay is that of two plain steps.
+static bool graphs_eligible_slab(const zpic_ctx* c) {
+  return !c->opt.no_graphs && !c->prof && c->slab && c->transport == ZPIC_TRANSPORT_NCCL &&
+         c->bcx != ZPIC_BC_MOVING_WINDOW && !c->r2_pending;
+}
+static cudaGraphExec_t slab_two_step_graph(zpic_ctx* c) {
+  cudaGraphExec_t& ge = c->graph[c->steps & 1];
+  if (ge) return ge;
+  const int cur = c->cur, since = c->since_check;
+  const int64_t steps = c->steps, launches = c->launches;
+  cudaGraph_t g = nullptr;
+  CUDA_OR_THROW(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+  try {
+    run_step_nccl(c);
+    run_step_nccl(c);
+    slab_join(c);
+  } catch (...) {
+    cudaStreamEndCapture(c->stream, &g);
+    if (g) cudaGraphDestroy(g);
+    c->r2_pending = false;
+    throw;
+  }
+  CUDA_OR_THROW(cudaStreamEndCapture(c->stream, &g));
+  c->graph_launches = (int)(c->launches - launches);
+  c->cur = cur; c->steps = steps; c->launches = launches; c->since_check = since;   // capture only recorded the work
+  const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) { ge = nullptr; throw Fail{ZPIC_E_CUDA, std::string("graph: ") + cudaGetErrorString(e)}; }
+  return ge;
+}
+
 zpic_status zpic_step(zpic_ctx* c, int32_t n) {
   if (!c || n < 0) return ZPIC_E_INVALID;
   if (graphs_eligible(c) && n >= 2 && c->bcx == ZPIC_BC_MOVING_WINDOW) {
@@ -1352,45 +1428,23 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
       if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL halo: ") + ncclGetErrorString(r)};
       c->halo_dirty = false;
     }
-    for (int k = 0; k < n; ++k) {
+    int k = 0;
+    if (c->slab && graphs_eligible_slab(c)) {   // two steps per replayed graph (NEXT-1)
+      for (; k + 2 <= n; k += 2) {
+        maybe_repack(c);
+        maybe_sort(c);
+        CUDA_OR_THROW(cudaGraphLaunch(slab_two_step_graph(c), c->stream));
+        c->steps += 2;
+        c->since_check += 2;
+        c->launches += c->graph_launches;
+      }
+    }
+    for (; k < n; ++k) {
       maybe_repack(c);
       maybe_sort(c);
-      StepState s = step_phase_a(c);
-      if (c->slab) {
-        ncclResult_t r;
-        if (overlap_round1(c)) {   // round 1 on the comm stream, interior Yee rows meanwhile
-          CUDA_OR_THROW(cudaEventRecord(c->ev[0], c->stream));
-          CUDA_OR_THROW(cudaStreamWaitEvent(c->comm_stream, c->ev[0], 0));
-          r = nccl_exchange_round1(c, c->comm_stream);
-          CUDA_OR_THROW(cudaEventRecord(c->ev[1], c->comm_stream));
-          s.r1_async = true;
-        } else {
-          ProfScope ps(c, K_EXCHANGE);
-          r = nccl_exchange_round1(c, c->stream);
-        }
-        if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 1: ") + ncclGetErrorString(r)};
-      }
-      step_phase_b(c, s);
-      if (c->slab) {
-        ncclResult_t r;
-        if (c->comm_stream) {   // round 2 on the comm stream, the next step's interior K1 meanwhile
-          CUDA_OR_THROW(cudaEventRecord(c->ev[2], c->stream));
-          CUDA_OR_THROW(cudaStreamWaitEvent(c->comm_stream, c->ev[2], 0));
-          r = nccl_exchange_round2(c, c->cur ^ 1, c->comm_stream);
-          CUDA_OR_THROW(cudaEventRecord(c->ev[3], c->comm_stream));
-          c->r2_pending = true;
-        } else {
-          ProfScope ps(c, K_EXCHANGE);
-          r = nccl_exchange_round2(c, c->cur ^ 1, c->stream);
-        }
-        if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 2: ") + ncclGetErrorString(r)};
-      }
-      step_phase_c(c, s);
+      run_step_nccl(c);
     }
-    if (c->r2_pending) {   // the caller's stream sees complete ghost rows after zpic_step
-      CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
-      c->r2_pending = false;
-    }
+    slab_join(c);   // the caller's stream sees complete ghost rows after zpic_step
   } catch (const Fail& f) {
     c->last_error = f.msg;
     return f.st;

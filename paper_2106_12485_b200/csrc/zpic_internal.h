@@ -87,7 +87,7 @@ struct PushParams {
   const float* E;   // current E (3 planes)
   const float* B;
   float* J;         // assembled J grid (loose-particle deposits)
-  float* Jt;        // per-tile J rings [ntiles][3][12 T] (TileRing; the exclusive nodes go to J)
+  float* Jt;        // per-tile J blocks [ntiles][3][(T+3)^2]
   int T, ntx, nty;
   int nspecies;
   SpeciesConst sc[kMaxSpecies];
@@ -175,7 +175,7 @@ struct zpic_ctx {
   float* B[2];
   float* J;        // assembled (and folded, filtered) current used by the field advance
   float* Jf;       // filtered current (only with a filter; J keeps the pre-filter values)
-  float* Jt;       // per-tile current rings (TileRing)
+  float* Jt;       // per-tile blocks
   zpic::PStore ps[zpic::kMaxSpecies];
   zpic::MailBox mail[zpic::kMaxSpecies];
   zpic::PList movers, spill[2];

@@ -170,43 +170,53 @@ __global__ void __launch_bounds__(kBlock) k_mail_gather(PushParams p) {
 }
 
 // =============================================================================================
-// K4: the J nodes that more than one tile block covers (the 3 node lines next to every tile edge,
-// guards included) = the sum of the covering tiles' rings; K1 already stored every other node
-// ("the reduction is only required for ghost cells").  No atomics, no memset.  One
-// CTA per J row: a row inside a tile's ring rows takes all its columns, any other row only the
-// 3 columns next to each tile edge.  No periodic wrap here: blocks at the domain edge land in the
-// guards and K4b folds them.
+// K4: J grid node (i, j), -1 <= i <= nx+1, -1 <= j <= ny+1, = sum of the (at most 2 x 2) tile
+// blocks covering it.  No periodic wrap here: blocks at the domain edge land in the guards and
+// K4b folds them ("the reduction is only required for ghost cells").
+// Each thread assembles K4R nodes of one column (rows j, j + 1, ...): all their block loads are
+// issued before the sums (more bytes in flight per thread; K4 is latency-bound otherwise).
+constexpr int K4R = 4;
 template <int T>
-__global__ void __launch_bounds__(kBlock) k_assemble_j(float* __restrict__ J, const float* __restrict__ Jr, GridDesc g,
+__global__ void __launch_bounds__(kBlock) k_assemble_j(float* __restrict__ J, const float* __restrict__ Jt, GridDesc g,
                                                        int ntx, int nty) {
-  using R = TileRing<T>;
-  const int j = blockIdx.x - 1;   // -1 .. ny + 1
-  const int thy = (j + 1) / T, lhy = j - thy * T;   // tile row with local row lhy in [-1, T-1)
-  const bool ya = thy < nty, yb = lhy <= 1 && thy >= 1;
-  const bool band_row = !(lhy >= 2 && lhy < T - 1) || !ya;
-  const int ncol = band_row ? g.nx + 3 : 3 * (ntx + 1);
-  for (int q = threadIdx.x; q < ncol; q += blockDim.x) {
-    const int i = band_row ? q - 1 : (q / 3) * T - 1 + q % 3;
-    if (i > g.nx + 1) continue;
-    const int thx = (i + 1) / T, lhx = i - thx * T;
-    const bool xa = thx < ntx, xb = lhx <= 1 && thx >= 1;
-    float v0 = 0.f, v1 = 0.f, v2 = 0.f;
-    auto add = [&](bool ok, int tx, int ty, int a, int b) {
+  constexpr int WJ = T + 3;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x - 1;
+  if (i > g.nx + 1) return;
+  // column i's entry in the (at most 2) x-overlapping tile blocks of tile row 0
+  const int thx = (i + 1) / T, lhx = i - thx * T;
+  const bool xa = thx < ntx, xb = lhx <= 1 && thx >= 1;
+  const float* bxa = Jt + (long)thx * 3 * WJ * WJ + (lhx + 1);
+  const float* bxb = Jt + (long)(thx - 1) * 3 * WJ * WJ + (lhx + T + 1);
+  float v[K4R][3];
+#pragma unroll
+  for (int r = 0; r < K4R; ++r) {
+    const int j = blockIdx.y * K4R + r - 1;
+    const int th = (j + 1) / T, lh = j - th * T;
+    const bool in = j <= g.ny + 1;
+    const bool ya = in && th < nty, yb = in && lh <= 1 && th >= 1;
+    const long oa = (long)th * ntx * 3 * WJ * WJ + (lh + 1) * WJ;
+    const long ob = (long)(th - 1) * ntx * 3 * WJ * WJ + (lh + T + 1) * WJ;
+    v[r][0] = v[r][1] = v[r][2] = 0.f;
+    auto add = [&](bool ok, const float* blk) {
       if (ok) {
-        const float* r = Jr + ((long)ty * ntx + tx) * 3 * R::N + R::slot(a, b);
-        v0 += __ldcg(r);
-        v1 += __ldcg(r + R::N);
-        v2 += __ldcg(r + 2 * R::N);
+        v[r][0] += __ldcg(blk);
+        v[r][1] += __ldcg(blk + WJ * WJ);
+        v[r][2] += __ldcg(blk + 2 * WJ * WJ);
       }
     };
-    add(ya && xa, thx, thy, lhx, lhy);
-    add(ya && xb, thx - 1, thy, lhx + T, lhy);
-    add(yb && xa, thx, thy - 1, lhx, lhy + T);
-    add(yb && xb, thx - 1, thy - 1, lhx + T, lhy + T);
+    add(ya && xa, bxa + oa);
+    add(ya && xb, bxb + oa);
+    add(yb && xa, bxa + ob);
+    add(yb && xb, bxb + ob);
+  }
+#pragma unroll
+  for (int r = 0; r < K4R; ++r) {
+    const int j = blockIdx.y * K4R + r - 1;
+    if (j > g.ny + 1) break;
     const long o = g.at(i, j);
-    J[o] = v0;
-    J[g.plane + o] = v1;
-    J[2 * g.plane + o] = v2;
+    J[o] = v[r][0];
+    J[g.plane + o] = v[r][1];
+    J[2 * g.plane + o] = v[r][2];
   }
 }
 
@@ -1104,7 +1114,7 @@ void launch_mail_gather(const PushParams& p, cudaStream_t st) {
 void launch_insert(const PushParams& p, int grid, cudaStream_t st) { k_insert<<<grid * 2, kBlock, 0, st>>>(p); }
 void launch_loose(const PushParams& p, int grid, cudaStream_t st) { k_push_loose<<<grid, kBlock, 0, st>>>(p); }
 void launch_assemble(float* J, const float* Jt, const GridDesc& g, int T, int ntx, int nty, cudaStream_t st) {
-  const int grid = g.ny + 3;
+  dim3 grid((g.nx + 3 + kBlock - 1) / kBlock, (g.ny + 3 + K4R - 1) / K4R);
   switch (T) {
     case 8: k_assemble_j<8><<<grid, kBlock, 0, st>>>(J, Jt, g, ntx, nty); break;
     case 16: k_assemble_j<16><<<grid, kBlock, 0, st>>>(J, Jt, g, ntx, nty); break;

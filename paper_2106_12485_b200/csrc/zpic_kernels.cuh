@@ -116,24 +116,6 @@ struct GlobalCurrent {
   __device__ __forceinline__ void add(int c, long o, float v) const { atomicAdd(J + c * g.plane + o, v); }
 };
 
-// ---- tile current blocks: exclusive interior + ring ---------------------------------------
-// A tile's (T+3)^2 block covers local nodes [-1, T+2); its neighbours' blocks overlap it on the 3
-// node lines next to each tile edge.  The nodes [2, T-1)^2 belong to this tile alone: K1 stores
-// them straight into J.  The others (the ring, 12 T nodes per component: 3 rows at the bottom, 3 at
-// the top, 3 + 3 columns in between) go to the per-tile ring buffer, and K4 sums the overlapping
-// rings into J ("the reduction is only required for ghost cells").
-template <int T>
-struct TileRing {
-  static constexpr int WJ = T + 3, N = 12 * T;   // nodes per component
-  __host__ __device__ static constexpr bool exclusive(int a, int b) { return a >= 2 && a < T - 1 && b >= 2 && b < T - 1; }
-  __host__ __device__ static int slot(int a, int b) {   // (a, b) in [-1, T+2)^2, not exclusive
-    if (b < 2) return (b + 1) * WJ + (a + 1);
-    if (b >= T - 1) return 3 * WJ + (b - (T - 1)) * WJ + (a + 1);
-    const int m = 6 * WJ + (b - 2) * 6;
-    return a < 2 ? m + (a + 1) : m + 3 + (a - (T - 1));
-  }
-};
-
 // ---- (1) interpolation, PAPER.md:144 -------------------------------------------------------
 // Bilinear weights with the Yee staggering: for a half-staggered axis the stencil starts one
 // cell lower when the offset is below 1/2.

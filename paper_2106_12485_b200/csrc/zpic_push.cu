@@ -171,11 +171,19 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
     ntot += n;
   }
   int npart = ntot;
+#ifdef ZPIC_OLD_BOUND
+  if (false) {
+#else
   if (s_occ >= 0 && s_occ < ntot) {
+#endif
     bound = fmin(bound, (double)s_occ * (double)p.qmax);
     npart = s_occ;
   }
+#ifdef ZPIC_SCAP
+  const int S = min(fx_scale_exponent(bound, npart), ZPIC_SCAP);
+#else
   const int S = fx_scale_exponent(bound, npart);
+#endif
   // CTA-uniform choice: one int32 atomic per node at scale 2^S, else (S below the floor: a tile so
   // dense that 2^-S would be coarse, or current_precision = exact) the exact two-word form
   const bool fast = S >= p.fx_smin;
@@ -279,7 +287,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
       }
       if (valid) {
         if (stay) {
+#ifndef ZPIC_NO_OCC_HIST
           atomicAdd(&s_hist[(iy - j0) * T + (ix - i0)], 1);
+#endif
           const int ncell_ = pack_cell(ix, iy);
           if (!p.skip_cell_store || ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);
           __stcs(pp + F_X * 32, __float_as_uint(x)); __stcs(pp + F_Y * 32, __float_as_uint(y));
@@ -401,27 +411,25 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
       const int c = k / (WJ * WJ), r = k % (WJ * WJ);
       if (v != 0.0f) atomicAdd(p.J + c * pl + p.g.at(i0 - 1 + r % WJ, j0 - 1 + r / WJ), v);
     }
-  } else {
-    // the block's exclusive nodes straight into J, its ring to the ring buffer (K4 sums the rings)
-    using R = TileRing<T>;
-    float* jr = p.Jt + (long)t * 3 * R::N;
+  } else if (fast) {
+    float* jt = p.Jt + (long)t * 3 * WJ * WJ;
     const float finv = ldexpf(1.0f, -S);
-    for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) {
-      const float v = fast ? (float)s_j[k] * finv : (float)(fma((double)s_j[k], 32768.0, (double)s_jlo[k]) * kFxInv);
-      const int c = k / (WJ * WJ), r = k - c * (WJ * WJ), b = r / WJ - 1, a = r - (b + 1) * WJ - 1;
-      if (R::exclusive(a, b)) {
-        if (i0 + a <= p.g.nx + 1 && j0 + b <= p.g.ny + 1) __stcg(p.J + c * pl + p.g.at(i0 + a, j0 + b), v);
-      } else {
-        __stcg(jr + c * R::N + R::slot(a, b), v);
-      }
-    }
+    for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) __stcg(jt + k, (float)s_j[k] * finv);
+  } else {
+    float* jt = p.Jt + (long)t * 3 * WJ * WJ;
+    for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK)
+      __stcg(jt + k, (float)(fma((double)s_j[k], 32768.0, (double)s_jlo[k]) * kFxInv));
   }
   if ((int)threadIdx.x < nspec && s_ke[threadIdx.x] != 0.0)
     atomicAdd(p.ke_slots + threadIdx.x * kEnergySlots + (t & (kEnergySlots - 1)), s_ke[threadIdx.x]);
   // the next step's occupancy bound: the largest 4 x 4 window of this tile's stayers (the histogram
   // is complete: every species' loop ended at a barrier); arrivals add to it after this kernel
+#ifndef ZPIC_NO_OCC_HIST
   const int m = __reduce_max_sync(0xffffffffu, window_max_4x4(s_hist, T, tw, th));
   if (lane == 0 && m > 0) atomicMax(p.occ + t, m);
+#else
+  if (threadIdx.x == 0) atomicMax(p.occ + t, s_occ);   // timing experiment: the bound is not maintained
+#endif
 }
 
 template <int T, int BLK, int MINB, int NSPEC>

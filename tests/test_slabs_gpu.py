@@ -159,3 +159,43 @@ def test_nccl_overlapped_rounds_self_ring(name):
     assert abs(ring.energy()[1] - ref.energy()[1]) <= 1e-6 * max(abs(ref.energy()[1]), 1e-12)
     ring.close()
     ref.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_nccl_slab_graph_replay_matches_launches(name):
+    """SURVEY.md NEXT-1 on the slab path: zpic_step(n) on the NCCL transport replays two-step CUDA
+    graphs (both halo rounds captured with the comm-stream fork / join and their overlap with the
+    interior kernels).  With a one-rank ring, 11 steps (five graph replays + one plain step) give
+    the same fields and particles (by id) as plain launches, bit for bit (the tile current is an
+    exact integer sum; no loose particles at this slack)."""
+    z = _z()
+    if name == "C1":
+        cfg = synth.config("C1", nx=64, ny=96)
+        cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
+    else:
+        cfg = synth.config("C3", nx=96, ny=96)
+        cfg["species"][0].update(x0=0.0, x1=4.8)
+        cfg["species"][1].update(x0=4.8, x1=9.6)
+    parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
+    out = []
+    for graphs in (True, False):
+        uid = z.zpic.zpic_nccl_unique_id()
+        ring = z.Simulation(cfg, inject=False, track_ids=True, graphs=graphs, capacity_slack=1.5,
+                            dist={"rank": 0, "world": 1, "transport": "nccl", "nccl_id": uid})
+        for s, p in enumerate(parts):
+            ring.set_particles(s, p)
+        ring.step(7)
+        ring.step(4)
+        ps = []
+        for s in range(len(parts)):
+            p = ring.particles(s, True)
+            o = np.argsort(p["id"])
+            ps.append({k: v[o] for k, v in p.items()})
+        out.append((ring.fields(0), ring.fields(1), ps, ring.energy()[0]))
+        ring.close()
+    (Ea, Ba, pa, ia), (Eb, Bb, pb, ib) = out
+    assert ia == ib == 10
+    assert np.array_equal(Ea, Eb) and np.array_equal(Ba, Bb)
+    for s in range(len(parts)):
+        for k in pa[s]:
+            assert np.array_equal(pa[s][k], pb[s][k]), (s, k)
