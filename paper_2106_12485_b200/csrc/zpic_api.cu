@@ -54,6 +54,7 @@ PList particle_msg_list(void* buf, int cap);
 void launch_recv_insert(const PushParams& p, const PList& lo, const PList& hi, cudaStream_t st);
 void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, cudaStream_t st);
 void launch_occupancy(const PushParams& p, cudaStream_t st);
+void launch_tile_scale(const PushParams& p, cudaStream_t st);
 }  // namespace zpic
 
 using namespace zpic;
@@ -236,11 +237,11 @@ void refresh_field_guards(zpic_ctx* c, float* F, bool is_E) {
 // ---- profiling ---------------------------------------------------------------------------
 constexpr int kSortEveryDefault = 0;   // steps between K2s re-sorts (ZPIC_SORT_EVERY overrides; 0 = off)
 enum KId { K_PUSH = 0, K_INSERT, K_ASSEMBLE, K_LOOSE, K_FOLD, K_HALO, K_FILTER, K_YEE, K_WINDOW, K_EPI, K_EXCHANGE,
-           K_MAIL, K_SORT, K_COUNT };
+           K_MAIL, K_SORT, K_SCALE, K_COUNT };
 const char* kNames[K_COUNT] = {"k_push_tiles", "k_insert",        "k_assemble_j", "k_push_loose",
                                "k_guard_fold", "k_apply_halo",    "k_filter_x",   "k_yee",
                                "k_inject_column", "k_epilogue",   "halo_exchange", "k_mail_gather",
-                               "k_sort_tiles"};
+                               "k_sort_tiles", "k_tile_scale"};
 
 struct ProfScope {
   zpic_ctx* c;
@@ -299,6 +300,7 @@ PushParams push_params(zpic_ctx* c) {
   for (int s = 0; s < c->nspecies; ++s) p.mail[s] = c->mail[s];
   p.fx_smin = c->opt.current_precision == 1 ? 99 : fx_smin();
   p.occ = c->occ;
+  p.tscale = c->tscale;
   p.qmax = 0.f;
   for (int s = 0; s < c->nspecies; ++s) p.qmax = std::max(p.qmax, std::fabs(c->sc[s].q));
   p.T = c->T; p.ntx = c->ntx; p.nty = c->nty;
@@ -604,6 +606,7 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     c->err = alloc_n<int>(c, 1);
     c->stats = alloc_n<int>(c, 4);
     c->occ = alloc_n<int32_t>(c, (size_t)c->ntiles);
+    c->tscale = alloc_n<int32_t>(c, (size_t)c->ntiles);
     if (c->opt.current_precision != 0 && c->opt.current_precision != 1)
       throw Fail{ZPIC_E_INVALID, "current_precision must be 0 or 1"};
     {
@@ -1092,6 +1095,11 @@ StepState step_phase_a(zpic_ctx* c) {
   if (p.commutative) {   // the tiles add into J: start from zero (guards included)
     ProfScope ps(c, K_ASSEMBLE);
     CUDA_OR_THROW(cudaMemsetAsync(c->J, 0, (size_t)3 * c->g.plane * sizeof(float), c->stream));
+  }
+  {
+    ProfScope ps(c, K_SCALE);
+    launch_tile_scale(p, c->stream);   // K1s: the tiles' current scales from the occupancy bounds
+    ++s.launches;
   }
   {
     ProfScope ps(c, K_PUSH);

@@ -113,6 +113,7 @@ struct PushParams {
   // maximum of its stayers' end cells, every insertion into the tile (K3m, K3, loose re-insertion,
   // halo receive, window injection) adds to it; -1 = unknown (the tile count bounds it).
   int32_t* occ;
+  int32_t* tscale;      // [ntiles] the scale exponent S of each tile's current this step (K1s)
   float qmax;           // max_s |q_s|
   int tile0;            // K1 launches over tiles [tile0, tile0 + grid) (the slab overlap splits it)
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
@@ -185,6 +186,7 @@ struct zpic_ctx {
   int* err;
   int* stats;      // [0] movers of last step, [1] spill count
   int32_t* occ = nullptr;   // [ntiles] occupancy bound of the fixed-point current (PushParams::occ)
+  int32_t* tscale = nullptr;   // [ntiles] per-tile scale exponent, from occ before every K1 (K1s)
   bool occ_stale = true;    // the particles were (re)loaded: recompute occ before the next step
   int cur;         // index of the current E/B buffer
   int64_t steps;

@@ -1226,6 +1226,34 @@ __global__ void __launch_bounds__(kBlock) k_occupancy(PushParams p) {
   __syncthreads();
   if (threadIdx.x == 0) p.occ[t] = s_max;
 }
+// K1s: every tile's fixed-point scale exponent for the K1 that follows: 2^S from a
+// bound on |J| at any node of the tile's block.  Every particle adds at most |q_s| to any node
+// (|v| < 1, the weights of its pieces sum to 1), and only the particles of a 4 x 4 cell window reach
+// a node: |J_node| <= occ * max_s |q_s|, occ the tile's occupancy bound (else the tile count:
+// sum_s n_s |q_s|).  The occupancy slot is reset here; K1 (its stayers' window maximum) and every
+// insertion after it (K3m, K3, loose re-insertion, halo receive, window injection) rebuild it.
+__global__ void k_tile_scale(PushParams p) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= p.ntx * p.nty) return;
+  const int occ = p.occ[t];
+  p.occ[t] = 0;
+  double bound = 0.0;
+  int ntot = 0;
+  for (int s = 0; s < p.nspecies; ++s) {
+    const int n = p.ps[s].cnt[t];
+    bound += (double)n * fabs((double)p.sc[s].q);
+    ntot += n;
+  }
+  int npart = ntot;
+  if (occ >= 0 && occ < ntot) {
+    bound = fmin(bound, (double)occ * (double)p.qmax);
+    npart = occ;
+  }
+  p.tscale[t] = fx_scale_exponent(bound, npart);
+}
+void launch_tile_scale(const PushParams& p, cudaStream_t st) {
+  k_tile_scale<<<(p.ntx * p.nty + kBlock - 1) / kBlock, kBlock, 0, st>>>(p);
+}
 void launch_occupancy(const PushParams& p, cudaStream_t st) {
   k_occupancy<<<p.ntx * p.nty, kBlock, 0, st>>>(p);
 }

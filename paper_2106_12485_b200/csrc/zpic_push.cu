@@ -106,7 +106,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   __shared__ int s_wsum[2][NW];
   __shared__ double s_ke[kMaxSpecies];
   __shared__ int s_hist[T * T];   // stayers per end cell (the occupancy bound of the next step)
-  __shared__ int s_occ;
+  __shared__ int s_occ;            // the tile current's scale exponent S
   if (threadIdx.x < kMaxSpecies) s_ke[threadIdx.x] = 0.0;
 
   const int t = blockIdx.x + p.tile0;
@@ -140,10 +140,9 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
           : "memory");
     }
     for (int k = threadIdx.x; k < T * T; k += BLK) s_hist[k] = 0;
-    if (threadIdx.x == 32) {   // this step's occupancy bound; the slot collects the next step's
-      s_occ = p.occ[t];
-      p.occ[t] = 0;
-    }
+    // the tile current's scale exponent S, computed by K1s from this tile's occupancy bound
+    // before this kernel (a plain load: nothing of it stays live in the particle loop)
+    if (threadIdx.x == 32) s_occ = p.tscale[t];
     __syncthreads();   // the barrier is initialised before anyone waits on it
     asm volatile(
         "{\n .reg .pred done;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 done, [%0], 0;\n"
@@ -159,31 +158,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
     }
     __syncthreads();   // the boxes are consumed before the current is zeroed and the rings are used
   }
-  // fixed-point scale of this tile's current: 2^S from a bound on |J| at any node of the block.
-  // Every particle adds at most |q_s| to any node (|v| < 1, the weights of its pieces sum to 1), and
-  // only the particles of a 4 x 4 cell window reach a node: |J_node| <= occ * max_s |q_s| with occ
-  // the tile's occupancy bound (else the tile count: sum_s n_s |q_s|).  DESIGN.md §2.
-  double bound = 0.0;
-  int ntot = 0;
-  for (int s = 0; s < nspec; ++s) {
-    const int n = p.ps[s].cnt[t];
-    bound += (double)n * fabs((double)p.sc[s].q);
-    ntot += n;
-  }
-  int npart = ntot;
-#ifdef ZPIC_OLD_BOUND
-  if (false) {
-#else
-  if (s_occ >= 0 && s_occ < ntot) {
-#endif
-    bound = fmin(bound, (double)s_occ * (double)p.qmax);
-    npart = s_occ;
-  }
-#ifdef ZPIC_SCAP
-  const int S = min(fx_scale_exponent(bound, npart), ZPIC_SCAP);
-#else
-  const int S = fx_scale_exponent(bound, npart);
-#endif
+  const int S = s_occ;   // (the tile's scale exponent, see above)
   // CTA-uniform choice: one int32 atomic per node at scale 2^S, else (S below the floor: a tile so
   // dense that 2^-S would be coarse, or current_precision = exact) the exact two-word form
   const bool fast = S >= p.fx_smin;
@@ -402,18 +377,19 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   };
   if (fast) push_all(SmemCurrentI32<WJ>{s_j}, ldexpf(1.0f, S));
   else push_all(SmemCurrentFx<WJ>{s_j, s_jlo}, kFxScale);
+  const bool fast2 = s_occ >= p.fx_smin;   // re-derived after the loop (no register kept live)
   if (p.commutative) {
     // "commutative" ghost current: add the block into J with global atomics;
     // nodes a tile cannot reach stay zero and are skipped (they may lie outside the guards)
     for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) {
-      const float v = fast ? (float)s_j[k] * ldexpf(1.0f, -S)
+      const float v = fast2 ? (float)s_j[k] * ldexpf(1.0f, -s_occ)
                            : (float)(fma((double)s_j[k], 32768.0, (double)s_jlo[k]) * kFxInv);
       const int c = k / (WJ * WJ), r = k % (WJ * WJ);
       if (v != 0.0f) atomicAdd(p.J + c * pl + p.g.at(i0 - 1 + r % WJ, j0 - 1 + r / WJ), v);
     }
-  } else if (fast) {
+  } else if (fast2) {
     float* jt = p.Jt + (long)t * 3 * WJ * WJ;
-    const float finv = ldexpf(1.0f, -S);
+    const float finv = ldexpf(1.0f, -s_occ);
     for (int k = threadIdx.x; k < 3 * WJ * WJ; k += BLK) __stcg(jt + k, (float)s_j[k] * finv);
   } else {
     float* jt = p.Jt + (long)t * 3 * WJ * WJ;
@@ -427,8 +403,6 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
 #ifndef ZPIC_NO_OCC_HIST
   const int m = __reduce_max_sync(0xffffffffu, window_max_4x4(s_hist, T, tw, th));
   if (lane == 0 && m > 0) atomicMax(p.occ + t, m);
-#else
-  if (threadIdx.x == 0) atomicMax(p.occ + t, s_occ);   // timing experiment: the bound is not maintained
 #endif
 }
 
