@@ -52,8 +52,9 @@ void launch_apply_j_halo(float* J, const GridDesc& g, const float* rup, const fl
 size_t particle_msg_bytes(int cap);
 PList particle_msg_list(void* buf, int cap);
 void launch_recv_insert(const PushParams& p, const PList& lo, const PList& hi, cudaStream_t st);
-void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, cudaStream_t st);
+void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, int* stats, cudaStream_t st);
 void launch_occupancy(const PushParams& p, cudaStream_t st);
+void launch_loose_drop_species(const PList& L, int s, const PList& out, cudaStream_t st);
 void launch_tile_scale(const PushParams& p, cudaStream_t st);
 }  // namespace zpic
 
@@ -935,7 +936,7 @@ static void maybe_sort(zpic_ctx* c) {
   for (int s = 0; s < c->nspecies; ++s) {
     if (!c->ps[s].data) continue;
     ProfScope pr(c, K_SORT);
-    launch_sort_tiles(c->ps[s], c->T, c->ntx, c->ntiles, c->stream);
+    launch_sort_tiles(c->ps[s], c->T, c->ntx, c->ntiles, c->stats, c->stream);
     CUDA_OR_THROW(cudaGetLastError());
     c->launches += 1;
   }
@@ -1007,6 +1008,40 @@ static bool load_chunked(zpic_ctx* c, int s, int64_t n, const int32_t* ix, const
   return true;
 }
 
+// Species s emptied: its tiles (counts 0) and its loose-list entries (the live loose list is
+// compacted through the other, idle spill list).  zpic_set_particles starts from here and comes back
+// here on any error, so a failed upload leaves the species empty (include/zpic.h).
+static void clear_species(zpic_ctx* c, int s) {
+  c->occ_stale = true;
+  if (c->ps[s].data) CUDA_OR_THROW(cudaMemsetAsync(c->ps[s].cnt, 0, (size_t)c->ntiles * 4, c->stream));
+  PList& live = c->spill[c->steps & 1];
+  PList& idle = c->spill[(c->steps & 1) ^ 1];
+  if (!live.count || !idle.count) return;
+  int nl = 0;
+  CUDA_OR_THROW(cudaMemcpyAsync(&nl, live.count, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  if (nl == 0) return;
+  CUDA_OR_THROW(cudaMemsetAsync(idle.count, 0, 4, c->stream));
+  launch_loose_drop_species(live, s, idle, c->stream);
+  CUDA_OR_THROW(cudaGetLastError());
+  int m = 0;
+  CUDA_OR_THROW(cudaMemcpyAsync(&m, idle.count, 4, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  m = std::min(m, idle.cap);
+  const size_t b = (size_t)m * 4;
+  if (m > 0) {
+    for (auto f : {std::make_pair((void*)live.cell, (void*)idle.cell), std::make_pair((void*)live.x, (void*)idle.x),
+                   std::make_pair((void*)live.y, (void*)idle.y), std::make_pair((void*)live.ux, (void*)idle.ux),
+                   std::make_pair((void*)live.uy, (void*)idle.uy), std::make_pair((void*)live.uz, (void*)idle.uz),
+                   std::make_pair((void*)live.species, (void*)idle.species)})
+      CUDA_OR_THROW(cudaMemcpyAsync(f.first, f.second, b, cudaMemcpyDeviceToDevice, c->stream));
+    if (live.id && idle.id) CUDA_OR_THROW(cudaMemcpyAsync(live.id, idle.id, b, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  CUDA_OR_THROW(cudaMemcpyAsync(live.count, &m, 4, cudaMemcpyHostToDevice, c->stream));
+  CUDA_OR_THROW(cudaMemsetAsync(idle.count, 0, 4, c->stream));
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+}
+
 zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t* ix, const int32_t* iy, const float* x,
                                const float* y, const float* ux, const float* uy, const float* uz, const uint32_t* id) {
   if (!c) return ZPIC_E_INVALID;
@@ -1015,6 +1050,7 @@ zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t*
   }
   drop_graphs(c);
   try {
+    clear_species(c, s);   // the old particles of species s go (tiles and loose list)
     if (load_chunked(c, s, n, ix, iy, x, y, ux, uy, uz, id)) {
       size_lists(c);
       return check_sticky(c);
@@ -1043,6 +1079,7 @@ zpic_status zpic_set_particles(zpic_ctx* c, int32_t s, int64_t n, const int32_t*
     size_lists(c);
   } catch (const Fail& f) {
     c->last_error = f.msg;
+    try { clear_species(c, s); } catch (const Fail&) {}   // a failed upload leaves the species empty
     return f.st;
   }
   return check_sticky(c);
@@ -1661,7 +1698,7 @@ zpic_status zpic_counters(zpic_ctx* c, int64_t* out, int32_t n) {
   if (!c || !out) return ZPIC_E_INVALID;
   zpic_status st = check_sticky(c);
   if (st != ZPIC_OK) return st;
-  int stats[4] = {0, 0, 0, 0};
+  int stats[4] = {0, 0, 0, 0};   // [0] movers of the last step, [1] loose, [2] / [3] tiles K2s sorted / left
   cudaMemcpy(stats, c->stats, sizeof(stats), cudaMemcpyDeviceToHost);
   int64_t total = 0;
   int maxfill = 0;
@@ -1672,8 +1709,9 @@ zpic_status zpic_counters(zpic_ctx* c, int64_t* out, int32_t n) {
   }
   int nl = 0;
   cudaMemcpy(&nl, c->spill[c->steps & 1].count, 4, cudaMemcpyDeviceToHost);
-  const int64_t v[8] = {total + nl, stats[0], maxfill, c->repacks, c->steps, c->ntiles, c->launches, c->T};
-  for (int k = 0; k < n && k < 8; ++k) out[k] = v[k];
+  const int64_t v[10] = {total + nl, stats[0], maxfill, c->repacks, c->steps, c->ntiles, c->launches, c->T,
+                          stats[2], stats[3]};
+  for (int k = 0; k < n && k < 10; ++k) out[k] = v[k];
   return ZPIC_OK;
 }
 

@@ -237,7 +237,7 @@ constexpr int kSortK = 9;   // particles per thread: nstage <= kSortBlock * kSor
 template <int T>
 constexpr int kSortBits = T == 16 ? 16384 : 32768;
 template <int T>
-__global__ void __launch_bounds__(kSortBlock, 2) k_sort_tiles(PStore ps, int ntx, int nstage) {
+__global__ void __launch_bounds__(kSortBlock, 2) k_sort_tiles(PStore ps, int ntx, int nstage, int* stats) {
   constexpr int NC = T * T, RMAX = kSortBits<T> / NC, NW = kSortBits<T> / 32, PER = NW / kSortBlock > 0 ? NW / kSortBlock : 1;
   extern __shared__ __align__(16) uint32_t sort_smem[];
   __shared__ int s_cnt[NC];
@@ -247,7 +247,11 @@ __global__ void __launch_bounds__(kSortBlock, 2) k_sort_tiles(PStore ps, int ntx
   __shared__ int s_ovf;
   const int t = blockIdx.x;
   const int n = min(ps.cnt[t], ps.cap);
-  if (n > nstage) return;   // CTA-uniform: this tile stays unsorted
+  if (n > nstage) {   // CTA-uniform: this tile stays unsorted (counted: zpic_counters "unsorted_tiles")
+    if (threadIdx.x == 0) atomicAdd(stats + 3, 1);
+    return;
+  }
+  if (threadIdx.x == 0 && n > 0) atomicAdd(stats + 2, 1);
   const int nf = ps.nf;
   uint32_t* stage = sort_smem;                                                        // [nf - 1][nstage]
   unsigned short* sidx = reinterpret_cast<unsigned short*>(sort_smem + (nf - 1) * nstage);   // [nstage]
@@ -347,21 +351,21 @@ int sort_stage_capacity(int nf) {
   const int per = 4 * (nf - 1) + 4;   // staged fields + slot index + local cell
   return std::min(kSortBlock * kSortK, (int)((104 * 1024) / per) / 32 * 32);   // 2 x (dyn + static + 1 KB) <= 228 KB
 }
-void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, cudaStream_t st) {
+void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, int* stats, cudaStream_t st) {
   const int nstage = sort_stage_capacity(ps.nf);
   const size_t smem = (size_t)nstage * (4 * (ps.nf - 1) + 4);
   switch (T) {
     case 8:
       cudaFuncSetAttribute(k_sort_tiles<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_sort_tiles<8><<<ntiles, kSortBlock, smem, st>>>(ps, ntx, nstage);
+      k_sort_tiles<8><<<ntiles, kSortBlock, smem, st>>>(ps, ntx, nstage, stats);
       break;
     case 16:
       cudaFuncSetAttribute(k_sort_tiles<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_sort_tiles<16><<<ntiles, kSortBlock, smem, st>>>(ps, ntx, nstage);
+      k_sort_tiles<16><<<ntiles, kSortBlock, smem, st>>>(ps, ntx, nstage, stats);
       break;
     case 32:
       cudaFuncSetAttribute(k_sort_tiles<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      k_sort_tiles<32><<<ntiles, kSortBlock, smem, st>>>(ps, ntx, nstage);
+      k_sort_tiles<32><<<ntiles, kSortBlock, smem, st>>>(ps, ntx, nstage, stats);
       break;
   }
 }
@@ -1100,6 +1104,19 @@ __global__ void k_loose_extract(PList L, int s, int y0, int32_t* ix, int32_t* iy
     x[o] = L.x[k]; y[o] = L.y[k]; ux[o] = L.ux[k]; uy[o] = L.uy[k]; uz[o] = L.uz[k];
     if (id) id[o] = L.id ? L.id[k] : 0u;
   }
+}
+// The loose-list entries of every species but s, appended to `out` (zpic_set_particles replaces
+// species s: its loose particles go with its old tile contents).
+__global__ void k_loose_drop_species(PList L, int s, PList out) {
+  const int n = min(*L.count, L.cap);
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    if (L.species[k] == s) continue;
+    const int o = atomicAdd(out.count, 1);
+    list_put(out, o, L.cell[k], L.x[k], L.y[k], L.ux[k], L.uy[k], L.uz[k], L.id ? L.id[k] : 0u, L.species[k]);
+  }
+}
+void launch_loose_drop_species(const PList& L, int s, const PList& out, cudaStream_t st) {
+  k_loose_drop_species<<<148 * 2, kBlock, 0, st>>>(L, s, out);
 }
 void launch_loose_extract(const PList& L, int s, int y0, int64_t out0, int32_t* ix, int32_t* iy, float* x, float* y,
                           float* ux, float* uy, float* uz, uint32_t* id, int* counter, cudaStream_t st) {

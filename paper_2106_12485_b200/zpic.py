@@ -214,9 +214,10 @@ def zpic_energy(ctx, nspecies):
 
 
 def zpic_counters(ctx):
-    out = (ctypes.c_int64 * 8)()
-    _check(_lib.zpic_counters(ctx, out, 8), ctx)
-    keys = ("particles", "movers", "max_fill_permille", "repacks", "steps", "tiles", "launches", "tile")
+    out = (ctypes.c_int64 * 10)()
+    _check(_lib.zpic_counters(ctx, out, 10), ctx)
+    keys = ("particles", "movers", "max_fill_permille", "repacks", "steps", "tiles", "launches", "tile",
+            "sorted_tiles", "unsorted_tiles")
     return dict(zip(keys, list(out)))
 
 

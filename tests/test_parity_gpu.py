@@ -159,8 +159,8 @@ def test_c4_lwfa_window_filter_reduced():
 def test_paper_weibel_pairs_reduced(tile):
     """the paper's Weibel case, an electron and a positron
     cloud (m_q = -1, +1) counter-streaming along z at 256 ppc each, on 24 x 20 cells, 10 steps.
-    16 x 16 tiles hold 2 x 65536 particles (the tile current takes the exact two-word form),
-    8 x 8 tiles the int32 form."""
+    16 x 16 tiles hold 2 x 65536 particles, 8 x 8 tiles 2 x 16384: both take the one-word current
+    at S ~ 26 (a 4 x 4 window holds 8192 particles of charge 1/512: |J_node| <= 16)."""
     cfg = synth.config("P-WEIBEL", nx=24, ny=20)
     print(_parity_run(cfg, 10, tile=tile, check_every_step=False))
 
@@ -543,8 +543,10 @@ def test_periodic_resort_is_invisible(graphs, tile, monkeypatch):
     cfg = synth.config("C2", nx=72, ny=56)
     for sp in cfg["species"]:
         sp["uth"] = (0.3, 0.3, 0.3)
+        sp["ppc"] = (2, 2)      # 16 x 16 tiles of 2 species x 1024 particles fit K2s's stage (7 words with ids)
     parts = [synth.species_particles(cfg, s) for s in range(2)]
     out = []
+    sorted_tiles = []
     for every in ("1", "0"):
         monkeypatch.setenv("ZPIC_SORT_EVERY", every)
         g = _z().Simulation(cfg, inject=False, track_ids=True, tile=tile, capacity_slack=1.5, graphs=graphs)
@@ -558,7 +560,11 @@ def test_periodic_resort_is_invisible(graphs, tile, monkeypatch):
             o = np.argsort(p["id"])
             ps.append({k: v[o] for k, v in p.items()})
         out.append((g.fields(0), g.fields(1), g.fields(2), ps, g.energy()))
+        cnt = g.counters()
+        sorted_tiles.append((cnt["sorted_tiles"], cnt["unsorted_tiles"]))
         g.close()
+    assert sorted_tiles[0][0] > 0 and sorted_tiles[0][1] == 0, sorted_tiles    # K2s really ran on every tile
+    assert sorted_tiles[1] == (0, 0)
     (Ea, Ba, Ja, pa, ea), (Eb, Bb, Jb, pb, eb) = out
     assert np.array_equal(Ja, Jb) and np.array_equal(Ea, Eb) and np.array_equal(Ba, Bb)
     for s in range(2):
@@ -576,6 +582,7 @@ def test_resort_rank_overflow_and_crowded_cells(monkeypatch):
     and every particle survives."""
     cfg = synth.config("C1", nx=64, ny=64)
     cfg["species"][0]["uth"] = (0.2, 0.2, 0.2)
+    cfg["species"][0]["ppc"] = (2, 2)     # 1024 per 16 x 16 tile (+ the cluster): fits K2s's stage
     bg = synth.species_particles(cfg, 0)
     rng = np.random.default_rng(7)
     k = 200
@@ -593,9 +600,36 @@ def test_resort_rank_overflow_and_crowded_cells(monkeypatch):
         p = g.particles(0, True)
         o = np.argsort(p["id"])
         out.append(({f: v[o] for f, v in p.items()}, g.fields(0), g.fields(1)))
+        if every == "1":
+            cnt = g.counters()
+            assert cnt["sorted_tiles"] > 0 and cnt["unsorted_tiles"] == 0, cnt
         g.close()
     (pa, Ea, Ba), (pb, Eb, Bb) = out
     assert len(pa["id"]) == len(parts["x"]) and np.array_equal(pa["id"], np.sort(parts["id"]))
     assert np.array_equal(Ea, Eb) and np.array_equal(Ba, Bb)
     for f in pa:
         assert np.array_equal(pa[f], pb[f]), f
+
+
+def test_set_particles_replaces_the_species_loose_particles_included():
+    """zpic_set_particles replaces a species: after steps that left particles in the loose list
+    (tile slack 1.0), a new upload of that species is the whole species — nothing of the old set
+    survives in the tiles or the loose list — and a rejected upload leaves it empty."""
+    cfg = synth.config("C1", nx=48, ny=48)
+    cfg["species"][0]["uth"] = (0.4, 0.4, 0.4)
+    parts = synth.species_particles(cfg, 0)
+    g = gpu_from_particles(cfg, [parts], slack=1.0)
+    g.step(4)
+    assert g.counters()["particles"] == len(parts["x"])
+    half = {k: v[: len(v) // 2].copy() for k, v in parts.items()}
+    g.set_particles(0, half)
+    assert g.counters()["particles"] == len(half["x"])
+    got = g.particles(0, True)
+    assert np.array_equal(np.sort(got["id"]), np.sort(half["id"]))
+    bad = dict(half)
+    bad["x"] = half["x"].copy()
+    bad["x"][3] = 1.5
+    with pytest.raises(_z().ZpicError):
+        g.set_particles(0, bad)
+    assert g.counters()["particles"] == 0
+    g.close()
