@@ -236,7 +236,8 @@ zpic_status zpic_layout(zpic_ctx* ctx, int32_t* y0, int32_t* ny_local);
  * tile occupancy / capacity in per-mille, out[3] re-packs done, out[4] steps taken,
  * out[5] number of tiles, out[6] kernels launched by zpic_step so far, out[7] tile size T,
  * out[8] / out[9] tiles the periodic in-tile re-sort (K2s, ZPIC_SORT_EVERY) sorted / left unsorted
- * (a tile holding more particles than its shared-memory stage) so far.  n <= 10 entries are written. */
+ * (a tile holding more particles than its shared-memory stage) so far, out[10] particles in the
+ * loose list now (no room in their tile; pushed from global memory).  n <= 11 entries are written. */
 zpic_status zpic_counters(zpic_ctx* ctx, int64_t* out, int32_t n);
 
 /* Per-kernel device time (ms) summed over the steps since the last call, when

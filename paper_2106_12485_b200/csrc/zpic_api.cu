@@ -1709,9 +1709,9 @@ zpic_status zpic_counters(zpic_ctx* c, int64_t* out, int32_t n) {
   }
   int nl = 0;
   cudaMemcpy(&nl, c->spill[c->steps & 1].count, 4, cudaMemcpyDeviceToHost);
-  const int64_t v[10] = {total + nl, stats[0], maxfill, c->repacks, c->steps, c->ntiles, c->launches, c->T,
-                          stats[2], stats[3]};
-  for (int k = 0; k < n && k < 10; ++k) out[k] = v[k];
+  const int64_t v[11] = {total + nl, stats[0], maxfill, c->repacks, c->steps, c->ntiles, c->launches, c->T,
+                          stats[2], stats[3], nl};
+  for (int k = 0; k < n && k < 11; ++k) out[k] = v[k];
   return ZPIC_OK;
 }
 

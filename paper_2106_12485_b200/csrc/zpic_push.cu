@@ -231,12 +231,19 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         qvz = qs * uz * rg;
         x0 = x; y0 = y;
         const float x1 = __fadd_rn(x, dxp), y1 = __fadd_rn(y, dyp);
-        int di = (x1 >= 1.0f) - (x1 < 0.0f), dj = (y1 >= 1.0f) - (y1 < 0.0f);
-        cross = di || dj;
+        const float fx1 = floorf(x1), fy1 = floorf(y1);
+        int di = (int)fx1, dj = (int)fy1;
+        cross = (di | dj) != 0;
         // a path inside its start cell is one piece, deposited now; a crossing path is queued
         // and split in the drain (the same pieces path_crossings gives, t1 = 1: fma(1, d, x) = x1)
         if (!cross) deposit_seg(A, Seg{lx, ly, x, y, x1, y1, qvz}, jxs, jys);
-        renormalise(x1, y1, di, dj, x, y);
+        {   // x1 - floor(x1) equals x1 - di exactly; the R6 rule as in renormalise
+          float xn = x1 - fx1, yn = y1 - fy1;
+          if (xn >= 1.0f) { xn = 0.0f; di += 1; }
+          if (yn >= 1.0f) { yn = 0.0f; dj += 1; }
+          x = xn;
+          y = yn;
+        }
         di -= p.shift;   // moving window: the cell index follows the shift at the end of the step
         ix += di; iy += dj;
         if ((unsigned)(lx + di) < (unsigned)tw && (unsigned)(ly + dj) < (unsigned)th) stay = true;
@@ -260,11 +267,47 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
           __syncwarp();   // the drained entries are read before the next put overwrites them
         }
       }
-      if (valid) {
-        if (stay) {
-#ifndef ZPIC_NO_OCC_HIST
-          atomicAdd(&s_hist[(iy - j0) * T + (ix - i0)], 1);
-#endif
+      if (valid && stay) {
+        atomicAdd(&s_hist[(iy - j0) * T + (ix - i0)], 1);
+        const int ncell_ = pack_cell(ix, iy);
+        if (!p.skip_cell_store || ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);
+        __stcs(pp + F_X * 32, __float_as_uint(x)); __stcs(pp + F_Y * 32, __float_as_uint(y));
+        __stcs(pp + F_UX * 32, __float_as_uint(ux)); __stcs(pp + F_UY * 32, __float_as_uint(uy));
+        __stcs(pp + F_UZ * 32, __float_as_uint(uz));
+      }
+      // leavers (~20 % of the warp-chunks at C5): one warp-uniform branch for the hole record, the
+      // mailbox and the mover list
+      const bool leave = valid && !stay;
+      if (__any_sync(0xffffffffu, leave)) {
+        if (leave) {
+          pp[F_CELL * 32] = (uint32_t)kHole;
+          const int h = atomicAdd(&s_cnt[0], 1);
+          if (h < kHCap) s_holes[h] = i;
+          else s_cnt[3] = 1;
+        }
+        // this tile's mailbox for the direction of travel, else (box full, slab exit) the list
+        int mslot = -1;
+        if (mdir >= 0) {
+          const int k = atomicAdd(&s_mbc[mdir], 1);
+          if (k < mail_cap(p.mail[s], mdir)) mslot = k;
+        }
+        const bool glob = move && mslot < 0;
+        const int m = warp_reserve(p.movers.count, glob);
+        if (mslot >= 0) {
+          const MailBox& M = p.mail[s];
+          uint32_t* q = M.data + ((long)t * M.per_tile + mail_offset(M, mdir) + mslot) * M.nf;
+          q[F_CELL] = (uint32_t)pack_cell(ix, iy);
+          q[F_X] = __float_as_uint(x); q[F_Y] = __float_as_uint(y);
+          q[F_UX] = __float_as_uint(ux); q[F_UY] = __float_as_uint(uy);
+          q[F_UZ] = __float_as_uint(uz);
+          if (M.nf > F_ID) q[F_ID] = id;
+        }
+        if (glob) {
+          if (m < p.movers.cap) list_put(p.movers, m, pack_cell(ix, iy), x, y, ux, uy, uz, id, s);
+          else atomicOr(p.err, ERR_OVERFLOW);
+        }
+      }
+    }
           const int ncell_ = pack_cell(ix, iy);
           if (!p.skip_cell_store || ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);
           __stcs(pp + F_X * 32, __float_as_uint(x)); __stcs(pp + F_Y * 32, __float_as_uint(y));
@@ -299,6 +342,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         else atomicOr(p.err, ERR_OVERFLOW);
       }
     }
+#endif
     if (lane < qn) drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys, p.err);
     // kinetic energy: warp reduction, one shared fp64 add per warp, one global add per CTA
     for (int o = 16; o > 0; o >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, o);
@@ -400,10 +444,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
     atomicAdd(p.ke_slots + threadIdx.x * kEnergySlots + (t & (kEnergySlots - 1)), s_ke[threadIdx.x]);
   // the next step's occupancy bound: the largest 4 x 4 window of this tile's stayers (the histogram
   // is complete: every species' loop ended at a barrier); arrivals add to it after this kernel
-#ifndef ZPIC_NO_OCC_HIST
   const int m = __reduce_max_sync(0xffffffffu, window_max_4x4(s_hist, T, tw, th));
   if (lane == 0 && m > 0) atomicMax(p.occ + t, m);
-#endif
 }
 
 template <int T, int BLK, int MINB, int NSPEC>

@@ -214,10 +214,10 @@ def zpic_energy(ctx, nspecies):
 
 
 def zpic_counters(ctx):
-    out = (ctypes.c_int64 * 10)()
-    _check(_lib.zpic_counters(ctx, out, 10), ctx)
+    out = (ctypes.c_int64 * 11)()
+    _check(_lib.zpic_counters(ctx, out, 11), ctx)
     keys = ("particles", "movers", "max_fill_permille", "repacks", "steps", "tiles", "launches", "tile",
-            "sorted_tiles", "unsorted_tiles")
+            "sorted_tiles", "unsorted_tiles", "loose")
     return dict(zip(keys, list(out)))
 
 
