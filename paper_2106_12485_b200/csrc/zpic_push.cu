@@ -308,41 +308,6 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         }
       }
     }
-          const int ncell_ = pack_cell(ix, iy);
-          if (!p.skip_cell_store || ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);
-          __stcs(pp + F_X * 32, __float_as_uint(x)); __stcs(pp + F_Y * 32, __float_as_uint(y));
-          __stcs(pp + F_UX * 32, __float_as_uint(ux)); __stcs(pp + F_UY * 32, __float_as_uint(uy));
-          __stcs(pp + F_UZ * 32, __float_as_uint(uz));
-        } else {
-          pp[F_CELL * 32] = (uint32_t)kHole;
-          const int h = atomicAdd(&s_cnt[0], 1);
-          if (h < kHCap) s_holes[h] = i;
-          else s_cnt[3] = 1;
-        }
-      }
-      // leavers: this tile's mailbox for their direction, else (box full, slab exit) the list
-      int mslot = -1;
-      if (mdir >= 0) {
-        const int k = atomicAdd(&s_mbc[mdir], 1);
-        if (k < mail_cap(p.mail[s], mdir)) mslot = k;
-      }
-      const bool glob = move && mslot < 0;
-      const int m = warp_reserve(p.movers.count, glob);
-      if (mslot >= 0) {
-        const MailBox& M = p.mail[s];
-        uint32_t* q = M.data + ((long)t * M.per_tile + mail_offset(M, mdir) + mslot) * M.nf;
-        q[F_CELL] = (uint32_t)pack_cell(ix, iy);
-        q[F_X] = __float_as_uint(x); q[F_Y] = __float_as_uint(y);
-        q[F_UX] = __float_as_uint(ux); q[F_UY] = __float_as_uint(uy);
-        q[F_UZ] = __float_as_uint(uz);
-        if (M.nf > F_ID) q[F_ID] = id;
-      }
-      if (glob) {
-        if (m < p.movers.cap) list_put(p.movers, m, pack_cell(ix, iy), x, y, ux, uy, uz, id, s);
-        else atomicOr(p.err, ERR_OVERFLOW);
-      }
-    }
-#endif
     if (lane < qn) drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys, p.err);
     // kinetic energy: warp reduction, one shared fp64 add per warp, one global add per CTA
     for (int o = 16; o > 0; o >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, o);
