@@ -782,3 +782,17 @@ def test_window_injection_follows_the_profile_beyond_the_box():
         sim = OracleSim(nx, ny, 0.1, 0.1, 0.05, [bad], bc=(2, 1))
         with pytest.raises(ValueError):
             sim._shift_window()
+
+
+def test_cell_index_exemption_is_per_axis():
+    """R23: an index mismatch is excused only when the oracle's offset is within 2^-20 of a cell
+    edge on the mismatching axis (parity_util.compare_particles)."""
+    from parity_util import compare_particles
+    o = {"ix": np.array([3, 3, 3]), "iy": np.array([5, 5, 5]), "x": np.array([1e-9, 0.5, 0.5]),
+         "y": np.array([0.5, 1e-9, 0.5]), "ux": np.zeros(3), "uy": np.zeros(3), "uz": np.zeros(3),
+         "id": np.arange(3)}
+    g = dict(o)
+    g["ix"] = np.array([2, 2, 3])   # particle 0: x near its edge (excused); particle 1: y near, x differs
+    g["iy"] = np.array([5, 5, 5])
+    c = compare_particles(g, o, 16, 16)
+    assert c["cell_bad"] == 1
