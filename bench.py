@@ -78,8 +78,8 @@ def launch_ranks(args, argv):
 
 def k1_traffic(config, nx, ny):
     """DRAM bytes per K1 launch from the committed ncu capture of the same workload
-    (profiles/r1_k1_traffic_c5.json), else None."""
-    p = os.path.join(ROOT, "profiles", "r1_k1_traffic_c5.json")
+    (profiles/r2_k1_traffic_c5.json), else None."""
+    p = os.path.join(ROOT, "profiles", "r2_k1_traffic_c5.json")
     if config == "C5" and (nx, ny) == (8192, 8192) and os.path.exists(p):
         return json.load(open(p))["per_launch_bytes"]
     return None
@@ -439,7 +439,7 @@ def main():
                      "achieved_dram": traffic / k1_avg_s / 1e9 if (traffic and k1_n) else None,
                      "frac_dram": traffic / k1_avg_s / 1e9 / peak if (traffic and k1_n) else None,
                      "frac_nominal_8tbs": achieved / 8000.0 if k1_n else None,
-                     "traffic_source": "profiles/r1_k1_traffic_c5.json (ncu dram__bytes_read+write, C5)",
+                     "traffic_source": "profiles/r2_k1_traffic_c5.json (ncu dram__bytes_read+write, C5)",
                      "kernel": "k_push_tiles", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": k1_avg_s * 1e3 if k1_n else None,
                      **({"note": "--graphs: CUDA-graph replay, no per-kernel events"} if args.graphs else {})},
