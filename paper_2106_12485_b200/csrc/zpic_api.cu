@@ -53,7 +53,7 @@ size_t particle_msg_bytes(int cap);
 PList particle_msg_list(void* buf, int cap);
 void launch_recv_insert(const PushParams& p, const PList& lo, const PList& hi, cudaStream_t st);
 void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, int* stats, cudaStream_t st);
-void launch_occupancy(const PushParams& p, cudaStream_t st);
+void launch_occupancy(const PushParams& p, cudaStream_t st, int mode = 0);
 void launch_loose_drop_species(const PList& L, int s, const PList& out, cudaStream_t st);
 void launch_tile_scale(const PushParams& p, cudaStream_t st);
 }  // namespace zpic
@@ -302,6 +302,8 @@ PushParams push_params(zpic_ctx* c) {
   p.fx_smin = c->opt.current_precision == 1 ? 99 : fx_smin();
   p.occ = c->occ;
   p.tscale = c->tscale;
+  p.hist = c->hist;
+  p.check_occ = c->check_occ;
   p.qmax = 0.f;
   for (int s = 0; s < c->nspecies; ++s) p.qmax = std::max(p.qmax, std::fabs(c->sc[s].q));
   p.T = c->T; p.ntx = c->ntx; p.nty = c->nty;
@@ -445,6 +447,7 @@ zpic_status check_sticky(zpic_ctx* c) {
     return ZPIC_E_OVERFLOW;
   }
   if (err & ERR_MIGRATION) { c->last_error = "a particle moved >= 1 cell in one step"; return ZPIC_E_MIGRATION; }
+  if (err & ERR_HIST) { c->last_error = "tile cell histogram / occupancy bound inconsistent (ZPIC_CHECK_OCC)"; return ZPIC_E_STATE; }
   return ZPIC_OK;
 }
 
@@ -608,6 +611,11 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     c->stats = alloc_n<int>(c, 4);
     c->occ = alloc_n<int32_t>(c, (size_t)c->ntiles);
     c->tscale = alloc_n<int32_t>(c, (size_t)c->ntiles);
+    c->hist = alloc_n<int32_t>(c, (size_t)c->ntiles * c->T * c->T);
+    {
+      const char* e = getenv("ZPIC_CHECK_OCC");   // read per context (tests)
+      c->check_occ = e ? atoi(e) : 0;
+    }
     if (c->opt.current_precision != 0 && c->opt.current_precision != 1)
       throw Fail{ZPIC_E_INVALID, "current_precision must be 0 or 1"};
     {
@@ -1135,6 +1143,7 @@ StepState step_phase_a(zpic_ctx* c) {
   }
   {
     ProfScope ps(c, K_SCALE);
+    if (c->check_occ) { launch_occupancy(p, c->stream, 1); ++s.launches; }   // verify hist / occ (tests)
     launch_tile_scale(p, c->stream);   // K1s: the tiles' current scales from the occupancy bounds
     ++s.launches;
   }

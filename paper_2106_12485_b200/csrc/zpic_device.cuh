@@ -107,6 +107,7 @@ __device__ __forceinline__ void insert_particle(const PushParams& p, int s, int 
   const int cell = pack_cell(ix, iy);
   if (slot < ps.cap) {
     atomicAdd(p.occ + t, 1);   // the tile's occupancy bound grows with every arrival
+    atomicAdd(p.hist + (long)t * p.T * p.T + (iy - (iy / p.T) * p.T) * p.T + (ix - (ix / p.T) * p.T), 1);
     uint32_t* q = ps.slot((long)t * ps.cap + slot);
     q[F_CELL * 32] = (uint32_t)cell;
     q[F_X * 32] = __float_as_uint(x); q[F_Y * 32] = __float_as_uint(y);

@@ -114,6 +114,9 @@ struct PushParams {
   // halo receive, window injection) adds to it; -1 = unknown (the tile count bounds it).
   int32_t* occ;
   int32_t* tscale;      // [ntiles] the scale exponent S of each tile's current this step (K1s)
+  int32_t* hist;        // [ntiles][T * T] particles per cell of each tile (all species), exact at the
+                        // start of every K1: K1 moves its crossing particles, insertions add
+  int check_occ;        // 1: K1s verifies hist against a recount (ZPIC_CHECK_OCC; tests)
   float qmax;           // max_s |q_s|
   int tile0;            // K1 launches over tiles [tile0, tile0 + grid) (the slab overlap splits it)
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
@@ -149,7 +152,7 @@ struct LaserParams {
   double a0, omega0, fwhm, W0, start, yc;
 };
 
-enum ErrBits { ERR_OVERFLOW = 1, ERR_MIGRATION = 2, ERR_HALO = 8 };   // 4: k_count's out-of-slab upload
+enum ErrBits { ERR_OVERFLOW = 1, ERR_MIGRATION = 2, ERR_HALO = 8, ERR_HIST = 16 };   // 4: k_count's out-of-slab upload
 
 }  // namespace zpic
 
@@ -187,6 +190,8 @@ struct zpic_ctx {
   int* stats;      // [0] movers of last step, [1] spill count
   int32_t* occ = nullptr;   // [ntiles] occupancy bound of the fixed-point current (PushParams::occ)
   int32_t* tscale = nullptr;   // [ntiles] per-tile scale exponent, from occ before every K1 (K1s)
+  int32_t* hist = nullptr;     // [ntiles][T * T] per-tile cell histogram (PushParams::hist)
+  int check_occ = 0;           // ZPIC_CHECK_OCC=1: verify hist every step (ERR_HIST)
   bool occ_stale = true;    // the particles were (re)loaded: recompute occ before the next step
   int cur;         // index of the current E/B buffer
   int64_t steps;

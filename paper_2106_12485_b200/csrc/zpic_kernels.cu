@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(kBlock) k_insert(PushParams p) {
       }
       const PStore& ps = p.ps[sp[u]];
       if (slot[u] < ps.cap) {
-        atomicAdd(p.occ + t[u], 1);   // occupancy bound of the destination tile
+        atomicAdd(p.occ + t[u], 1);   // occupancy bound and cell histogram of the destination tile
+        atomicAdd(p.hist + (long)t[u] * p.T * p.T + (cell_iy(cell[u]) % p.T) * p.T + cell_ix(cell[u]) % p.T, 1);
         uint32_t* q = ps.slot((long)t[u] * ps.cap + slot[u]);
         q[F_CELL * 32] = (uint32_t)cell[u];
         q[F_X * 32] = __float_as_uint(x[u]); q[F_Y * 32] = __float_as_uint(y[u]);
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(kBlock) k_mail_gather(PushParams p) {
     const uint32_t id = M.nf > F_ID ? src[F_ID] : 0u;
     const int slot = pos + e;
     if (slot < ps.cap) {
+      atomicAdd(p.hist + (long)t * p.T * p.T + (cell_iy((int)cell) % p.T) * p.T + cell_ix((int)cell) % p.T, 1);
       uint32_t* q = ps.slot((long)t * ps.cap + slot);
       q[F_CELL * 32] = cell; q[F_X * 32] = x; q[F_Y * 32] = y;
       q[F_UX * 32] = ux; q[F_UY * 32] = uy; q[F_UZ * 32] = uz;
@@ -1219,7 +1221,10 @@ namespace zpic {
 // =============================================================================================
 // Occupancy bound of the fixed-point tile current after a (re)load (PushParams::occ): one CTA per
 // tile histograms the cells of every species' particles and takes the largest 4 x 4 window sum.
-__global__ void __launch_bounds__(kBlock) k_occupancy(PushParams p) {
+// mode 0 (after a (re)load): store the histogram (p.hist) and the occupancy bound (p.occ).
+// mode 1 (ZPIC_CHECK_OCC, before K1s): verify that p.hist equals the recount and that p.occ bounds
+// the recount's largest window; a violation sets ERR_HIST (the step returns ZPIC_E_STATE).
+__global__ void __launch_bounds__(kBlock) k_occupancy(PushParams p, int mode) {
   __shared__ int h[32 * 32];
   __shared__ int s_max;
   const int t = blockIdx.x, T = p.T;
@@ -1240,9 +1245,23 @@ __global__ void __launch_bounds__(kBlock) k_occupancy(PushParams p) {
   __syncthreads();
   const int m = window_max_4x4(h, T, tw, th);
   atomicMax(&s_max, m);
+  int* H = p.hist + (long)t * T * T;
+  if (mode == 0) {
+    for (int k = threadIdx.x; k < T * T; k += blockDim.x) H[k] = h[k];
+  } else {
+    for (int k = threadIdx.x; k < T * T; k += blockDim.x)
+      if (H[k] != h[k]) atomicOr(p.err, ERR_HIST);
+  }
   __syncthreads();
-  if (threadIdx.x == 0) p.occ[t] = s_max;
+  if (threadIdx.x == 0) {
+    if (mode == 0) p.occ[t] = s_max;
+    else if (p.occ[t] < s_max) atomicOr(p.err, ERR_HIST);
+  }
 }
+void launch_occupancy(const PushParams& p, cudaStream_t st, int mode) {
+  k_occupancy<<<p.ntx * p.nty, kBlock, 0, st>>>(p, mode);
+}
+
 // K1s: every tile's fixed-point scale exponent for the K1 that follows: 2^S from a
 // bound on |J| at any node of the tile's block.  Every particle adds at most |q_s| to any node
 // (|v| < 1, the weights of its pieces sum to 1), and only the particles of a 4 x 4 cell window reach
@@ -1270,8 +1289,5 @@ __global__ void k_tile_scale(PushParams p) {
 }
 void launch_tile_scale(const PushParams& p, cudaStream_t st) {
   k_tile_scale<<<(p.ntx * p.nty + kBlock - 1) / kBlock, kBlock, 0, st>>>(p);
-}
-void launch_occupancy(const PushParams& p, cudaStream_t st) {
-  k_occupancy<<<p.ntx * p.nty, kBlock, 0, st>>>(p);
 }
 }  // namespace zpic

@@ -31,19 +31,29 @@ constexpr int kHole = -1;   // cell value of a vacated slot
 
 // Per-warp ring of crossing paths in shared memory (structure of arrays: conflict-free lanes).
 struct PathRing {
-  int* c;     // packed (lx + 8) | (ly + 8) << 16
+  int* c;     // packed bytes: start cell lx + 8, ly + 8; end cell (this tile, after the window shift)
+              // ex + 8, ey + 8, or ey + 8 = 255 when the particle leaves the tile
   float *x, *y, *dx, *dy, *qvz;
-  __device__ __forceinline__ void put(int k, int lx, int ly, float x0, float y0, float dxp, float dyp, float q) const {
-    c[k] = (lx + 8) | ((ly + 8) << 16);
+  __device__ __forceinline__ void put(int k, int lx, int ly, int ex, int ey, float x0, float y0, float dxp, float dyp,
+                                      float q) const {
+    c[k] = (lx + 8) | ((ly + 8) << 8) | ((ex + 8) << 16) | ((ey + 8) << 24);
     x[k] = x0; y[k] = y0; dx[k] = dxp; dy[k] = dyp; qvz[k] = q;
   }
 };
+constexpr int kRingLeaves = 255 - 8;   // ey of a path whose particle leaves the tile
 
 // Deposit every piece of queued crossing path k (the split of PAPER.md:197).
-template <class A>
-__device__ __forceinline__ void drain_path(const A& acc, const PathRing& Q, int k, float jxs, float jys, int* err) {
+// The tile's cell histogram follows the particle: -1 at its start cell (in the frame after the
+// window shift; a start cell shifted out of the tile was dropped with its column), +1 at its end
+// cell if it stays in the tile (occupancy bound).
+template <int T, class A>
+__device__ __forceinline__ void drain_path(const A& acc, const PathRing& Q, int k, float jxs, float jys, int* err,
+                                           int* hist, int shift) {
   const int v = Q.c[k];
-  const int lx = (v & 0xffff) - 8, ly = (v >> 16) - 8;
+  const int lx = (v & 0xff) - 8, ly = ((v >> 8) & 0xff) - 8;
+  const int ex = ((v >> 16) & 0xff) - 8, ey = ((v >> 24) & 0xff) - 8;
+  if (lx - shift >= 0) atomicAdd(&hist[ly * T + lx - shift], -1);
+  if (ey != kRingLeaves) atomicAdd(&hist[ey * T + ex], 1);
   const float x = Q.x[k], y = Q.y[k], dxp = Q.dx[k], dyp = Q.dy[k], qvz = Q.qvz[k];
   // a path that stays in its cell moved less than a cell: only a queued path can move >= 1
   if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(err, ERR_MIGRATION);
@@ -105,7 +115,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   __shared__ int s_mbc[8];  // mailbox fill per direction (this species)
   __shared__ int s_wsum[2][NW];
   __shared__ double s_ke[kMaxSpecies];
-  __shared__ int s_hist[T * T];   // stayers per end cell (the occupancy bound of the next step)
+  __shared__ int s_hist[T * T];   // the tile's particles per cell (all species)
   __shared__ int s_occ;            // the tile current's scale exponent S
   if (threadIdx.x < kMaxSpecies) s_ke[threadIdx.x] = 0.0;
 
@@ -139,7 +149,15 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
           ::"r"(smem_u32(landB)), "l"(reinterpret_cast<uint64_t>(&p.tmB)), "r"(cx), "r"(cy), "r"(0), "r"(bar)
           : "memory");
     }
-    for (int k = threadIdx.x; k < T * T; k += BLK) s_hist[k] = 0;
+    // the tile's cell histogram (p.hist, exact at every step start); with a window shift at the
+    // end of this step every cell moves one column left and column 0 leaves the tile
+    {
+      const int* h = p.hist + (long)t * T * T;
+      for (int k = threadIdx.x; k < T * T; k += BLK) {
+        const int cx = k % T;
+        s_hist[k] = (cx + p.shift < T) ? __ldcg(h + k + p.shift) : 0;
+      }
+    }
     // the tile current's scale exponent S, computed by K1s from this tile's occupancy bound
     // before this kernel (a plain load: nothing of it stays live in the particle loop)
     if (threadIdx.x == 32) s_occ = p.tscale[t];
@@ -257,18 +275,19 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
       // crossing paths -> this warp's ring; drain full batches of 32 with every lane active
       const unsigned bal = __ballot_sync(0xffffffffu, cross);
       if (bal) {   // warp-uniform
-        if (cross) Q.put((qh + qn + __popc(bal & ltmask)) & (kQRing - 1), lx, ly, x0, y0, dxp, dyp, qvz);
+        if (cross)
+          Q.put((qh + qn + __popc(bal & ltmask)) & (kQRing - 1), lx, ly, stay ? ix - i0 : 0, stay ? iy - j0 : kRingLeaves,
+                x0, y0, dxp, dyp, qvz);
         qn += __popc(bal);
         __syncwarp();
         if (qn >= 32) {
-          drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys, p.err);
+          drain_path<T>(A, Q, (qh + lane) & (kQRing - 1), jxs, jys, p.err, s_hist, p.shift);
           qh = (qh + 32) & (kQRing - 1);
           qn -= 32;
           __syncwarp();   // the drained entries are read before the next put overwrites them
         }
       }
       if (valid && stay) {
-        atomicAdd(&s_hist[(iy - j0) * T + (ix - i0)], 1);
         const int ncell_ = pack_cell(ix, iy);
         if (!p.skip_cell_store || ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);
         __stcs(pp + F_X * 32, __float_as_uint(x)); __stcs(pp + F_Y * 32, __float_as_uint(y));
@@ -308,7 +327,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         }
       }
     }
-    if (lane < qn) drain_path(A, Q, (qh + lane) & (kQRing - 1), jxs, jys, p.err);
+    if (lane < qn) drain_path<T>(A, Q, (qh + lane) & (kQRing - 1), jxs, jys, p.err, s_hist, p.shift);
     // kinetic energy: warp reduction, one shared fp64 add per warp, one global add per CTA
     for (int o = 16; o > 0; o >>= 1) ke += __shfl_xor_sync(0xffffffffu, ke, o);
     if (lane == 0) atomicAdd(&s_ke[s], (double)ke);
@@ -408,9 +427,14 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   if ((int)threadIdx.x < nspec && s_ke[threadIdx.x] != 0.0)
     atomicAdd(p.ke_slots + threadIdx.x * kEnergySlots + (t & (kEnergySlots - 1)), s_ke[threadIdx.x]);
   // the next step's occupancy bound: the largest 4 x 4 window of this tile's stayers (the histogram
-  // is complete: every species' loop ended at a barrier); arrivals add to it after this kernel
+  // is complete: every species' loop ended at a barrier); arrivals add to it after this kernel, to
+  // the bound and to their cell of the stored histogram
   const int m = __reduce_max_sync(0xffffffffu, window_max_4x4(s_hist, T, tw, th));
   if (lane == 0 && m > 0) atomicMax(p.occ + t, m);
+  {
+    int* h = p.hist + (long)t * T * T;
+    for (int k = threadIdx.x; k < T * T; k += BLK) __stcg(h + k, s_hist[k]);
+  }
 }
 
 template <int T, int BLK, int MINB, int NSPEC>

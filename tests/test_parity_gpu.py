@@ -633,3 +633,48 @@ def test_set_particles_replaces_the_species_loose_particles_included():
         g.set_particles(0, bad)
     assert g.counters()["particles"] == 0
     g.close()
+
+
+@pytest.mark.parametrize("case", ["ragged8", "ragged32", "open_x", "window", "loose", "repack", "two_species"])
+def test_occupancy_histogram_stays_exact(case, monkeypatch):
+    """The per-tile cell histogram behind the fixed-point current's occupancy bound
+    is maintained incrementally: K1 moves only its crossing particles, every insertion adds.  With
+    ZPIC_CHECK_OCC=1 a recount before every step verifies it cell by cell, and that the bound covers
+    the recount's largest 4 x 4 window (a violation stops the run with ZPIC_E_STATE), across partial
+    tiles, open-edge removal, the moving window (shift + injection), the loose list, a re-pack and
+    two species."""
+    monkeypatch.setenv("ZPIC_CHECK_OCC", "1")
+    slack, steps, tile = 1.25, 20, 16
+    if case.startswith("ragged"):
+        cfg = synth.config("C1", nx=50, ny=37)
+        cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
+        tile = int(case[6:])
+    elif case == "open_x":
+        cfg = synth.config("C3", nx=128, ny=32)
+        cfg["species"][0].update(x0=0.0, x1=6.4)
+        cfg["species"][1].update(x0=6.4, x1=12.8)
+        steps = 40
+    elif case == "window":
+        cfg = c4_reduced(nx=200, ny=32)
+        steps = 30
+    elif case == "loose":
+        cfg = synth.config("C1", nx=48, ny=48)
+        cfg["species"][0]["uth"] = (0.4, 0.4, 0.4)
+        slack = 1.0
+    elif case == "repack":
+        cfg = synth.config("C1", nx=128, ny=128)
+        cfg["species"][0]["uth"] = (0.4, 0.4, 0.4)
+        slack, steps = 0.97, 18
+    else:
+        cfg = synth.config("C2", nx=64, ny=64)
+        for sp in cfg["species"]:
+            sp["uth"] = (0.3, 0.3, 0.3)
+    g = _z().Simulation(cfg, inject=True, tile=tile, capacity_slack=slack)
+    for _ in range(steps):
+        g.step(1)
+        g.counters()   # syncs and raises ZPIC_E_STATE on ERR_HIST
+    if case == "repack":
+        assert g.counters()["repacks"] >= 1
+    if case == "loose":
+        assert g.counters()["loose"] > 0 or g.counters()["repacks"] > 0
+    g.close()
