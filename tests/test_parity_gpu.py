@@ -669,7 +669,10 @@ def test_occupancy_histogram_stays_exact(case, monkeypatch):
         cfg = synth.config("C2", nx=64, ny=64)
         for sp in cfg["species"]:
             sp["uth"] = (0.3, 0.3, 0.3)
-    g = _z().Simulation(cfg, inject=True, tile=tile, capacity_slack=slack)
+    if case == "repack":   # an upload into tiles 3 % short of the lattice: loose list, re-pack at step 16
+        g = gpu_from_particles(cfg, [synth.species_particles(cfg, 0)], tile=tile, slack=slack)
+    else:
+        g = _z().Simulation(cfg, inject=True, tile=tile, capacity_slack=slack)
     for _ in range(steps):
         g.step(1)
         g.counters()   # syncs and raises ZPIC_E_STATE on ERR_HIST
