@@ -136,4 +136,22 @@ __device__ __forceinline__ int window_max_4x4(const int* h, int T, int tw, int t
   }
   return m;
 }
+// The same for a full T x T tile with T known at compile time: lane a < T - 3 of the calling warp
+// slides a 4-row window down column strip [a, a + 4) (4 loads per row, running sums in registers);
+// returns the warp maximum (every lane), so one warp does the whole tile.
+template <int T>
+__device__ __forceinline__ int window_max_4x4_full_warp(const int* h) {
+  const int a = threadIdx.x & 31;
+  int m = 0;
+  if (a < T - 3) {
+    int r0 = 0, r1 = 0, r2 = 0;
+#pragma unroll
+    for (int y = 0; y < T; ++y) {
+      const int r = h[y * T + a] + h[y * T + a + 1] + h[y * T + a + 2] + h[y * T + a + 3];
+      if (y >= 3) m = max(m, r0 + r1 + r2 + r);
+      r0 = r1; r1 = r2; r2 = r;
+    }
+  }
+  return __reduce_max_sync(0xffffffffu, m);
+}
 }  // namespace zpic

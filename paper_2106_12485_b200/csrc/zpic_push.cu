@@ -429,8 +429,15 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   // the next step's occupancy bound: the largest 4 x 4 window of this tile's stayers (the histogram
   // is complete: every species' loop ended at a barrier); arrivals add to it after this kernel, to
   // the bound and to their cell of the stored histogram
-  const int m = __reduce_max_sync(0xffffffffu, window_max_4x4(s_hist, T, tw, th));
-  if (lane == 0 && m > 0) atomicMax(p.occ + t, m);
+  if (tw == T && th == T) {   // full tile: one warp slides the windows (T known at compile time)
+    if (warp == NW - 1) {
+      const int m = window_max_4x4_full_warp<T>(s_hist);
+      if (lane == 0 && m > 0) atomicMax(p.occ + t, m);
+    }
+  } else {
+    const int m = __reduce_max_sync(0xffffffffu, window_max_4x4(s_hist, T, tw, th));
+    if (lane == 0 && m > 0) atomicMax(p.occ + t, m);
+  }
   {
     int* h = p.hist + (long)t * T * T;
     for (int k = threadIdx.x; k < T * T; k += BLK) __stcg(h + k, s_hist[k]);
