@@ -29,15 +29,18 @@ constexpr int kQRing = 64;  // per-warp ring of queued crossing paths (<= 31 lef
 constexpr int kHCap = 256;  // holes recorded per tile and species (else the sentinel fallback)
 constexpr int kHole = -1;   // cell value of a vacated slot
 
-// Per-warp ring of crossing paths in shared memory (structure of arrays: conflict-free lanes).
+// Per-warp ring of crossing paths in shared memory: one 16-byte (x0, y0, dx, dy) and one 8-byte
+// (cells, q vz) record per entry (two vector stores per put, two vector loads per drain; the
+// entries of a put / drain are consecutive: conflict-free quarter-warps).  The cells word packs
+// bytes: start cell lx + 8, ly + 8; end cell (this tile, after the window shift) ex + 8, ey + 8,
+// or ey + 8 = 255 when the particle leaves the tile.
 struct PathRing {
-  int* c;     // packed bytes: start cell lx + 8, ly + 8; end cell (this tile, after the window shift)
-              // ex + 8, ey + 8, or ey + 8 = 255 when the particle leaves the tile
-  float *x, *y, *dx, *dy, *qvz;
+  float4* p4;
+  float2* p2;
   __device__ __forceinline__ void put(int k, int lx, int ly, int ex, int ey, float x0, float y0, float dxp, float dyp,
                                       float q) const {
-    c[k] = (lx + 8) | ((ly + 8) << 8) | ((ex + 8) << 16) | ((ey + 8) << 24);
-    x[k] = x0; y[k] = y0; dx[k] = dxp; dy[k] = dyp; qvz[k] = q;
+    p4[k] = make_float4(x0, y0, dxp, dyp);
+    p2[k] = make_float2(__int_as_float((lx + 8) | ((ly + 8) << 8) | ((ex + 8) << 16) | ((ey + 8) << 24)), q);
   }
 };
 constexpr int kRingLeaves = 255 - 8;   // ey of a path whose particle leaves the tile
@@ -49,12 +52,14 @@ constexpr int kRingLeaves = 255 - 8;   // ey of a path whose particle leaves the
 template <int T, class A>
 __device__ __forceinline__ void drain_path(const A& acc, const PathRing& Q, int k, float jxs, float jys, int* err,
                                            int* hist, int shift) {
-  const int v = Q.c[k];
+  const float4 a = Q.p4[k];
+  const float2 b = Q.p2[k];
+  const int v = __float_as_int(b.x);
   const int lx = (v & 0xff) - 8, ly = ((v >> 8) & 0xff) - 8;
   const int ex = ((v >> 16) & 0xff) - 8, ey = ((v >> 24) & 0xff) - 8;
   if (lx - shift >= 0) atomicAdd(&hist[ly * T + lx - shift], -1);
   if (ey != kRingLeaves) atomicAdd(&hist[ey * T + ex], 1);
-  const float x = Q.x[k], y = Q.y[k], dxp = Q.dx[k], dyp = Q.dy[k], qvz = Q.qvz[k];
+  const float x = a.x, y = a.y, dxp = a.z, dyp = a.w, qvz = b.y;
   // a path that stays in its cell moved less than a cell: only a queued path can move >= 1
   if (fabsf(dxp) >= 1.0f || fabsf(dyp) >= 1.0f) atomicOr(err, ERR_MIGRATION);
   const float x1 = __fadd_rn(x, dxp), y1 = __fadd_rn(y, dyp);
@@ -99,7 +104,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   extern __shared__ __align__(128) unsigned char smem_raw[];
   int* s_j = reinterpret_cast<int*>(smem_raw);         // int32 current, or the high words (exact form)
   int* s_jlo = s_j + JWORDS;                           // low words (exact form only)
-  int* s_q = reinterpret_cast<int*>(smem_raw + L::JBYTES);   // 6 arrays of NW * kQRing words
+  int* s_q = reinterpret_cast<int*>(smem_raw + L::JBYTES);   // path rings: NW x kQRing float4, then float2
   float2* s_eb1 = reinterpret_cast<float2*>(smem_raw + L::JBYTES + L::QBYTES(BLK));
   float2* s_eb2 = s_eb1 + W * W;
   float* s_ez = reinterpret_cast<float*>(s_eb2 + W * W);
@@ -185,9 +190,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
 
   const SmemFields<W> F{s_eb1, s_eb2, s_ez, s_bz};
   const int qo = warp * kQRing;
-  const PathRing Q{s_q + qo, reinterpret_cast<float*>(s_q + NW * kQRing + qo),
-                   reinterpret_cast<float*>(s_q + 2 * NW * kQRing + qo), reinterpret_cast<float*>(s_q + 3 * NW * kQRing + qo),
-                   reinterpret_cast<float*>(s_q + 4 * NW * kQRing + qo), reinterpret_cast<float*>(s_q + 5 * NW * kQRing + qo)};
+  const PathRing Q{reinterpret_cast<float4*>(s_q) + qo, reinterpret_cast<float2*>(s_q + 4 * NW * kQRing) + qo};
 
   auto push_all = [&](const auto& A, const float fscale) {
   for (int s = 0; s < nspec; ++s) {
