@@ -154,7 +154,6 @@ void alloc_store(zpic_ctx* c, int s, int cap) {
   ps.cap = cap;
   ps.nf = c->opt.track_ids ? 7 : 6;
   ps.data = (uint32_t*)dev_alloc(c, n * ps.nf * sizeof(uint32_t));   // contents defined by cnt, no memset
-  ps.out = (uint32_t*)dev_alloc(c, n * ps.nf * sizeof(uint32_t));
   ps.cnt = alloc_n<int32_t>(c, c->ntiles);
   // mailboxes: an edge box holds half a tile column of the species' lattice, a corner box 32
   MailBox& M = c->mail[s];
@@ -181,7 +180,7 @@ void check_tile_capacity(zpic_ctx* c) {
 
 void free_store(zpic_ctx* c, int s) {
   PStore& ps = c->ps[s];
-  dev_free(c, ps.data); dev_free(c, ps.out); dev_free(c, ps.cnt);
+  dev_free(c, ps.data); dev_free(c, ps.cnt);
   ps = PStore{};
   dev_free(c, c->mail[s].data); dev_free(c, c->mail[s].cnt);
   c->mail[s] = MailBox{};
@@ -1129,12 +1128,6 @@ bool overlap_round1(const zpic_ctx* c) {
   return c->slab && c->transport == ZPIC_TRANSPORT_NCCL && c->comm_stream && c->opt.filter_passes == 0;
 }
 
-// K1 reads every species' particles from `data` and writes them to `out`; afterwards the two
-// buffers trade places (host pointers only; a captured step records the pointers it used).
-void swap_stores(zpic_ctx* c) {
-  for (int q = 0; q < c->nspecies; ++q) std::swap(c->ps[q].data, c->ps[q].out);
-}
-
 StepState step_phase_a(zpic_ctx* c) {
   StepState s{};
   s.p = push_params(c);
@@ -1169,8 +1162,6 @@ StepState step_phase_a(zpic_ctx* c) {
       ++s.launches;
     }
   }
-  swap_stores(c);                    // K1 wrote the particles into the other buffer: it is current now
-  for (int q = 0; q < c->nspecies; ++q) s.p.ps[q] = c->ps[q];
   if (p.use_mail) { ProfScope ps(c, K_MAIL); launch_mail_gather(p, c->stream); ++s.launches; }
   { ProfScope ps(c, K_INSERT); launch_insert(p, grid_small, c->stream); ++s.launches; }
   if (!p.commutative) {
@@ -1322,8 +1313,6 @@ static cudaGraphExec_t one_step_graph(zpic_ctx* c, int shift) {
   if (ge) return ge;
   const int cur = c->cur, since = c->since_check;
   const int64_t steps = c->steps, launches = c->launches, n_move = c->n_move;
-  PStore ps0[kMaxSpecies];
-  for (int q = 0; q < c->nspecies; ++q) ps0[q] = c->ps[q];
   cudaGraph_t g = nullptr;
   CUDA_OR_THROW(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
   try {
@@ -1336,7 +1325,6 @@ static cudaGraphExec_t one_step_graph(zpic_ctx* c, int shift) {
   CUDA_OR_THROW(cudaStreamEndCapture(c->stream, &g));
   c->graph1_launches[par][shift] = (int)(c->launches - launches);
   c->cur = cur; c->steps = steps; c->launches = launches; c->n_move = n_move; c->since_check = since;
-  for (int q = 0; q < c->nspecies; ++q) c->ps[q] = ps0[q];   // the replay swaps them (zpic_step)
   const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) { ge = nullptr; throw Fail{ZPIC_E_CUDA, std::string("graph: ") + cudaGetErrorString(e)}; }
@@ -1454,7 +1442,6 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
         const int shift = window_shifts(c) ? 1 : 0;
         const int par = c->steps & 1;
         CUDA_OR_THROW(cudaGraphLaunch(one_step_graph(c, shift), c->stream));
-        swap_stores(c);
         c->cur ^= 1;
         c->steps += 1;
         c->since_check += 1;

@@ -40,8 +40,6 @@ struct GridDesc {
 enum PField { F_CELL = 0, F_X, F_Y, F_UX, F_UY, F_UZ, F_ID };
 struct PStore {
   uint32_t* data;  // ntiles * cap / 32 blocks of 32 * nf words
-  uint32_t* out;   // the other buffer of the same shape: K1 reads `data` and writes the pushed
-                   // particles to `out` (in cell order); the host swaps the two after K1
   int nf;          // 6, or 7 with ids
   int32_t* cnt;    // [ntiles]
   int cap;         // slots per tile (multiple of 32)

@@ -195,8 +195,6 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   auto push_all = [&](const auto& A, const float fscale) {
   for (int s = 0; s < nspec; ++s) {
     const PStore ps = p.ps[s];
-    PStore po = ps;   // the output buffer of this step (same layout)
-    po.data = ps.out;
     const SpeciesConst sc = p.sc[s];
     const float jxs = sc.jx * fscale, jys = sc.jy * fscale, qs = sc.q * fscale;
     const int n = ps.cnt[t];
@@ -210,7 +208,6 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
     int qn = 0, qh = 0;  // warp-uniform ring fill and head
     // this thread's slot of the current chunk (segments and chunks start on 32-slot blocks)
     uint32_t* pp = ps.slot(base + threadIdx.x);
-    uint32_t* po_ = po.slot(base + threadIdx.x);   // this thread's output slot (same index)
     // software pipeline: the next chunk's particle is loaded while this one is pushed
     int ncell = 0;
     float nxo = 0.f, nyo = 0.f, nux = 0.f, nuy = 0.f, nuz = 0.f;
@@ -222,7 +219,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
       nuz = __uint_as_float(__ldcs(pp + F_UZ * 32));
       if (has_id) nid = __ldcs(pp + F_ID * 32);
     }
-    for (int c0 = 0; c0 < n; c0 += BLK, pp += chunk_words, po_ += chunk_words) {
+    for (int c0 = 0; c0 < n; c0 += BLK, pp += chunk_words) {
       const int i = c0 + threadIdx.x;
       const bool valid = i < n;
       const int cell = ncell;
@@ -295,18 +292,17 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
       }
       if (valid && stay) {
         const int ncell_ = pack_cell(ix, iy);
-        __stcs(po_ + F_CELL * 32, (uint32_t)ncell_);
-        __stcs(po_ + F_X * 32, __float_as_uint(x)); __stcs(po_ + F_Y * 32, __float_as_uint(y));
-        __stcs(po_ + F_UX * 32, __float_as_uint(ux)); __stcs(po_ + F_UY * 32, __float_as_uint(uy));
-        __stcs(po_ + F_UZ * 32, __float_as_uint(uz));
-        if (has_id) __stcs(po_ + F_ID * 32, id);
+        if (!p.skip_cell_store || ncell_ != cell) __stcs(pp + F_CELL * 32, (uint32_t)ncell_);
+        __stcs(pp + F_X * 32, __float_as_uint(x)); __stcs(pp + F_Y * 32, __float_as_uint(y));
+        __stcs(pp + F_UX * 32, __float_as_uint(ux)); __stcs(pp + F_UY * 32, __float_as_uint(uy));
+        __stcs(pp + F_UZ * 32, __float_as_uint(uz));
       }
       // leavers (~20 % of the warp-chunks at C5): one warp-uniform branch for the hole record, the
       // mailbox and the mover list
       const bool leave = valid && !stay;
       if (__any_sync(0xffffffffu, leave)) {
         if (leave) {
-          po_[F_CELL * 32] = (uint32_t)kHole;
+          pp[F_CELL * 32] = (uint32_t)kHole;
           const int h = atomicAdd(&s_cnt[0], 1);
           if (h < kHCap) s_holes[h] = i;
           else s_cnt[3] = 1;
@@ -367,8 +363,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         }
         __syncwarp();
         for (int k = lane; k < nhb; k += 32) {
-          uint32_t* d = po.slot(base + s_hb[k]);
-          const uint32_t* src = po.slot(base + s_sa[k]);
+          uint32_t* d = ps.slot(base + s_hb[k]);
+          const uint32_t* src = ps.slot(base + s_sa[k]);
           for (int f = 0; f < ps.nf; ++f) d[f * 32] = src[f * 32];
         }
       }
@@ -380,7 +376,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         const int i = c0 + threadIdx.x;
         uint32_t v[7] = {(uint32_t)kHole, 0u, 0u, 0u, 0u, 0u, 0u};
         if (i < n) {
-          const uint32_t* src = po.slot(base + i);
+          const uint32_t* src = ps.slot(base + i);
 #pragma unroll
           for (int f = 0; f < 7; ++f)
             if (f < ps.nf) v[f] = src[f * 32];
@@ -398,7 +394,7 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
         buf ^= 1;
         __syncthreads();   // every thread has read its slot before any slot of this chunk is rewritten
         if (keep) {
-          uint32_t* d = po.slot(base + out + before + __popc(bal & ltmask));
+          uint32_t* d = ps.slot(base + out + before + __popc(bal & ltmask));
 #pragma unroll
           for (int f = 0; f < 7; ++f)
             if (f < ps.nf) d[f * 32] = v[f];
