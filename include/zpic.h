@@ -150,9 +150,19 @@ typedef struct {
  *     ProcessGroupNCCL._comm_ptr()), or NULL with nccl_id = the 128-byte ncclUniqueId from
  *     zpic_nccl_unique_id() on rank 0, broadcast by the caller (the library then owns a comm);
  *   ZPIC_TRANSPORT_LOOPBACK: `world` contexts in one process on one device and one stream,
- *     stepped together with zpic_step_group (validation of the slab logic on one GPU).
+ *     stepped together with zpic_step_group (validation of the slab logic on one GPU);
+ *   ZPIC_TRANSPORT_PEER: one process per GPU of one node; no NCCL send / recv in the step: the
+ *     library's own kernels copy the halo rows and the migrating particles straight into the
+ *     neighbours' receive areas over NVLink (CUDA IPC pointers, exchanged once at zpic_init with
+ *     an all-gather on the NCCL communicator given as for ZPIC_TRANSPORT_NCCL) and signal them with
+ *     system-scope epoch flags the receiver's wait kernel acquires (a wait that never completes
+ *     stops the run with ZPIC_E_OVERFLOW after ~20 s instead of hanging); world = 1 is a ring on
+ *     the context's own buffers;
+ *   ZPIC_TRANSPORT_LOOPBACK_PEER: the PEER kernels in a loopback group (zpic_step_group; every
+ *     signal is enqueued before the wait that reads it, so no kernel ever waits on another).
  * Pass NULL for the unsplit single-GPU domain. */
-typedef enum { ZPIC_TRANSPORT_NCCL = 0, ZPIC_TRANSPORT_LOOPBACK = 1 } zpic_transport;
+typedef enum { ZPIC_TRANSPORT_NCCL = 0, ZPIC_TRANSPORT_LOOPBACK = 1, ZPIC_TRANSPORT_PEER = 2,
+               ZPIC_TRANSPORT_LOOPBACK_PEER = 3 } zpic_transport;
 typedef struct {
   int32_t rank, world;
   void* nccl_comm;

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libzpic_b200.so")
-SOURCES = ["zpic_api.cu", "zpic_kernels.cu", "zpic_push.cu"]
+SOURCES = ["zpic_api.cu", "zpic_kernels.cu", "zpic_push.cu", "zpic_peer.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 # -ftz=true: fp32 denormals flush to zero (no guard code around rsqrt / rcp); -prec-div=false:
 # approximate fp32 division (2 ulp) for the cell-crossing fractions.  The fp64 paths (injector RNG,

@@ -50,6 +50,16 @@ void launch_filter_x(const float* Jin, float* Jout, const GridDesc& g, int npass
 void launch_apply_j_halo(float* J, const GridDesc& g, const float* rup, const float* rdn, int has_lo, int has_hi,
                          cudaStream_t st);
 size_t particle_msg_bytes(int cap);
+PeerView peer_view(void* block, int pitch, int pcap);
+size_t peer_block_bytes(int pitch, int pcap);
+void launch_peer_put1(const float* J, const GridDesc& g, const void* send_dn, const void* send_up, int pcap,
+                      const PeerView& lo, const PeerView& up, int has_lo, int has_hi, cudaStream_t st);
+void launch_peer_put2(const float* E, const float* B, const GridDesc& g, const PeerView& lo, const PeerView& up,
+                      int has_lo, int has_hi, cudaStream_t st);
+void launch_peer_apply2(float* E, float* B, const GridDesc& g, const PeerView& self, int has_lo, int has_hi,
+                        cudaStream_t st);
+void launch_peer_signal(unsigned long long* fa, unsigned long long* fb, unsigned long long e, cudaStream_t st);
+void launch_peer_wait(const unsigned long long* flags, int ia, int ib, unsigned long long e, int* err, cudaStream_t st);
 PList particle_msg_list(void* buf, int cap);
 void launch_recv_insert(const PushParams& p, const PList& lo, const PList& hi, cudaStream_t st);
 void launch_sort_tiles(const PStore& ps, int T, int ntx, int ntiles, int* stats, cudaStream_t st);
@@ -461,6 +471,31 @@ const char* zpic_last_error(const zpic_ctx* ctx) { return ctx ? ctx->last_error.
 static void load_species(zpic_ctx* c, int s, int64_t n, char* tmp, bool has_id);
 static void size_lists(zpic_ctx* c, int64_t extra = 0);
 
+// PEER across processes: the CUDA IPC handles of every rank's receive block, all-gathered once on
+// the NCCL communicator; the y neighbours' blocks opened (peer access over NVLink).
+static void open_peer_blocks(zpic_ctx* c) {
+  cudaIpcMemHandle_t mine;
+  CUDA_OR_THROW(cudaIpcGetMemHandle(&mine, c->peer_block));
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  char* dbuf = alloc_n<char>(c, hb * (c->world + 1));
+  CUDA_OR_THROW(cudaMemcpyAsync(dbuf + hb * c->world, &mine, hb, cudaMemcpyHostToDevice, c->stream));
+  ncclResult_t r = ncclAllGather(dbuf + hb * c->world, dbuf, hb, ncclChar, (ncclComm_t)c->comm, c->stream);
+  if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("PEER handle all-gather: ") + ncclGetErrorString(r)};
+  std::vector<cudaIpcMemHandle_t> all(c->world);
+  CUDA_OR_THROW(cudaMemcpyAsync(all.data(), dbuf, hb * c->world, cudaMemcpyDeviceToHost, c->stream));
+  CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
+  dev_free(c, dbuf);
+  auto open = [&](int rank) -> PeerView {
+    if (rank == c->rank) return c->peer_self;
+    void* p = nullptr;
+    CUDA_OR_THROW(cudaIpcOpenMemHandle(&p, all[rank], cudaIpcMemLazyEnablePeerAccess));
+    c->ipc_open.push_back(p);
+    return peer_view(p, c->g.pitch, c->pcap);
+  };
+  if (c->has_lo) c->peer_lo = open(c->lower);
+  if (c->has_hi) c->peer_hi = c->upper == c->lower && c->has_lo ? c->peer_lo : open(c->upper);
+}
+
 // The one x sub-row of a ramp species (R16), in the oracle-independent arithmetic of the library:
 // ramp positions by cumulative inversion, then the regular sub-lattice from x1 on; cell index and
 // fp32 offset with the R6 rule.
@@ -518,8 +553,12 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
     if (grid->ny % dist->world != 0 || grid->ny / dist->world < 2) {
       g_init_error = "ny must be a multiple of world with >= 2 rows per slab"; return ZPIC_E_DECOMP;
     }
-    if (dist->transport == ZPIC_TRANSPORT_NCCL && !dist->nccl_comm && !dist->nccl_id) {
-      g_init_error = "NCCL transport needs nccl_comm or nccl_id"; return ZPIC_E_DECOMP;
+    if ((dist->transport == ZPIC_TRANSPORT_NCCL || (dist->transport == ZPIC_TRANSPORT_PEER && dist->world > 1)) &&
+        !dist->nccl_comm && !dist->nccl_id) {
+      g_init_error = "NCCL / PEER transport needs nccl_comm or nccl_id"; return ZPIC_E_DECOMP;
+    }
+    if (dist->transport < ZPIC_TRANSPORT_NCCL || dist->transport > ZPIC_TRANSPORT_LOOPBACK_PEER) {
+      g_init_error = "unknown transport"; return ZPIC_E_DECOMP;
     }
   }
 
@@ -720,17 +759,28 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       // the thermal crossing rate of C5 (u_th = 0.1: 2.8 % per step and direction) — 1 MB per
       // direction at C5 instead of a whole-row bound; more crossers than that stop the run with
       // ZPIC_E_OVERFLOW (ERR_HALO; zpic_options.halo_particles raises the capacity)
-      c->jrup = alloc_n<float>(c, (size_t)3 * 2 * g.pitch);
-      c->jrdn = alloc_n<float>(c, (size_t)3 * 2 * g.pitch);
       int ppc_sum = 0;
       for (int s = 0; s < n_species; ++s) ppc_sum += species[s].ppc[0] * species[s].ppc[1];
       c->pcap = c->opt.halo_particles > 0 ? round_up(c->opt.halo_particles, 32)
                                           : std::max(4096, round_up(g.nx * std::max(ppc_sum, 1) / 4, 32));
-      for (int d = 0; d < 2; ++d) {
-        c->pmsg_send[d] = alloc_n<char>(c, particle_msg_bytes(c->pcap));
-        c->pmsg_recv[d] = alloc_n<char>(c, particle_msg_bytes(c->pcap));
+      for (int d = 0; d < 2; ++d) c->pmsg_send[d] = alloc_n<char>(c, particle_msg_bytes(c->pcap));
+      c->peer = c->transport == ZPIC_TRANSPORT_PEER || c->transport == ZPIC_TRANSPORT_LOOPBACK_PEER;
+      if (c->peer) {   // the receive areas in one cudaMalloc'd block (exportable with CUDA IPC)
+        const size_t pb = peer_block_bytes(g.pitch, c->pcap);
+        CUDA_OR_THROW(cudaMalloc(&c->peer_block, pb));
+        CUDA_OR_THROW(cudaMemsetAsync(c->peer_block, 0, pb, c->stream));
+        c->peer_self = peer_view(c->peer_block, g.pitch, c->pcap);
+        c->peer_lo = c->peer_hi = c->peer_self;   // a one-rank ring; loopback groups bind at zpic_step_group
+        c->jrup = c->peer_self.jrup;
+        c->jrdn = c->peer_self.jrdn;
+        c->pmsg_recv[0] = c->peer_self.pmsg[0];
+        c->pmsg_recv[1] = c->peer_self.pmsg[1];
+      } else {
+        c->jrup = alloc_n<float>(c, (size_t)3 * 2 * g.pitch);
+        c->jrdn = alloc_n<float>(c, (size_t)3 * 2 * g.pitch);
+        for (int d = 0; d < 2; ++d) c->pmsg_recv[d] = alloc_n<char>(c, particle_msg_bytes(c->pcap));
       }
-      if (c->transport == ZPIC_TRANSPORT_NCCL) {
+      if (c->transport == ZPIC_TRANSPORT_NCCL || (c->transport == ZPIC_TRANSPORT_PEER && c->world > 1)) {
         if (c->dist.nccl_comm) {
           c->comm = c->dist.nccl_comm;
           c->own_comm = false;
@@ -743,8 +793,12 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
           c->comm = comm;
           c->own_comm = true;
         }
-        CUDA_OR_THROW(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
-        for (auto& e : c->ev) CUDA_OR_THROW(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        if (c->transport == ZPIC_TRANSPORT_NCCL) {
+          CUDA_OR_THROW(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+          for (auto& e : c->ev) CUDA_OR_THROW(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        } else {
+          open_peer_blocks(c);   // PEER across processes: every rank's block by CUDA IPC
+        }
       }
     }
     CUDA_OR_THROW(cudaGetLastError());
@@ -1128,6 +1182,30 @@ bool overlap_round1(const zpic_ctx* c) {
   return c->slab && c->transport == ZPIC_TRANSPORT_NCCL && c->comm_stream && c->opt.filter_passes == 0;
 }
 
+// PEER transports (zpic_peer.cu): round 1 = raw J rows + particle messages into the neighbours'
+// receive areas, round 2 = E/B rows of buffer b into their guard-row areas; epochs count the rounds
+// (every rank of a chain steps in lockstep, so the epochs agree).
+void peer_round1_send(zpic_ctx* c) {
+  c->peer_e1 += 1;
+  launch_peer_put1(c->J, c->g, c->pmsg_send[0], c->pmsg_send[1], c->pcap, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi,
+                   c->stream);
+  launch_peer_signal(c->has_hi ? c->peer_hi.flags + 0 : nullptr, c->has_lo ? c->peer_lo.flags + 1 : nullptr, c->peer_e1,
+                     c->stream);
+}
+void peer_round1_wait(zpic_ctx* c) {
+  launch_peer_wait(c->peer_self.flags, c->has_lo ? 0 : -1, c->has_hi ? 1 : -1, c->peer_e1, c->err, c->stream);
+}
+void peer_round2_send(zpic_ctx* c, int b) {
+  c->peer_e2 += 1;
+  launch_peer_put2(c->E[b], c->B[b], c->g, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi, c->stream);
+  launch_peer_signal(c->has_hi ? c->peer_hi.flags + 2 : nullptr, c->has_lo ? c->peer_lo.flags + 3 : nullptr, c->peer_e2,
+                     c->stream);
+}
+void peer_round2_recv(zpic_ctx* c, int b) {
+  launch_peer_wait(c->peer_self.flags, c->has_lo ? 2 : -1, c->has_hi ? 3 : -1, c->peer_e2, c->err, c->stream);
+  launch_peer_apply2(c->E[b], c->B[b], c->g, c->peer_self, c->has_lo, c->has_hi, c->stream);
+}
+
 StepState step_phase_a(zpic_ctx* c) {
   StepState s{};
   s.p = push_params(c);
@@ -1152,7 +1230,8 @@ StepState step_phase_a(zpic_ctx* c) {
     if (c->r2_pending) {   // the E/B ghost rows of this step are still in flight
       const int tb = c->ntx, te = std::max(c->ntx, (c->nty - 1) * c->ntx);
       launch_push_tiles(p, tb, te, c->stream);
-      CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
+      if (c->peer) peer_round2_recv(c, c->cur);   // the neighbours' E/B rows into this buffer's guards
+      else CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
       c->r2_pending = false;
       launch_push_tiles(p, 0, std::min(tb, c->ntiles), c->stream);
       launch_push_tiles(p, std::max(te, tb), c->ntiles, c->stream);
@@ -1211,10 +1290,11 @@ void step_phase_b(zpic_ctx* c, StepState& s) {
       ++s.launches;
       yee_done_to = hi;
     }
-    CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[1], 0));
+    if (!c->peer) CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[1], 0));
   }
   if (c->slab) {
     ProfScope ps(c, K_HALO);
+    if (c->peer) peer_round1_wait(c);
     launch_apply_j_halo(c->J, c->g, c->jrup, c->jrdn, c->has_lo, c->has_hi, c->stream);
     launch_recv_insert(s.p, particle_msg_list(c->pmsg_recv[0], c->pcap), particle_msg_list(c->pmsg_recv[1], c->pcap),
                        c->stream);
@@ -1360,7 +1440,10 @@ static cudaGraphExec_t two_step_graph(zpic_ctx* c) {
 // next step's K1 (r2_pending) until slab_join.
 static void run_step_nccl(zpic_ctx* c) {
   StepState s = step_phase_a(c);
-  if (c->slab) {
+  if (c->slab && c->peer) {   // round 1 by the peer-put kernels; interior Yee rows before the wait
+    peer_round1_send(c);
+    s.r1_async = c->opt.filter_passes == 0;
+  } else if (c->slab) {
     ncclResult_t r;
     if (overlap_round1(c)) {   // round 1 on the comm stream, interior Yee rows meanwhile
       CUDA_OR_THROW(cudaEventRecord(c->ev[0], c->stream));
@@ -1375,7 +1458,10 @@ static void run_step_nccl(zpic_ctx* c) {
     if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 1: ") + ncclGetErrorString(r)};
   }
   step_phase_b(c, s);
-  if (c->slab) {
+  if (c->slab && c->peer) {   // round 2 by the peer-put kernels; received before the next boundary K1
+    peer_round2_send(c, c->cur ^ 1);
+    c->r2_pending = true;
+  } else if (c->slab) {
     ncclResult_t r;
     if (c->comm_stream) {   // round 2 on the comm stream, the next step's interior K1 meanwhile
       CUDA_OR_THROW(cudaEventRecord(c->ev[2], c->stream));
@@ -1393,7 +1479,8 @@ static void run_step_nccl(zpic_ctx* c) {
 }
 static void slab_join(zpic_ctx* c) {
   if (c->r2_pending) {
-    CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
+    if (c->peer) peer_round2_recv(c, c->cur);
+    else CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
     c->r2_pending = false;
   }
 }
@@ -1472,14 +1559,19 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
     }
     return step_error(c);
   }
-  if (c->slab && c->transport != ZPIC_TRANSPORT_NCCL) {
+  if (c->slab && (c->transport == ZPIC_TRANSPORT_LOOPBACK || c->transport == ZPIC_TRANSPORT_LOOPBACK_PEER)) {
     c->last_error = "loopback slabs are stepped with zpic_step_group";
     return ZPIC_E_STATE;
   }
   try {
     if (c->slab && c->halo_dirty) {
-      ncclResult_t r = nccl_exchange_round2(c, c->cur, c->stream);
-      if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL halo: ") + ncclGetErrorString(r)};
+      if (c->peer) {
+        peer_round2_send(c, c->cur);
+        peer_round2_recv(c, c->cur);
+      } else {
+        ncclResult_t r = nccl_exchange_round2(c, c->cur, c->stream);
+        if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL halo: ") + ncclGetErrorString(r)};
+      }
       c->halo_dirty = false;
     }
     int k = 0;
@@ -1510,24 +1602,42 @@ zpic_status zpic_step_group(zpic_ctx** cs, int32_t count, int32_t n) {
   if (!cs || count < 1 || n < 0) return ZPIC_E_INVALID;
   for (int r = 0; r < count; ++r) {
     zpic_ctx* c = cs[r];
-    if (!c || !c->slab || c->transport != ZPIC_TRANSPORT_LOOPBACK || c->world != count || c->rank != r ||
-        c->stream != cs[0]->stream) {
+    if (!c || !c->slab || c->transport != cs[0]->transport ||
+        (c->transport != ZPIC_TRANSPORT_LOOPBACK && c->transport != ZPIC_TRANSPORT_LOOPBACK_PEER) ||
+        c->world != count || c->rank != r || c->stream != cs[0]->stream) {
       if (c) c->last_error = "zpic_step_group: not one complete loopback group on one stream (ranks in order)";
       return ZPIC_E_STATE;
     }
   }
+  const bool peer = cs[0]->transport == ZPIC_TRANSPORT_LOOPBACK_PEER;
   try {
+    if (peer)   // the group's views of each other's receive areas (one address space)
+      for (int r = 0; r < count; ++r) {
+        cs[r]->peer_lo = cs[cs[r]->lower]->peer_self;
+        cs[r]->peer_hi = cs[cs[r]->upper]->peer_self;
+      }
     if (cs[0]->halo_dirty) {
-      loop_exchange_round2(cs, count, cs[0]->cur);
+      if (peer) {   // every signal is enqueued before the wait that reads it
+        for (int r = 0; r < count; ++r) peer_round2_send(cs[r], cs[r]->cur);
+        for (int r = 0; r < count; ++r) peer_round2_recv(cs[r], cs[r]->cur);
+      } else {
+        loop_exchange_round2(cs, count, cs[0]->cur);
+      }
       for (int r = 0; r < count; ++r) cs[r]->halo_dirty = false;
     }
     for (int k = 0; k < n; ++k) {
       for (int r = 0; r < count; ++r) maybe_sort(cs[r]);
       std::vector<StepState> st(count);
       for (int r = 0; r < count; ++r) st[r] = step_phase_a(cs[r]);
-      loop_exchange_round1(cs, count);
+      if (peer) for (int r = 0; r < count; ++r) peer_round1_send(cs[r]);
+      else loop_exchange_round1(cs, count);
       for (int r = 0; r < count; ++r) step_phase_b(cs[r], st[r]);
-      loop_exchange_round2(cs, count, cs[0]->cur ^ 1);
+      if (peer) {
+        for (int r = 0; r < count; ++r) peer_round2_send(cs[r], cs[r]->cur ^ 1);
+        for (int r = 0; r < count; ++r) peer_round2_recv(cs[r], cs[r]->cur ^ 1);
+      } else {
+        loop_exchange_round2(cs, count, cs[0]->cur ^ 1);
+      }
       for (int r = 0; r < count; ++r) step_phase_c(cs[r], st[r]);
     }
   } catch (const Fail& f) {
@@ -1750,6 +1860,8 @@ void zpic_free(zpic_ctx* c) {
     if (e) cudaEventDestroy(e);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+  for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
+  if (c->peer_block) cudaFree(c->peer_block);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   for (void* p : c->allocations) {
     if (c->opt.free) c->opt.free(p, c->opt.alloc_user);

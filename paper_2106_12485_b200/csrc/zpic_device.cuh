@@ -154,4 +154,22 @@ __device__ __forceinline__ int window_max_4x4_full_warp(const int* h) {
   }
   return __reduce_max_sync(0xffffffffu, m);
 }
+// Particle message: [count, pad x3][cell][x][y][ux][uy][uz][id][species], each `cap` long.
+__host__ __device__ inline size_t msg_bytes(int cap) { return 16 + (size_t)cap * 32; }
+__host__ __device__ inline PList msg_list(void* buf, int cap) {
+  char* b = (char*)buf;
+  PList L;
+  L.count = (int32_t*)b;
+  L.cell = (int32_t*)(b + 16);
+  L.x = (float*)(L.cell + cap);
+  L.y = L.x + cap;
+  L.ux = L.y + cap;
+  L.uy = L.ux + cap;
+  L.uz = L.uy + cap;
+  L.id = (uint32_t*)(L.uz + cap);
+  L.species = (int32_t*)(L.id + cap);
+  L.cap = cap;
+  return L;
+}
+
 }  // namespace zpic

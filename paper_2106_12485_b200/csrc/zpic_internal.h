@@ -152,6 +152,17 @@ struct LaserParams {
   double a0, omega0, fwhm, W0, start, yc;
 };
 
+// A neighbour's receive area of the PEER transports (zpic_peer.cu): its own pointers in a loopback
+// group, CUDA IPC pointers across processes, this context's block in a one-rank ring.
+struct PeerView {
+  float* jrup;       // [3][2][pitch] the upper neighbour's raw J rows -1, 0 (round 1)
+  float* jrdn;       // [3][2][pitch] the lower neighbour's raw J rows ny, ny+1 (round 1)
+  char* pmsg[2];     // particle messages from the lower [0] / upper [1] neighbour (round 1)
+  float* eb_lo;      // [E/B][3][pitch] the lower neighbour's row ny-1: this slab's guard row -1 (round 2)
+  float* eb_hi;      // [E/B][3][2][pitch] the upper neighbour's rows 0, 1: guard rows ny, ny+1 (round 2)
+  unsigned long long* flags;   // [4] epochs: round 1 from lower / upper, round 2 from lower / upper
+};
+
 enum ErrBits { ERR_OVERFLOW = 1, ERR_MIGRATION = 2, ERR_HALO = 8, ERR_HIST = 16 };   // 4: k_count's out-of-slab upload
 
 }  // namespace zpic
@@ -216,7 +227,13 @@ struct zpic_ctx {
   void* pmsg_send[2];  // particle messages to the lower [0] / upper [1] neighbour
   void* pmsg_recv[2];  // from the lower [0] / upper [1] neighbour
   int pcap;
-  bool halo_dirty;   // E/B guard rows of the current buffer must be exchanged before the next step
+  bool halo_dirty;
+  // PEER transports: this context's receive block (cudaMalloc: exportable), the neighbours' views
+  bool peer = false;
+  void* peer_block = nullptr;
+  zpic::PeerView peer_self{}, peer_lo{}, peer_hi{};
+  unsigned long long peer_e1 = 0, peer_e2 = 0;   // rounds 1 / 2 done (the next epoch to signal is +1)
+  std::vector<void*> ipc_open;                   // neighbour blocks opened with cudaIpcOpenMemHandle   // E/B guard rows of the current buffer must be exchanged before the next step
   std::vector<void*> allocations;
   std::string last_error;
   // CUDA graphs of two steps, by step parity (the state a two-step replay returns to)

@@ -65,11 +65,13 @@ class LoopbackGroup:
     """`world` slab contexts of one decomposition in this process, on one GPU and one stream,
     stepped together (zpic_step_group).  Validates the slab exchange logic on a single GPU."""
 
-    def __init__(self, cfg, world, **kw):
+    def __init__(self, cfg, world, transport="loopback", **kw):
+        """transport: "loopback" (the rounds as device copies between the contexts) or
+        "loopback_peer" (the PEER transport's own put / signal / wait kernels)."""
         import torch
         from .zpic import Simulation
         self.stream = torch.cuda.Stream()
-        self.sims = [Simulation(cfg, stream=self.stream, dist={"rank": r, "world": world, "transport": "loopback"},
+        self.sims = [Simulation(cfg, stream=self.stream, dist={"rank": r, "world": world, "transport": transport},
                                 **kw) for r in range(world)]
         self.world = world
         self.cfg = cfg

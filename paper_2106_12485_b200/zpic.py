@@ -58,7 +58,9 @@ class zpic_options(ctypes.Structure):
                 ("current_precision", ctypes.c_int32), ("halo_particles", ctypes.c_int32)]
 
 
-TRANSPORT_NCCL, TRANSPORT_LOOPBACK = 0, 1
+TRANSPORT_NCCL, TRANSPORT_LOOPBACK, TRANSPORT_PEER, TRANSPORT_LOOPBACK_PEER = 0, 1, 2, 3
+TRANSPORTS = {"nccl": TRANSPORT_NCCL, "loopback": TRANSPORT_LOOPBACK, "peer": TRANSPORT_PEER,
+              "loopback_peer": TRANSPORT_LOOPBACK_PEER}
 
 
 class zpic_dist(ctypes.Structure):
@@ -249,7 +251,7 @@ class Simulation:
 
     def __init__(self, cfg, inject=True, track_ids=False, tile=16, profile=False, capacity_slack=1.25,
                  torch_plumbing=True, stream=None, dist=None, current_mode=0, graphs=True, current_precision=0):
-        """dist: None (whole domain) or {"rank", "world", "transport": "nccl" | "loopback",
+        """dist: None (whole domain) or {"rank", "world", "transport": "nccl" | "loopback" | "peer" | "loopback_peer",
         "nccl_id": 128 bytes | "nccl_comm": ncclComm_t address} (y-slab decomposition)."""
         self.cfg = cfg
         self.nx, self.ny = cfg["nx"], cfg["ny"]
@@ -310,7 +312,7 @@ class Simulation:
         if dist is not None:
             dst = zpic_dist()
             dst.rank, dst.world = dist["rank"], dist["world"]
-            dst.transport = TRANSPORT_LOOPBACK if dist.get("transport", "nccl") == "loopback" else TRANSPORT_NCCL
+            dst.transport = TRANSPORTS[dist.get("transport", "nccl")]
             dst.nccl_comm = dist.get("nccl_comm")
             self._nccl_id = ctypes.create_string_buffer(dist["nccl_id"], 128) if dist.get("nccl_id") else None
             dst.nccl_id = ctypes.cast(self._nccl_id, ctypes.c_void_p) if self._nccl_id is not None else None

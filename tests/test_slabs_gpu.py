@@ -199,3 +199,108 @@ def test_nccl_slab_graph_replay_matches_launches(name):
     for s in range(len(parts)):
         for k in pa[s]:
             assert np.array_equal(pa[s][k], pb[s][k]), (s, k)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_loopback_peer_transport_matches_oracle(world):
+    """The PEER transport's kernels (the halo rows and the migrating particles written straight into
+    the neighbours' receive areas, epoch flags signalled and acquired) in a loopback group: C1
+    physics against the oracle (particles after 1 and 10 steps, fields after 10, energies)."""
+    cfg = synth.config("C1", nx=48, ny=40)
+    cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
+    parts = [synth.species_particles(cfg, 0)]
+    from paper_2106_12485_b200.dist import LoopbackGroup
+    g = LoopbackGroup(cfg, world, transport="loopback_peer", inject=False, track_ids=True)
+    g.set_particles(0, parts[0])
+    o = from_config(cfg, particles=parts)
+    fe_g, fe_o = [], []
+    for n in range(12):
+        g.step(1)
+        o.step()
+        it, fe, ke = g.energy()
+        fe_g.append(fe + sum(ke))
+        fe_o.append(o.fe[-1] + sum(o.ke[-1]))
+        if n in (0, 9):
+            c = compare_particles(g.particles(0, True), oracle_particles(o, 0), 48, 40)
+            if n == 0:
+                assert c["pos_max"] <= POS_TOL and c["mom_max"] <= MOM_TOL, c
+            assert c["cell_exact_frac"] >= CELL_FRAC, c
+        if n == 9:
+            for w in (0, 1):
+                assert rel_l2(g.fields(w), o.fields(w)) <= FIELD_TOL, w
+    assert energy_agreement(fe_g, fe_o) <= ENERGY_TOL
+    assert g.counters()["particles"] == len(parts[0]["x"])
+    g.close()
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C4"])
+def test_loopback_peer_equals_loopback_copies(name):
+    """PEER rounds vs the device-copy rounds of the same loopback group (periodic y, open x, and
+    C4's window + open y chain): the same particles (by id) and fields, bit for bit."""
+    if name == "C1":
+        cfg = synth.config("C1", nx=48, ny=64)
+        cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
+    elif name == "C3":
+        cfg = synth.config("C3", nx=96, ny=64)
+        cfg["species"][0].update(x0=0.0, x1=4.8)
+        cfg["species"][1].update(x0=4.8, x1=9.6)
+    else:
+        cfg = synth.config("C4", nx=200, ny=32)
+        cfg["species"][0].update(x0=2.0, x1=2.0 + 20 * cfg["dx"])
+        cfg["laser"] = dict(cfg["laser"], start=cfg["nx"] * cfg["dx"] - 2.0)
+    parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
+    from paper_2106_12485_b200.dist import LoopbackGroup
+    out = []
+    for tr in ("loopback", "loopback_peer"):
+        g = LoopbackGroup(cfg, 4, transport=tr, inject=False, track_ids=True, capacity_slack=1.5)
+        for s, p in enumerate(parts):
+            g.set_particles(s, p)
+        if name == "C4":
+            E, B = synth.laser_fields(cfg)
+            g.set_fields(0, E)
+            g.set_fields(1, B)
+        g.step(10)
+        ps = []
+        for s in range(len(parts)):
+            p = g.particles(s, True)
+            o = np.argsort(p["id"])
+            ps.append({k: v[o] for k, v in p.items()})
+        out.append((g.fields(0), g.fields(1), ps))
+        g.close()
+    (Ea, Ba, pa), (Eb, Bb, pb) = out
+    assert np.array_equal(Ea, Eb) and np.array_equal(Ba, Bb)
+    for s in range(len(parts)):
+        for k in pa[s]:
+            assert np.array_equal(pa[s][k], pb[s][k]), (s, k)
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_peer_transport_self_ring(name):
+    """ZPIC_TRANSPORT_PEER with one rank: the ring's neighbour is the context itself, so every
+    round goes through the put / signal / wait kernels on its own receive block (round 2 pending
+    into the next step's boundary K1, as across GPUs); equal to the unsplit domain."""
+    z = _z()
+    if name == "C1":
+        cfg = synth.config("C1", nx=64, ny=160)
+        cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
+    else:
+        cfg = synth.config("C3", nx=96, ny=160)
+        cfg["species"][0].update(x0=0.0, x1=4.8)
+        cfg["species"][1].update(x0=4.8, x1=9.6)
+    parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
+    ref = z.Simulation(cfg, inject=False, track_ids=True, graphs=False)
+    ring = z.Simulation(cfg, inject=False, track_ids=True, dist={"rank": 0, "world": 1, "transport": "peer"})
+    for s, p in enumerate(parts):
+        ref.set_particles(s, p)
+        ring.set_particles(s, p)
+    ref.step(12)
+    ring.step(7)
+    ring.step(5)
+    for w in (0, 1, 2):
+        assert rel_l2(ring.fields(w), ref.fields(w)) < 2e-5, w
+    for s in range(len(parts)):
+        c = compare_particles(ring.particles(s, True), ref.particles(s, True), cfg["nx"], cfg["ny"],
+                              (cfg["bc"][0] == 0, True))
+        assert c["pos_max"] < 1e-4 and c["cell_exact_frac"] >= CELL_FRAC, c
+    ring.close()
+    ref.close()
