@@ -329,6 +329,9 @@ def main():
     ap.add_argument("--ny", type=int, default=0)
     ap.add_argument("--graphs", action="store_true",
                     help="time zpic_step with CUDA-graph replay (no per-kernel events: no roofline / kernel times)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer"],
+                    help="y-slab halo rounds at N>1: NCCL send / recv, or the library's peer-put kernels over "
+                         "CUDA IPC peer memory (NVLink)")
     ap.add_argument("--current-mode", type=int, default=0, choices=[0, 1],
                     help="0 = tile-block reduction (K4), 1 = commutative global atomics (SURVEY.md NEXT-4)")
     ap.add_argument("--current-precision", default="auto", choices=["auto", "exact"],
@@ -365,7 +368,8 @@ def main():
     dist_kw = None
     if world > 1:   # y-slabs, one per GPU, NCCL send/recv halos
         from paper_2106_12485_b200.dist import nccl_id_broadcast
-        dist_kw = {"rank": rank, "world": world, "transport": "nccl", "nccl_id": nccl_id_broadcast(), "device": local}
+        dist_kw = {"rank": rank, "world": world, "transport": args.transport, "nccl_id": nccl_id_broadcast(),
+                   "device": local}
     sim = z.Simulation(cfg, inject=True, profile=not args.graphs, tile=args.tile, dist=dist_kw,
                        current_mode=args.current_mode, current_precision=args.current_precision)
     n_particles = sim.counters()["particles"]
@@ -429,7 +433,7 @@ def main():
                    "tile": cnt["tile"], "current_mode": ["reduction", "commutative"][args.current_mode],
                    "current_precision": args.current_precision,
                    "l2": "inputs larger than L2 (particle store %.1f GB)" % (n_particles * 24 / 1e9),
-                   "parallelism": "y-slabs x%d" % world},
+                   "parallelism": "y-slabs x%d" % world, "transport": args.transport if world > 1 else None},
         "cell_updates_per_s": n_cells * args.steps / (ms * 1e-3),
         "k1_pushes_per_s": cnt["particles"] / k1_avg_s if k1_n else None,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

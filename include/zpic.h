@@ -118,7 +118,11 @@ typedef struct {
                                  0 = "reduction" (default): every tile stores its private current block
                                      and K4 sums the overlapping guard nodes (no atomics);
                                  1 = "commutative": every tile adds its block into the global J with
-                                     fp32 global atomics (J zeroed first each step, no K4). */
+                                     fp32 global atomics (J zeroed first each step, no K4); on the
+                                     PEER transports the slab-edge tiles and loose particles also add
+                                     their ghost rows (-1, 0 / ny, ny+1) straight into the neighbour
+                                     slab's J over peer memory, so round 1 carries particles only
+                                     (each J zeroed and flagged before any neighbour's K1 adds). */
   int32_t laser;              /* 1 = initialise E, B with a laser pulse: linearly
                                  polarised along y, travelling along +x, E_y = a0 w0 env(x)
                                  exp(-(y - Ly/2)^2 / W0^2) cos(w0 (x - xc)), B_z = E_y at B_z's points;
@@ -160,6 +164,8 @@ typedef struct {
  *     the context's own buffers;
  *   ZPIC_TRANSPORT_LOOPBACK_PEER: the PEER kernels in a loopback group (zpic_step_group; every
  *     signal is enqueued before the wait that reads it, so no kernel ever waits on another).
+ * PEER with current_mode = 1 allocates J with cudaMalloc (exported by CUDA IPC like the receive
+ * block), independent of zpic_options.alloc.
  * Pass NULL for the unsplit single-GPU domain. */
 typedef enum { ZPIC_TRANSPORT_NCCL = 0, ZPIC_TRANSPORT_LOOPBACK = 1, ZPIC_TRANSPORT_PEER = 2,
                ZPIC_TRANSPORT_LOOPBACK_PEER = 3 } zpic_transport;

@@ -53,7 +53,8 @@ size_t particle_msg_bytes(int cap);
 PeerView peer_view(void* block, int pitch, int pcap);
 size_t peer_block_bytes(int pitch, int pcap);
 void launch_peer_put1(const float* J, const GridDesc& g, const void* send_dn, const void* send_up, int pcap,
-                      const PeerView& lo, const PeerView& up, int has_lo, int has_hi, cudaStream_t st);
+                      const PeerView& lo, const PeerView& up, int has_lo, int has_hi, int rows,
+                      cudaStream_t st);
 void launch_peer_put2(const float* E, const float* B, const GridDesc& g, const PeerView& lo, const PeerView& up,
                       int has_lo, int has_hi, cudaStream_t st);
 void launch_peer_apply2(float* E, float* B, const GridDesc& g, const PeerView& self, int has_lo, int has_hi,
@@ -336,6 +337,13 @@ PushParams push_params(zpic_ctx* c) {
     p.send[0] = particle_msg_list(c->pmsg_send[0], c->pcap);
     p.send[1] = particle_msg_list(c->pmsg_send[1], c->pcap);
   }
+  if (c->peer_j) {   // cross-slab commutative current: the neighbours' J
+    p.Jlo = c->has_lo ? c->jlo : nullptr;
+    p.Jhi = c->has_hi ? c->jhi : nullptr;
+    p.lo_plane = c->lo_plane;
+    p.hi_plane = c->hi_plane;
+    p.lo_ny = c->lo_ny;
+  }
   return p;
 }
 
@@ -473,27 +481,51 @@ static void size_lists(zpic_ctx* c, int64_t extra = 0);
 
 // PEER across processes: the CUDA IPC handles of every rank's receive block, all-gathered once on
 // the NCCL communicator; the y neighbours' blocks opened (peer access over NVLink).
+struct PeerRecord {
+  cudaIpcMemHandle_t block, j;   // the receive block; J (cross-slab commutative current only)
+  int32_t ny;
+  int32_t pad[15];
+};
 static void open_peer_blocks(zpic_ctx* c) {
-  cudaIpcMemHandle_t mine;
-  CUDA_OR_THROW(cudaIpcGetMemHandle(&mine, c->peer_block));
-  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  PeerRecord mine{};
+  CUDA_OR_THROW(cudaIpcGetMemHandle(&mine.block, c->peer_block));
+  if (c->peer_j) CUDA_OR_THROW(cudaIpcGetMemHandle(&mine.j, c->j_block));
+  mine.ny = c->g.ny;
+  const size_t hb = sizeof(PeerRecord);
   char* dbuf = alloc_n<char>(c, hb * (c->world + 1));
   CUDA_OR_THROW(cudaMemcpyAsync(dbuf + hb * c->world, &mine, hb, cudaMemcpyHostToDevice, c->stream));
   ncclResult_t r = ncclAllGather(dbuf + hb * c->world, dbuf, hb, ncclChar, (ncclComm_t)c->comm, c->stream);
   if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("PEER handle all-gather: ") + ncclGetErrorString(r)};
-  std::vector<cudaIpcMemHandle_t> all(c->world);
+  std::vector<PeerRecord> all(c->world);
   CUDA_OR_THROW(cudaMemcpyAsync(all.data(), dbuf, hb * c->world, cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
   dev_free(c, dbuf);
-  auto open = [&](int rank) -> PeerView {
-    if (rank == c->rank) return c->peer_self;
-    void* p = nullptr;
-    CUDA_OR_THROW(cudaIpcOpenMemHandle(&p, all[rank], cudaIpcMemLazyEnablePeerAccess));
-    c->ipc_open.push_back(p);
-    return peer_view(p, c->g.pitch, c->pcap);
+  std::vector<void*> opened(2 * c->world, nullptr);   // each peer allocation opened once per process
+  auto open_ptr = [&](int rank, int which) -> void* {
+    if (rank == c->rank) return which ? c->j_block : c->peer_block;
+    void*& p = opened[2 * rank + which];
+    if (!p) {
+      CUDA_OR_THROW(cudaIpcOpenMemHandle(&p, which ? all[rank].j : all[rank].block, cudaIpcMemLazyEnablePeerAccess));
+      c->ipc_open.push_back(p);
+    }
+    return p;
   };
-  if (c->has_lo) c->peer_lo = open(c->lower);
-  if (c->has_hi) c->peer_hi = c->upper == c->lower && c->has_lo ? c->peer_lo : open(c->upper);
+  const long row_floats = c->g.pitch;
+  if (c->has_lo) {
+    c->peer_lo = peer_view(open_ptr(c->lower, 0), c->g.pitch, c->pcap);
+    if (c->peer_j) {
+      c->jlo = (float*)open_ptr(c->lower, 1);
+      c->lo_ny = all[c->lower].ny;
+      c->lo_plane = (long)(all[c->lower].ny + 3) * row_floats;
+    }
+  }
+  if (c->has_hi) {
+    c->peer_hi = peer_view(open_ptr(c->upper, 0), c->g.pitch, c->pcap);
+    if (c->peer_j) {
+      c->jhi = (float*)open_ptr(c->upper, 1);
+      c->hi_plane = (long)(all[c->upper].ny + 3) * row_floats;
+    }
+  }
 }
 
 // The one x sub-row of a ramp species (R16), in the oracle-independent arithmetic of the library:
@@ -630,7 +662,17 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       make_field_tmap(&c->tm[0][b], c->E[b], g, c->T);
       make_field_tmap(&c->tm[1][b], c->B[b], g, c->T);
     }
-    c->J = alloc_n<float>(c, 3 * g.plane);
+    c->peer_j = c->slab && c->opt.current_mode == 1 &&
+                (c->transport == ZPIC_TRANSPORT_PEER || c->transport == ZPIC_TRANSPORT_LOOPBACK_PEER);
+    if (c->peer_j) {   // its own cudaMalloc: the neighbours open it with CUDA IPC
+      CUDA_OR_THROW(cudaMalloc(&c->j_block, sizeof(float) * 3 * g.plane));
+      c->J = (float*)c->j_block;
+      c->jlo = c->jhi = c->J;   // a one-rank ring adds into itself; groups / IPC rebind them
+      c->lo_plane = c->hi_plane = g.plane;
+      c->lo_ny = g.ny;
+    } else {
+      c->J = alloc_n<float>(c, 3 * g.plane);
+    }
     c->Jf = c->opt.filter_passes > 0 ? alloc_n<float>(c, 3 * g.plane) : nullptr;
     // K5's TMA maps (boxes: zpic_kernels.cu YeeBox)
     for (int b = 0; b < 2; ++b) {
@@ -1188,7 +1230,7 @@ bool overlap_round1(const zpic_ctx* c) {
 void peer_round1_send(zpic_ctx* c) {
   c->peer_e1 += 1;
   launch_peer_put1(c->J, c->g, c->pmsg_send[0], c->pmsg_send[1], c->pcap, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi,
-                   c->stream);
+                   c->peer_j ? 0 : 1, c->stream);
   launch_peer_signal(c->has_hi ? c->peer_hi.flags + 0 : nullptr, c->has_lo ? c->peer_lo.flags + 1 : nullptr, c->peer_e1,
                      c->stream);
 }
@@ -1200,6 +1242,19 @@ void peer_round2_send(zpic_ctx* c, int b) {
   launch_peer_put2(c->E[b], c->B[b], c->g, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi, c->stream);
   launch_peer_signal(c->has_hi ? c->peer_hi.flags + 2 : nullptr, c->has_lo ? c->peer_lo.flags + 3 : nullptr, c->peer_e2,
                      c->stream);
+}
+// Cross-slab commutative current: J zeroed, then "zeroed" signalled to both neighbours (whose K1
+// adds into this J only after they waited for it, before their first K1 launch of the step).
+void peer_zero_j(zpic_ctx* c) {
+  CUDA_OR_THROW(cudaMemsetAsync(c->J, 0, (size_t)3 * c->g.plane * sizeof(float), c->stream));
+  c->peer_e0 += 1;
+  launch_peer_signal(c->has_hi ? c->peer_hi.flags + 4 : nullptr, c->has_lo ? c->peer_lo.flags + 5 : nullptr, c->peer_e0,
+                     c->stream);
+  c->j_zeroed = true;
+}
+void peer_zero_wait(zpic_ctx* c) {
+  launch_peer_wait(c->peer_self.flags, c->has_lo ? 4 : -1, c->has_hi ? 5 : -1, c->peer_e0, c->err, c->stream);
+  c->j_zeroed = false;
 }
 void peer_round2_recv(zpic_ctx* c, int b) {
   launch_peer_wait(c->peer_self.flags, c->has_lo ? 2 : -1, c->has_hi ? 3 : -1, c->peer_e2, c->err, c->stream);
@@ -1217,7 +1272,13 @@ StepState step_phase_a(zpic_ctx* c) {
   const PushParams& p = s.p;
   if (p.commutative) {   // the tiles add into J: start from zero (guards included)
     ProfScope ps(c, K_ASSEMBLE);
-    CUDA_OR_THROW(cudaMemsetAsync(c->J, 0, (size_t)3 * c->g.plane * sizeof(float), c->stream));
+    if (c->peer_j) {   // and the neighbours add into it too: zeroed on both sides before any K1
+      if (!c->j_zeroed) peer_zero_j(c);
+      peer_zero_wait(c);
+      s.launches += 2;
+    } else {
+      CUDA_OR_THROW(cudaMemsetAsync(c->J, 0, (size_t)3 * c->g.plane * sizeof(float), c->stream));
+    }
   }
   {
     ProfScope ps(c, K_SCALE);
@@ -1249,7 +1310,7 @@ StepState step_phase_a(zpic_ctx* c) {
     ++s.launches;
   }
   { ProfScope ps(c, K_LOOSE); launch_loose(p, grid_small, c->stream); ++s.launches; }
-  {
+  if (!c->peer_j) {   // (cross-slab commutative current: after the neighbours' adds, phase b)
     ProfScope ps(c, K_FOLD);
     launch_guard_x(c->J, c->g, c->bcx == ZPIC_BC_PERIODIC ? 0 : 2, 0, c->stream);
     ++s.launches;
@@ -1295,7 +1356,12 @@ void step_phase_b(zpic_ctx* c, StepState& s) {
   if (c->slab) {
     ProfScope ps(c, K_HALO);
     if (c->peer) peer_round1_wait(c);
-    launch_apply_j_halo(c->J, c->g, c->jrup, c->jrdn, c->has_lo, c->has_hi, c->stream);
+    if (c->peer_j) {   // every add into this J is in: the x-guard fold now
+      launch_guard_x(c->J, c->g, c->bcx == ZPIC_BC_PERIODIC ? 0 : 2, 0, c->stream);
+      ++s.launches;
+    }
+    launch_apply_j_halo(c->J, c->g, c->peer_j ? nullptr : c->jrup, c->peer_j ? nullptr : c->jrdn, c->has_lo, c->has_hi,
+                        c->stream);
     launch_recv_insert(s.p, particle_msg_list(c->pmsg_recv[0], c->pcap), particle_msg_list(c->pmsg_recv[1], c->pcap),
                        c->stream);
     s.launches += 2;
@@ -1442,7 +1508,9 @@ static void run_step_nccl(zpic_ctx* c) {
   StepState s = step_phase_a(c);
   if (c->slab && c->peer) {   // round 1 by the peer-put kernels; interior Yee rows before the wait
     peer_round1_send(c);
-    s.r1_async = c->opt.filter_passes == 0;
+    // interior Yee rows before the wait need a folded J: not with the cross-slab commutative
+    // current, whose x-guard fold waits for the neighbours' adds
+    s.r1_async = c->opt.filter_passes == 0 && !c->peer_j;
   } else if (c->slab) {
     ncclResult_t r;
     if (overlap_round1(c)) {   // round 1 on the comm stream, interior Yee rows meanwhile
@@ -1613,8 +1681,14 @@ zpic_status zpic_step_group(zpic_ctx** cs, int32_t count, int32_t n) {
   try {
     if (peer)   // the group's views of each other's receive areas (one address space)
       for (int r = 0; r < count; ++r) {
-        cs[r]->peer_lo = cs[cs[r]->lower]->peer_self;
-        cs[r]->peer_hi = cs[cs[r]->upper]->peer_self;
+        zpic_ctx* lo = cs[cs[r]->lower];
+        zpic_ctx* hi = cs[cs[r]->upper];
+        cs[r]->peer_lo = lo->peer_self;
+        cs[r]->peer_hi = hi->peer_self;
+        if (cs[r]->peer_j) {
+          cs[r]->jlo = lo->J; cs[r]->lo_plane = lo->g.plane; cs[r]->lo_ny = lo->g.ny;
+          cs[r]->jhi = hi->J; cs[r]->hi_plane = hi->g.plane;
+        }
       }
     if (cs[0]->halo_dirty) {
       if (peer) {   // every signal is enqueued before the wait that reads it
@@ -1627,6 +1701,8 @@ zpic_status zpic_step_group(zpic_ctx** cs, int32_t count, int32_t n) {
     }
     for (int k = 0; k < n; ++k) {
       for (int r = 0; r < count; ++r) maybe_sort(cs[r]);
+      for (int r = 0; r < count; ++r)   // every "zeroed" signal before the first wait for one
+        if (cs[r]->peer_j) peer_zero_j(cs[r]);
       std::vector<StepState> st(count);
       for (int r = 0; r < count; ++r) st[r] = step_phase_a(cs[r]);
       if (peer) for (int r = 0; r < count; ++r) peer_round1_send(cs[r]);
@@ -1862,6 +1938,7 @@ void zpic_free(zpic_ctx* c) {
   if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
   for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
   if (c->peer_block) cudaFree(c->peer_block);
+  if (c->j_block) cudaFree(c->j_block);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   for (void* p : c->allocations) {
     if (c->opt.free) c->opt.free(p, c->opt.alloc_user);

@@ -172,4 +172,22 @@ __host__ __device__ inline PList msg_list(void* buf, int cap) {
   return L;
 }
 
+// Cross-slab commutative current ("adjacent regions ... in any order"): a deposit
+// at node offset o (component c) on this slab's row y <= 0 is also added into the lower neighbour's
+// J at its row y + ny_lo, one on row y >= ny into the upper neighbour's row y - ny (same pitch).
+__device__ __forceinline__ void peer_add_j(const PushParams& p, int c, int y, long o, float v) {
+  if (p.Jlo && y <= 0) atomicAdd(p.Jlo + c * p.lo_plane + o + (long)p.lo_ny * p.g.pitch, v);
+  if (p.Jhi && y >= p.g.ny) atomicAdd(p.Jhi + c * p.hi_plane + o - (long)p.g.ny * p.g.pitch, v);
+}
+// K1L's accumulator in that mode: the slab's own J plus the neighbour's copy of the shared rows
+struct PeerGlobalCurrent {
+  const PushParams* p;
+  __device__ __forceinline__ long index(int i, int k) const { return p->g.at(i, k); }
+  __device__ __forceinline__ long row() const { return p->g.pitch; }
+  __device__ __forceinline__ void add(int c, long o, float v) const {
+    atomicAdd(p->J + c * p->g.plane + o, v);
+    peer_add_j(*p, c, (int)(o / p->g.pitch) - 1, o, v);
+  }
+};
+
 }  // namespace zpic

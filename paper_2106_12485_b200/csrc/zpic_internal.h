@@ -119,6 +119,13 @@ struct PushParams {
   int check_occ;        // 1: K1s verifies hist against a recount (ZPIC_CHECK_OCC; tests)
   float qmax;           // max_s |q_s|
   int tile0;            // K1 launches over tiles [tile0, tile0 + grid) (the slab overlap splits it)
+  // Cross-slab "commutative" current (PEER transport + current_mode 1): deposits on
+  // this slab's rows -1, 0 are also added into the lower neighbour's J rows ny_lo - 1, ny_lo, those on
+  // rows ny, ny + 1 into the upper neighbour's rows 0, 1 (peer pointers; null = not this mode / edge)
+  float* Jlo;
+  float* Jhi;
+  long lo_plane, hi_plane;
+  int lo_ny;
   double* ke_slots; // [kMaxSpecies][kEnergySlots]
   int* err;         // sticky device error flags (bit 0 overflow, bit 1 migration)
 };
@@ -160,7 +167,8 @@ struct PeerView {
   char* pmsg[2];     // particle messages from the lower [0] / upper [1] neighbour (round 1)
   float* eb_lo;      // [E/B][3][pitch] the lower neighbour's row ny-1: this slab's guard row -1 (round 2)
   float* eb_hi;      // [E/B][3][2][pitch] the upper neighbour's rows 0, 1: guard rows ny, ny+1 (round 2)
-  unsigned long long* flags;   // [4] epochs: round 1 from lower / upper, round 2 from lower / upper
+  unsigned long long* flags;   // [6] epochs: round 1 from lower / upper, round 2 from lower / upper,
+                               // J zeroed by the lower / upper neighbour (cross-slab commutative current)
 };
 
 enum ErrBits { ERR_OVERFLOW = 1, ERR_MIGRATION = 2, ERR_HALO = 8, ERR_HIST = 16 };   // 4: k_count's out-of-slab upload
@@ -233,6 +241,15 @@ struct zpic_ctx {
   void* peer_block = nullptr;
   zpic::PeerView peer_self{}, peer_lo{}, peer_hi{};
   unsigned long long peer_e1 = 0, peer_e2 = 0;   // rounds 1 / 2 done (the next epoch to signal is +1)
+  // cross-slab commutative current (PEER + current_mode 1): J in its own cudaMalloc (exportable),
+  // the neighbours' J, their planes and the lower's ny; e0 counts the "J zeroed" signals
+  bool peer_j = false, j_zeroed = false;
+  void* j_block = nullptr;
+  float* jlo = nullptr;
+  float* jhi = nullptr;
+  long lo_plane = 0, hi_plane = 0;
+  int lo_ny = 0;
+  unsigned long long peer_e0 = 0;
   std::vector<void*> ipc_open;                   // neighbour blocks opened with cudaIpcOpenMemHandle   // E/B guard rows of the current buffer must be exchanged before the next step
   std::vector<void*> allocations;
   std::string last_error;

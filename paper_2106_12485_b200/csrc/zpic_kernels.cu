@@ -399,11 +399,13 @@ __global__ void __launch_bounds__(kBlock) k_push_loose(PushParams p) {
     int di, dj;
     Seg seg[3];
     const int nseg = split_path(ix, iy, x, y, dxp, dyp, sc.q * uz * rg, seg, di, dj);
-    for (int q = 0; q < nseg; ++q) deposit_seg(A, seg[q], sc.jx, sc.jy);
+    if (p.Jlo || p.Jhi) for (int q = 0; q < nseg; ++q) deposit_seg(PeerGlobalCurrent{&p}, seg[q], sc.jx, sc.jy);
+    else for (int q = 0; q < nseg; ++q) deposit_seg(A, seg[q], sc.jx, sc.jy);
     ix += di - p.shift; iy += dj;
     if (domain_bc(ix, iy, p)) insert_particle(p, s, ix, iy, x, y, ux, uy, uz, id);
   }
   for (int s = 0; s < p.nspecies; ++s) block_add_double((double)ke[s], p.ke_slots + s * kEnergySlots + (blockIdx.x & (kEnergySlots - 1)));
+  if (p.Jlo || p.Jhi) __threadfence_system();
 }
 
 // =============================================================================================
@@ -885,15 +887,19 @@ __global__ void k_apply_j_halo(float* J, GridDesc g, const float* rup, const flo
   float* F = J + c * g.plane + col;
   const long P = g.pitch;
   if (has_hi) {
-    F[(long)g.ny * P] += rup[(2 * c) * P + col];                       // row ny-1
-    F[(long)(g.ny + 1) * P] += rup[(2 * c + 1) * P + col];             // guard row ny
+    if (rup) {   // (null: the cross-slab commutative current added these rows already)
+      F[(long)g.ny * P] += rup[(2 * c) * P + col];                     // row ny-1
+      F[(long)(g.ny + 1) * P] += rup[(2 * c + 1) * P + col];           // guard row ny
+    }
   } else {
     F[(long)(g.ny + 1) * P] = 0.f;
     F[(long)(g.ny + 2) * P] = 0.f;
   }
   if (has_lo) {
-    F[1 * P] += rdn[(2 * c) * P + col];                                // row 0
-    F[2 * P] += rdn[(2 * c + 1) * P + col];                            // row 1
+    if (rdn) {
+      F[1 * P] += rdn[(2 * c) * P + col];                              // row 0
+      F[2 * P] += rdn[(2 * c + 1) * P + col];                          // row 1
+    }
   } else {
     F[0] = 0.f;                                                        // guard row -1
   }

@@ -10,7 +10,9 @@
 // round's epoch into the receiver's flag) and, on the receiver, one wait kernel (an acquire spin
 // until the flag reaches the epoch, bounded: a neighbour that never signals sets ERR_HALO instead
 // of hanging the GPU).  Flags in the receiver's block: [0] round 1 from its lower neighbour, [1]
-// round 1 from its upper one, [2] round 2 from the lower, [3] round 2 from the upper.
+// round 1 from its upper one, [2] round 2 from the lower, [3] round 2 from the upper, [4] / [5] J
+// zeroed by the lower / upper neighbour (cross-slab commutative current: from then on the
+// neighbours' K1 may add into this slab's J).
 // Reuse of an area is ordered by the protocol: a sender overwrites the receiver's round-1 area only
 // after it waited for the receiver's round 2 of the previous step, which the receiver sends after it
 // consumed that area.
@@ -34,7 +36,7 @@ struct PeerLayout {
     eb_lo = pmsg1 + mb;
     eb_hi = eb_lo + (size_t)2 * 3 * pitch * 4;
     flags = eb_hi + (size_t)2 * 3 * 2 * pitch * 4;
-    bytes = flags + 4 * sizeof(unsigned long long);
+    bytes = flags + 6 * sizeof(unsigned long long);
   }
 };
 PeerView peer_view(void* block, int pitch, int pcap) {
@@ -66,12 +68,13 @@ __device__ __forceinline__ void copy_msg(const char* src, char* dst, int pcap, l
 }
 
 // Round 1: raw J rows ny, ny+1 and the up-going particles into the upper neighbour's area, raw J
-// rows -1, 0 and the down-going particles into the lower neighbour's area.
+// rows -1, 0 and the down-going particles into the lower neighbour's area (rows = 0: particles
+// only; the cross-slab commutative current already added the rows into the neighbours' J).
 __global__ void k_peer_put1(const float* J, GridDesc g, const char* send_dn, const char* send_up, int pcap,
-                            PeerView lo, PeerView up, int has_lo, int has_hi) {
+                            PeerView lo, PeerView up, int has_lo, int has_hi, int rows) {
   const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long)gridDim.x * blockDim.x;
   const int P = g.pitch;
-  for (long k = tid; k < 6L * P; k += nth) {
+  for (long k = tid; k < (rows ? 6L * P : 0L); k += nth) {
     const int c = (int)(k / (2 * P)), r = (int)((k / P) % 2), x = (int)(k % P);
     if (has_hi) up.jrdn[(c * 2 + r) * P + x] = crow(J, g, c, g.ny + r)[x];
     if (has_lo) lo.jrup[(c * 2 + r) * P + x] = crow(J, g, c, r - 1)[x];
@@ -119,6 +122,8 @@ __global__ void k_peer_signal(unsigned long long* fa, unsigned long long* fb, un
 }
 
 // One thread: acquire-spin until flags[ia] (and flags[ib]) reach the epoch (-1: not waited for).
+// A wait is always enqueued after the signal it reads when both ranks share a stream (loopback
+// groups, the one-rank ring), so on one GPU no wait kernel depends on a concurrently running one.
 // Bounded (~20 s of GPU clock): a neighbour that never signals sets ERR_HALO instead of hanging.
 __global__ void k_peer_wait(const unsigned long long* flags, int ia, int ib, unsigned long long e, int* err) {
   const long long t0 = clock64();
@@ -136,8 +141,9 @@ __global__ void k_peer_wait(const unsigned long long* flags, int ia, int ib, uns
 }
 
 void launch_peer_put1(const float* J, const GridDesc& g, const void* send_dn, const void* send_up, int pcap,
-                      const PeerView& lo, const PeerView& up, int has_lo, int has_hi, cudaStream_t st) {
-  k_peer_put1<<<148, 256, 0, st>>>(J, g, (const char*)send_dn, (const char*)send_up, pcap, lo, up, has_lo, has_hi);
+                      const PeerView& lo, const PeerView& up, int has_lo, int has_hi, int rows, cudaStream_t st) {
+  k_peer_put1<<<148, 256, 0, st>>>(J, g, (const char*)send_dn, (const char*)send_up, pcap, lo, up, has_lo, has_hi,
+                                   rows);
 }
 void launch_peer_put2(const float* E, const float* B, const GridDesc& g, const PeerView& lo, const PeerView& up,
                       int has_lo, int has_hi, cudaStream_t st) {

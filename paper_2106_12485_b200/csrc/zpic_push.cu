@@ -416,8 +416,13 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
       const float v = fast2 ? (float)s_j[k] * ldexpf(1.0f, -s_occ)
                            : (float)(fma((double)s_j[k], 32768.0, (double)s_jlo[k]) * kFxInv);
       const int c = k / (WJ * WJ), r = k % (WJ * WJ);
-      if (v != 0.0f) atomicAdd(p.J + c * pl + p.g.at(i0 - 1 + r % WJ, j0 - 1 + r / WJ), v);
+      if (v != 0.0f) {
+        const long o = p.g.at(i0 - 1 + r % WJ, j0 - 1 + r / WJ);
+        atomicAdd(p.J + c * pl + o, v);
+        if (p.Jlo || p.Jhi) peer_add_j(p, c, j0 - 1 + r / WJ, o, v);   // a slab-edge tile row
+      }
     }
+    if (p.Jlo || p.Jhi) __threadfence_system();   // the neighbours' round-1 wait follows this kernel
   } else if (fast2) {
     float* jt = p.Jt + (long)t * 3 * WJ * WJ;
     const float finv = ldexpf(1.0f, -s_occ);

@@ -18,9 +18,9 @@ def _z():
     return z
 
 
-def _group(cfg, world, parts, laser=False):
+def _group(cfg, world, parts, laser=False, **kw):
     from paper_2106_12485_b200.dist import LoopbackGroup
-    g = LoopbackGroup(cfg, world, inject=False, track_ids=True)
+    g = LoopbackGroup(cfg, world, inject=False, track_ids=True, **kw)
     for s, p in enumerate(parts):
         g.set_particles(s, p)
     if laser:
@@ -30,9 +30,9 @@ def _group(cfg, world, parts, laser=False):
     return g
 
 
-def _run_vs_oracle(cfg, world, steps, laser=False):
+def _run_vs_oracle(cfg, world, steps, laser=False, **kw):
     parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
-    g = _group(cfg, world, parts, laser)
+    g = _group(cfg, world, parts, laser, **kw)
     o = from_config(cfg, particles=parts)
     per = (cfg["bc"][0] == 0, cfg["bc"][1] == 0)
     fe_g, fe_o = [], []
@@ -201,36 +201,31 @@ def test_nccl_slab_graph_replay_matches_launches(name):
             assert np.array_equal(pa[s][k], pb[s][k]), (s, k)
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_loopback_peer_transport_matches_oracle(world):
-    """The PEER transport's kernels (the halo rows and the migrating particles written straight into
-    the neighbours' receive areas, epoch flags signalled and acquired) in a loopback group: C1
-    physics against the oracle (particles after 1 and 10 steps, fields after 10, energies)."""
-    cfg = synth.config("C1", nx=48, ny=40)
-    cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
-    parts = [synth.species_particles(cfg, 0)]
-    from paper_2106_12485_b200.dist import LoopbackGroup
-    g = LoopbackGroup(cfg, world, transport="loopback_peer", inject=False, track_ids=True)
-    g.set_particles(0, parts[0])
-    o = from_config(cfg, particles=parts)
-    fe_g, fe_o = [], []
-    for n in range(12):
-        g.step(1)
-        o.step()
-        it, fe, ke = g.energy()
-        fe_g.append(fe + sum(ke))
-        fe_o.append(o.fe[-1] + sum(o.ke[-1]))
-        if n in (0, 9):
-            c = compare_particles(g.particles(0, True), oracle_particles(o, 0), 48, 40)
-            if n == 0:
-                assert c["pos_max"] <= POS_TOL and c["mom_max"] <= MOM_TOL, c
-            assert c["cell_exact_frac"] >= CELL_FRAC, c
-        if n == 9:
-            for w in (0, 1):
-                assert rel_l2(g.fields(w), o.fields(w)) <= FIELD_TOL, w
-    assert energy_agreement(fe_g, fe_o) <= ENERGY_TOL
-    assert g.counters()["particles"] == len(parts[0]["x"])
-    g.close()
+PEER_CASES = [(n, w, cm) for n in ("C1", "C3", "C4") for w in (2, 4) for cm in (0, 1)]
+
+
+@pytest.mark.parametrize("name,world,current_mode", PEER_CASES)
+def test_loopback_peer_transport_matches_oracle(name, world, current_mode):
+    """The PEER transport's kernels in a loopback group against the oracle (particles after 1,
+    10 and the last step, fields after 10, energies): current_mode 0 = the reduction (raw J rows
+    and particles written into the neighbours' receive areas, epoch flags), 1 = the cross-slab
+    "commutative" current (the slab-edge tiles and loose particles add their
+    ghost rows straight into the neighbours' J; "zeroed" flags before any K1, the x-guard fold
+    after the round-1 wait).  C1 periodic, C3 open x, C4 window + filter + open y."""
+    if name == "C1":
+        cfg = synth.config("C1", nx=48, ny=64)
+        cfg["species"][0]["uth"] = (0.3, 0.3, 0.3)
+        _run_vs_oracle(cfg, world, 12, transport="loopback_peer", current_mode=current_mode)
+    elif name == "C3":
+        cfg = synth.config("C3", nx=128, ny=32)
+        cfg["species"][0].update(x0=0.0, x1=6.4, uth=(0.1, 0.1, 0.1))
+        cfg["species"][1].update(x0=6.4, x1=12.8, uth=(0.1, 0.1, 0.1))
+        _run_vs_oracle(cfg, world, 20, transport="loopback_peer", current_mode=current_mode)
+    else:
+        cfg = synth.config("C4", nx=400, ny=64)
+        cfg["species"][0].update(x0=2.0, x1=2.4)
+        cfg["laser"] = dict(cfg["laser"], start=400 * cfg["dx"] - 2.0)
+        _run_vs_oracle(cfg, world, 20, laser=True, transport="loopback_peer", current_mode=current_mode)
 
 
 @pytest.mark.parametrize("name", ["C1", "C3", "C4"])
@@ -274,11 +269,13 @@ def test_loopback_peer_equals_loopback_copies(name):
             assert np.array_equal(pa[s][k], pb[s][k]), (s, k)
 
 
-@pytest.mark.parametrize("name", ["C1", "C3"])
-def test_peer_transport_self_ring(name):
+@pytest.mark.parametrize("name,current_mode", [("C1", 0), ("C3", 0), ("C1", 1), ("C3", 1)])
+def test_peer_transport_self_ring(name, current_mode):
     """ZPIC_TRANSPORT_PEER with one rank: the ring's neighbour is the context itself, so every
     round goes through the put / signal / wait kernels on its own receive block (round 2 pending
-    into the next step's boundary K1, as across GPUs); equal to the unsplit domain."""
+    into the next step's boundary K1, as across GPUs); with current_mode 1 the slab-edge tiles add
+    their ghost rows into their own J through the peer path (the periodic y fold).  Equal to the
+    unsplit domain."""
     z = _z()
     if name == "C1":
         cfg = synth.config("C1", nx=64, ny=160)
@@ -288,8 +285,9 @@ def test_peer_transport_self_ring(name):
         cfg["species"][0].update(x0=0.0, x1=4.8)
         cfg["species"][1].update(x0=4.8, x1=9.6)
     parts = [synth.species_particles(cfg, s) for s in range(len(cfg["species"]))]
-    ref = z.Simulation(cfg, inject=False, track_ids=True, graphs=False)
-    ring = z.Simulation(cfg, inject=False, track_ids=True, dist={"rank": 0, "world": 1, "transport": "peer"})
+    ref = z.Simulation(cfg, inject=False, track_ids=True, graphs=False, current_mode=current_mode)
+    ring = z.Simulation(cfg, inject=False, track_ids=True, dist={"rank": 0, "world": 1, "transport": "peer"},
+                        current_mode=current_mode)
     for s, p in enumerate(parts):
         ref.set_particles(s, p)
         ring.set_particles(s, p)
