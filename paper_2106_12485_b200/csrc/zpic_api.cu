@@ -166,10 +166,12 @@ void alloc_store(zpic_ctx* c, int s, int cap) {
   ps.nf = c->opt.track_ids ? 7 : 6;
   ps.data = (uint32_t*)dev_alloc(c, n * ps.nf * sizeof(uint32_t));   // contents defined by cnt, no memset
   ps.cnt = alloc_n<int32_t>(c, c->ntiles);
-  // mailboxes: an edge box holds half a tile column of the species' lattice, a corner box 32
+  // mailboxes: an edge box holds half a tile column of the species' lattice, a corner box 32;
+  // with a moving window 1.5 columns (every shift moves each tile's first column into the -x box)
   MailBox& M = c->mail[s];
   const int ppc = c->species[s].ppc[0] * c->species[s].ppc[1];
-  M.cap_edge = round_up(std::max(32, std::min(c->T * ppc / 2, cap)), 32);
+  const int edge = c->bcx == ZPIC_BC_MOVING_WINDOW ? c->T * ppc * 3 / 2 : c->T * ppc / 2;
+  M.cap_edge = round_up(std::max(32, std::min(edge, cap)), 32);
   M.cap_corner = 32;
   M.per_tile = 4 * M.cap_edge + 4 * M.cap_corner;
   M.stride = (long)c->ntiles * M.per_tile;

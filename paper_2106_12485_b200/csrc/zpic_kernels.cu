@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "zpic_device.cuh"
 
@@ -871,6 +872,86 @@ __global__ void k_filter_x(const float* __restrict__ Jin, float* __restrict__ Jo
   }
 }
 
+// The same filter with the passes in registers (total passes <= kFiltR): one thread per kFiltCW
+// consecutive outputs of a row, reading the window of the kFiltCW + 2 R inputs around them
+// straight from J (aligned 16-byte loads away from the row ends; the rows are L2-resident after
+// K4) and applying the passes to the shrinking window without shared memory or barriers, so
+// every SM keeps many rows' loads in flight (the row-per-CTA form above is latency-bound).
+// Positions outside the row are the periodic images (the refresh before every pass makes the
+// passes a circular convolution) or zero after every pass (the zero guards); the values and the
+// order of operations per node are those of k_filter_x, so the result is the same bit for bit.
+constexpr int kFiltCW = 8, kFiltR = 8;
+template <int R>
+__global__ void __launch_bounds__(256) k_filter_x_reg(const float* __restrict__ Jin, float* __restrict__ Jout, GridDesc g,
+                                                       int npass, int compensated, int periodic) {
+  static_assert(R <= 8, "the 16-byte window covers i0 - 8 .. i0 + 15");
+  const int nx = g.nx;
+  const int nch = (nx + kFiltCW - 1) / kFiltCW;
+  const long idx = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (long)nch * 3 * g.ny) return;
+  const int row = (int)(idx / nch), i0 = (int)(idx - (long)row * nch) * kFiltCW;
+  const int j = row % g.ny, c = row / g.ny;
+  const float* in = Jin + c * g.plane + g.at(0, j);   // interior column 0 of the row
+  float* out = Jout + c * g.plane + g.at(0, j);
+  constexpr int W = kFiltCW + 2 * R;
+  float a[W];
+  if (i0 >= 8 && i0 + 16 <= nx) {   // (in + i0 is 16-byte aligned: kXOff = 4, pitch % 32 == 0)
+    float f[24];
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(in + i0 - 8) + m);
+      f[4 * m] = v.x; f[4 * m + 1] = v.y; f[4 * m + 2] = v.z; f[4 * m + 3] = v.w;
+    }
+#pragma unroll
+    for (int k = 0; k < W; ++k) a[k] = f[k + 8 - R];
+  } else {
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+      int i = i0 - R + k;
+      const bool inside = i >= 0 && i < nx;
+      if (periodic) i = ((i % nx) + nx) % nx;
+      a[k] = (inside || periodic) ? in[i] : 0.f;
+    }
+  }
+  const int total = npass + (compensated && npass > 0 ? 1 : 0);
+#pragma unroll
+  for (int pass = 0; pass < R; ++pass) {
+    if (pass < total) {
+      const bool comp = pass == npass;
+      const float side = comp ? -0.25f * npass : 0.25f, centre = comp ? 1.0f + 0.5f * npass : 0.5f;
+      float prev = a[pass];   // the old value left of k (updated in place, left to right)
+#pragma unroll
+      for (int k = pass + 1; k < W - pass - 1; ++k) {
+        const float v = side * prev + centre * a[k] + side * a[k + 1];
+        prev = a[k];
+        const int i = i0 - R + k;
+        a[k] = (periodic || (i >= 0 && i < nx)) ? v : 0.f;
+      }
+    }
+  }
+  // a[R + q] is output i0 + q (the window shrank by one per pass from each side: R >= passes)
+  if (i0 + kFiltCW <= nx) {
+    reinterpret_cast<float4*>(out + i0)[0] = make_float4(a[R], a[R + 1], a[R + 2], a[R + 3]);
+    reinterpret_cast<float4*>(out + i0)[1] = make_float4(a[R + 4], a[R + 5], a[R + 6], a[R + 7]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < kFiltCW; ++q)
+      if (i0 + q < nx) out[i0 + q] = a[R + q];
+  }
+  // the x guards of the row: the periodic images of the filtered row (the threads that computed
+  // them write them), or zero
+  if (i0 == 0) {
+    out[nx] = periodic ? a[R] : 0.f;
+    out[nx + 1] = periodic ? a[R + 1] : 0.f;
+  }
+  if (i0 + kFiltCW >= nx) {
+    float last = 0.f;
+#pragma unroll
+    for (int q = 0; q < kFiltCW; ++q) last = i0 + q == nx - 1 ? a[R + q] : last;   // (registers only)
+    out[-1] = periodic ? last : 0.f;
+  }
+}
+
 // ---- y-slab decomposition (§8(e)) -----------------------------------------------------------
 // Round 1, current: the rows arrive raw (x-folded, not y-folded).  From the upper neighbour:
 // its raw rows -1, 0 (rup[c][0..1]); from the lower neighbour: its raw rows ny, ny+1
@@ -1180,6 +1261,16 @@ void launch_filter_x(const float* Jin, float* Jout, const GridDesc& g, int npass
   if (smem > 48 * 1024 && smem > attr) {
     cudaFuncSetAttribute(k_filter_x, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr = smem;
+  }
+  const int total = npass + (compensated && npass > 0 ? 1 : 0);
+  static const bool v1 = [] { const char* e = getenv("ZPIC_FILTER_V1"); return e && atoi(e); }();
+  if (total <= kFiltR && !v1) {   // the register form (same result bit for bit)
+    const long n = (long)((g.nx + kFiltCW - 1) / kFiltCW) * 3 * g.ny;
+    const int grid = (int)((n + 255) / 256);
+    if (total <= 2) k_filter_x_reg<2><<<grid, 256, 0, st>>>(Jin, Jout, g, npass, compensated, periodic);
+    else if (total <= 5) k_filter_x_reg<5><<<grid, 256, 0, st>>>(Jin, Jout, g, npass, compensated, periodic);
+    else k_filter_x_reg<kFiltR><<<grid, 256, 0, st>>>(Jin, Jout, g, npass, compensated, periodic);
+    return;
   }
   k_filter_x<<<3 * g.ny, kBlock, smem, st>>>(Jin, Jout, g, npass, compensated, periodic);
 }
