@@ -96,7 +96,12 @@ __global__ void __launch_bounds__(kBlock) k_insert(PushParams p) {
 // the neighbour n = tile - delta(d), read and written with consecutive lanes (coalesced loads
 // from the box, coalesced stores into the AoSoA segment).  The warp owns the tile's count in
 // this kernel; a full segment sends the rest to the loose list.
-__global__ void __launch_bounds__(kBlock) k_mail_gather(PushParams p) {
+// 8 CTAs / SM (32 registers, a 16-byte spill): K3m is latency-bound, the extra warps in flight
+// take it from 0.30 to 0.26 ms at C5 (same-box A/B, profiles/r2_ab_k3m.log)
+#ifndef K3M_MINB
+#define K3M_MINB 8
+#endif
+__global__ void __launch_bounds__(kBlock, K3M_MINB) k_mail_gather(PushParams p) {
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int ntiles = p.ntx * p.nty;
   if (w >= ntiles * p.nspecies) return;
@@ -156,7 +161,9 @@ __global__ void __launch_bounds__(kBlock) k_mail_gather(PushParams p) {
     const uint32_t id = M.nf > F_ID ? src[F_ID] : 0u;
     const int slot = pos + e;
     if (slot < ps.cap) {
+#ifndef K3M_NOHIST
       atomicAdd(p.hist + (long)t * p.T * p.T + (cell_iy((int)cell) % p.T) * p.T + cell_ix((int)cell) % p.T, 1);
+#endif
       uint32_t* q = ps.slot((long)t * ps.cap + slot);
       q[F_CELL * 32] = cell; q[F_X * 32] = x; q[F_Y * 32] = y;
       q[F_UX * 32] = ux; q[F_UY * 32] = uy; q[F_UZ * 32] = uz;
