@@ -146,8 +146,10 @@ def test_c4_lwfa_window_filter_reduced():
         if n == 9:
             for w in (0, 1):
                 assert rel_l2(g.fields(w), o.fields(w)) <= FIELD_TOL, (w, rel_l2(g.fields(w), o.fields(w)))
-            assert rel_l2(g.fields(3), o.fields(3)) <= 1e-3
-            assert rel_l2(g.fields(2), o.fields(2)) <= 1e-3
+            # J and the charge density after 10 steps: measured 1.8e-7 and 1.7e-7 (round 2); the
+            # bar is the fields' (north star 1e-4), tightened from round 1's 1e-3
+            assert rel_l2(g.fields(3), o.fields(3)) <= FIELD_TOL
+            assert rel_l2(g.fields(2), o.fields(2)) <= FIELD_TOL
     assert o.n_move == 28
     assert energy_agreement(fe_g, fe_o) <= ENERGY_TOL
     assert energy_agreement(ke_g, ke_o) <= ENERGY_TOL
