@@ -82,6 +82,29 @@ def test_ctypes_structs_match_the_header(tmp_path):
             assert int(got["%s.%s" % (name, f[0])]) == getattr(cls, f[0]).offset, (name, f[0])
 
 
+def test_enum_constants_match_the_header(tmp_path):
+    """The binding's enum constants (boundaries, density profiles, transports) are the header's."""
+    _build_module().build()
+    import paper_2106_12485_b200 as z
+    zz = z.zpic
+    consts = {"ZPIC_BC_PERIODIC": zz.BC_PERIODIC, "ZPIC_BC_OPEN": zz.BC_OPEN,
+              "ZPIC_BC_MOVING_WINDOW": zz.BC_MOVING_WINDOW, "ZPIC_TRANSPORT_NCCL": zz.TRANSPORT_NCCL,
+              "ZPIC_TRANSPORT_LOOPBACK": zz.TRANSPORT_LOOPBACK, "ZPIC_TRANSPORT_PEER": zz.TRANSPORT_PEER,
+              "ZPIC_TRANSPORT_LOOPBACK_PEER": zz.TRANSPORT_LOOPBACK_PEER}
+    lines = ['#include <stdio.h>', '#include "zpic.h"', "int main(void) {"]
+    lines += ['printf("%s %%d\\n", (int)%s);' % (k, k) for k in consts]
+    lines.append("return 0; }")
+    src = tmp_path / "enums.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "enums"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), "-o", str(exe), str(src)])
+    got = dict(l.rsplit(" ", 1) for l in subprocess.run([str(exe)], capture_output=True, text=True).stdout.splitlines())
+    for k, v in consts.items():
+        assert int(got[k]) == v, k
+    assert set(zz.TRANSPORTS.values()) == {zz.TRANSPORT_NCCL, zz.TRANSPORT_LOOPBACK, zz.TRANSPORT_PEER,
+                                          zz.TRANSPORT_LOOPBACK_PEER}
+
+
 def _init_status(cfg, profile_override=None):
     """zpic_init's status for a config; the argument checks run before any device call, so this
     needs no GPU (a config that passes them would go on to touch the device: not used here)."""
