@@ -218,6 +218,21 @@ zpic_status zpic_step_group(zpic_ctx** ctxs, int32_t count, int32_t n);
 /* Write a fresh ncclUniqueId (NCCL_UNIQUE_ID_BYTES = 128 bytes) to out (out_len >= 128). */
 zpic_status zpic_nccl_unique_id(void* out, size_t out_len);
 
+/* Self-test of the PEER halo protocol (the ZPIC_TRANSPORT_PEER rounds): `ranks`
+ * emulated slabs of nx x ny cells (a ring if periodic, else a chain), one CTA each in one
+ * cooperative launch on the current device, run `epochs` steps of round 1 (raw J rows -1, 0 /
+ * ny, ny+1 and particle messages of up to pcap records), signal, wait, verify, round 2 (E/B rows),
+ * signal, wait, verify, with the transport's own put / signal / wait code and receive-block
+ * layout; the waits spin on flags the other CTAs store concurrently.  Every value is a hash of
+ * (sender, epoch, place), so a record that arrives late, twice, from the wrong neighbour or into
+ * the wrong area is counted.  *errors_out = mismatched values + 2^40 per wait that exceeded
+ * budget_cycles (GPU clocks).  fault: 0 none; 1 rank 0 corrupts one J value it sent at epoch 2;
+ * 2 rank 0 skips its round-1 signal at epoch 2 (both must make *errors_out non-zero).  Allocates
+ * and frees its own device memory.  ZPIC_E_INVALID for ranks outside [1, 64], epochs < 1, nx < 1,
+ * ny < 4, pcap < 32 or a null errors_out; ZPIC_E_CUDA if allocation or the launch fails. */
+zpic_status zpic_peer_selftest(int32_t ranks, int32_t epochs, int32_t nx, int32_t ny, int32_t pcap, int32_t periodic,
+                               int64_t budget_cycles, int32_t fault, int64_t* errors_out);
+
 /* Block until all enqueued work is done; surface sticky device errors. */
 zpic_status zpic_sync(zpic_ctx* ctx);
 

@@ -19,6 +19,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "zpic_device.cuh"
 
 namespace zpic {
@@ -70,9 +72,10 @@ __device__ __forceinline__ void copy_msg(const char* src, char* dst, int pcap, l
 // Round 1: raw J rows ny, ny+1 and the up-going particles into the upper neighbour's area, raw J
 // rows -1, 0 and the down-going particles into the lower neighbour's area (rows = 0: particles
 // only; the cross-slab commutative current already added the rows into the neighbours' J).
-__global__ void k_peer_put1(const float* J, GridDesc g, const char* send_dn, const char* send_up, int pcap,
-                            PeerView lo, PeerView up, int has_lo, int has_hi, int rows) {
-  const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long)gridDim.x * blockDim.x;
+// Thread tid of nth; the caller fences (system scope) before the round is signalled.
+__device__ __forceinline__ void put1_body(const float* J, const GridDesc& g, const char* send_dn, const char* send_up,
+                                          int pcap, const PeerView& lo, const PeerView& up, int has_lo, int has_hi,
+                                          int rows, long tid, long nth) {
   const int P = g.pitch;
   for (long k = tid; k < (rows ? 6L * P : 0L); k += nth) {
     const int c = (int)(k / (2 * P)), r = (int)((k / P) % 2), x = (int)(k % P);
@@ -81,12 +84,17 @@ __global__ void k_peer_put1(const float* J, GridDesc g, const char* send_dn, con
   }
   if (has_hi) copy_msg(send_up, up.pmsg[0], pcap, tid, nth);
   if (has_lo) copy_msg(send_dn, lo.pmsg[1], pcap, tid, nth);
+}
+__global__ void k_peer_put1(const float* J, GridDesc g, const char* send_dn, const char* send_up, int pcap,
+                            PeerView lo, PeerView up, int has_lo, int has_hi, int rows) {
+  put1_body(J, g, send_dn, send_up, pcap, lo, up, has_lo, has_hi, rows, (long)blockIdx.x * blockDim.x + threadIdx.x,
+            (long)gridDim.x * blockDim.x);
   __threadfence_system();
 }
 
 // Round 2: E/B row ny-1 into the upper neighbour's guard-row area, rows 0, 1 into the lower's.
-__global__ void k_peer_put2(const float* E, const float* B, GridDesc g, PeerView lo, PeerView up, int has_lo, int has_hi) {
-  const long tid = (long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long)gridDim.x * blockDim.x;
+__device__ __forceinline__ void put2_body(const float* E, const float* B, const GridDesc& g, const PeerView& lo,
+                                          const PeerView& up, int has_lo, int has_hi, long tid, long nth) {
   const int P = g.pitch;
   for (long k = tid; k < 6L * P; k += nth) {   // (field, comp) pairs x pitch
     const int fc = (int)(k / P), x = (int)(k % P), f = fc / 3, c = fc % 3;
@@ -97,6 +105,9 @@ __global__ void k_peer_put2(const float* E, const float* B, GridDesc g, PeerView
       lo.eb_hi[(fc * 2 + 1) * P + x] = crow(F, g, c, 1)[x];
     }
   }
+}
+__global__ void k_peer_put2(const float* E, const float* B, GridDesc g, PeerView lo, PeerView up, int has_lo, int has_hi) {
+  put2_body(E, B, g, lo, up, has_lo, has_hi, (long)blockIdx.x * blockDim.x + threadIdx.x, (long)gridDim.x * blockDim.x);
   __threadfence_system();
 }
 
@@ -115,17 +126,14 @@ __global__ void k_peer_apply2(float* E, float* B, GridDesc g, const float* eb_lo
   }
 }
 
-// One thread: release-store the epoch into up to two receivers' flags (system scope: NVLink peers).
-__global__ void k_peer_signal(unsigned long long* fa, unsigned long long* fb, unsigned long long e) {
-  if (fa) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fa), "l"(e) : "memory");
-  if (fb) asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(fb), "l"(e) : "memory");
+// Release-store the epoch into a receiver's flag (system scope: NVLink peers).
+__device__ __forceinline__ void signal_flag(unsigned long long* f, unsigned long long e) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
 }
-
-// One thread: acquire-spin until flags[ia] (and flags[ib]) reach the epoch (-1: not waited for).
-// A wait is always enqueued after the signal it reads when both ranks share a stream (loopback
-// groups, the one-rank ring), so on one GPU no wait kernel depends on a concurrently running one.
-// Bounded (~20 s of GPU clock): a neighbour that never signals sets ERR_HALO instead of hanging.
-__global__ void k_peer_wait(const unsigned long long* flags, int ia, int ib, unsigned long long e, int* err) {
+// Acquire-spin until flags[ia] (and flags[ib]) reach the epoch (-1: not waited for); false when
+// `budget` GPU clock cycles pass first.
+__device__ __forceinline__ bool wait_flags(const unsigned long long* flags, int ia, int ib, unsigned long long e,
+                                           long long budget) {
   const long long t0 = clock64();
   for (int q = 0; q < 2; ++q) {
     const int i = q ? ib : ia;
@@ -134,10 +142,25 @@ __global__ void k_peer_wait(const unsigned long long* flags, int ia, int ib, uns
     for (;;) {
       asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + i) : "memory");
       if (v >= e) break;
-      if (clock64() - t0 > 40000000000LL) { atomicOr(err, ERR_HALO); return; }
+      if (clock64() - t0 > budget) return false;
       __nanosleep(256);
     }
   }
+  return true;
+}
+
+// One thread: release-store the epoch into up to two receivers' flags.
+__global__ void k_peer_signal(unsigned long long* fa, unsigned long long* fb, unsigned long long e) {
+  if (fa) signal_flag(fa, e);
+  if (fb) signal_flag(fb, e);
+}
+
+// One thread: wait for the round's flags.  Bounded (~20 s of GPU clock): a neighbour that never
+// signals sets ERR_HALO instead of hanging.
+// A wait is always enqueued after the signal it reads when both ranks share a stream (loopback
+// groups, the one-rank ring), so on one GPU no wait kernel depends on a concurrently running one.
+__global__ void k_peer_wait(const unsigned long long* flags, int ia, int ib, unsigned long long e, int* err) {
+  if (!wait_flags(flags, ia, ib, e, 40000000000LL)) atomicOr(err, ERR_HALO);
 }
 
 void launch_peer_put1(const float* J, const GridDesc& g, const void* send_dn, const void* send_up, int pcap,
@@ -160,4 +183,185 @@ void launch_peer_wait(const unsigned long long* flags, int ia, int ib, unsigned 
   k_peer_wait<<<1, 1, 0, st>>>(flags, ia, ib, e, err);
 }
 
+// ---- protocol self-test (zpic_peer_selftest) -------------------------------------------------
+// `ranks` emulated slabs of a ring (or chain), one CTA each, in ONE cooperative launch (all CTAs
+// co-resident), run `epochs` steps of the PEER protocol with the production bodies above: round 1
+// (put1_body: J rows + particle messages into the neighbours' areas), signal, wait, consume (here:
+// verify against the content the neighbour wrote for this epoch), round 2 (put2_body), signal,
+// wait, verify.  The waits really spin on flags other CTAs store concurrently, which the loopback
+// groups (one stream, every signal before its wait) never do, so this checks the flag indices, the
+// epochs and the reuse of the receive areas under true concurrency on one GPU (the profiling
+// guide's rule: emulate the ranks inside one kernel rather than as ranks that wait on one another).
+struct SelfRank {
+  float* J;
+  float* E;
+  float* B;
+  char* send[2];
+  PeerView self, lo, hi;
+  int has_lo, has_hi, lower, upper;
+};
+__device__ __forceinline__ uint32_t st_hash(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u ^ (c + 0x165667B1u) * 0xC2B2AE3Du ^ d * 0x27D4EB2Fu;
+  h ^= h >> 15; h *= 0x2C1B3C6Du; h ^= h >> 12;
+  return h;
+}
+__device__ __forceinline__ float st_val(uint32_t h) { return (float)(h & 0xFFFFF); }   // exact in fp32
+// what rank r writes, at epoch e, into row `row` (-1 .. ny+1) of component c of J / E / B
+__device__ __forceinline__ float st_row(int r, int e, int what, int c, int row, int x) {
+  return st_val(st_hash(r, e, what * 8 + c, (uint32_t)(row + 2) * 65536u + x));
+}
+__device__ __forceinline__ int st_count(int r, int e, int d, int pcap) { return (int)(st_hash(r, e, 99, d) % (pcap + 1)); }
+
+// fault (checks that the self-test can fail): 1 = rank 0 overwrites one value of its round-1 J rows in
+// the upper neighbour's area at epoch 2 after the put (a wrong value the receiver must see);
+// 2 = rank 0 does not signal round 1 at epoch 2 (its neighbours' waits must time out).
+__global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epochs, long long budget, int fault,
+                                unsigned long long* errors) {
+  const SelfRank me = ranks[blockIdx.x];
+  const int r = blockIdx.x, tid = threadIdx.x, nth = blockDim.x, P = g.pitch;
+  __shared__ int s_ok;
+  unsigned long long bad = 0;
+  for (int e = 1; e <= epochs; ++e) {
+    // this rank's J rows and messages of epoch e (its own buffers)
+    for (int k = tid; k < 3 * 4 * P; k += nth) {
+      const int c = k / (4 * P), q = (k / P) % 4, x = k % P, row = q < 2 ? q - 1 : g.ny + q - 2;
+      me.J[c * g.plane + (long)(row + 1) * P + x] = st_row(r, e, 0, c, row, x);
+    }
+    for (int d = 0; d < 2; ++d) {
+      const PList L = msg_list(me.send[d], pcap);
+      const int n = st_count(r, e, d, pcap);
+      if (tid == 0) *L.count = n;
+      for (int k = tid; k < n; k += nth) {
+        const uint32_t h = st_hash(r, e, 100 + d, k);
+        L.cell[k] = (int)h; L.x[k] = st_val(h ^ 1); L.y[k] = st_val(h ^ 2); L.ux[k] = st_val(h ^ 3);
+        L.uy[k] = st_val(h ^ 4); L.uz[k] = st_val(h ^ 5); L.id[k] = h ^ 6; L.species[k] = (int)(h & 3);
+      }
+    }
+    __syncthreads();
+    put1_body(me.J, g, me.send[0], me.send[1], pcap, me.lo, me.hi, me.has_lo, me.has_hi, 1, tid, nth);
+    if (fault == 1 && r == 0 && e == 2 && tid == 0 && me.has_hi) me.hi.jrdn[P + 3] += 1.0f;
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) {
+      const bool drop = fault == 2 && r == 0 && e == 2;
+      if (me.has_hi && !drop) signal_flag(me.hi.flags + 0, e);
+      if (me.has_lo && !drop) signal_flag(me.lo.flags + 1, e);
+      s_ok = wait_flags(me.self.flags, me.has_lo ? 0 : -1, me.has_hi ? 1 : -1, e, budget);
+      __threadfence();
+    }
+    __syncthreads();
+    if (!s_ok) { if (tid == 0) atomicAdd(errors, 1ull << 40); return; }
+    // consume round 1: the lower's raw rows ny, ny+1 and up-going particles, the upper's rows -1, 0
+    // and down-going particles
+    for (int k = tid; k < 6 * P; k += nth) {
+      const int c = k / (2 * P), q = (k / P) % 2, x = k % P;
+      if (me.has_lo && me.self.jrdn[(c * 2 + q) * P + x] != st_row(me.lower, e, 0, c, g.ny + q, x)) ++bad;
+      if (me.has_hi && me.self.jrup[(c * 2 + q) * P + x] != st_row(me.upper, e, 0, c, q - 1, x)) ++bad;
+    }
+    for (int side = 0; side < 2; ++side) {   // pmsg[0] from the lower (its up messages), [1] from the upper
+      if (side == 0 ? !me.has_lo : !me.has_hi) continue;
+      const int from = side == 0 ? me.lower : me.upper, d = side == 0 ? 1 : 0;
+      const PList L = msg_list(me.self.pmsg[side], pcap);
+      const int n = st_count(from, e, d, pcap);
+      if (tid == 0 && *L.count != n) ++bad;
+      for (int k = tid; k < n; k += nth) {
+        const uint32_t h = st_hash(from, e, 100 + d, k);
+        if (L.cell[k] != (int)h || L.x[k] != st_val(h ^ 1) || L.y[k] != st_val(h ^ 2) || L.ux[k] != st_val(h ^ 3) ||
+            L.uy[k] != st_val(h ^ 4) || L.uz[k] != st_val(h ^ 5) || L.id[k] != (h ^ 6) || L.species[k] != (int)(h & 3))
+          ++bad;
+      }
+    }
+    // round 2: this rank's E / B rows 0, 1, ny - 1 of epoch e
+    for (int k = tid; k < 2 * 3 * 3 * P; k += nth) {
+      const int f = k / (9 * P), c = (k / (3 * P)) % 3, q = (k / P) % 3, x = k % P, row = q < 2 ? q : g.ny - 1;
+      (f ? me.B : me.E)[c * g.plane + (long)(row + 1) * P + x] = st_row(r, e, 1 + f, c, row, x);
+    }
+    __syncthreads();
+    put2_body(me.E, me.B, g, me.lo, me.hi, me.has_lo, me.has_hi, tid, nth);
+    __threadfence_system();
+    __syncthreads();
+    if (tid == 0) {
+      if (me.has_hi) signal_flag(me.hi.flags + 2, e);
+      if (me.has_lo) signal_flag(me.lo.flags + 3, e);
+      s_ok = wait_flags(me.self.flags, me.has_lo ? 2 : -1, me.has_hi ? 3 : -1, e, budget);
+      __threadfence();
+    }
+    __syncthreads();
+    if (!s_ok) { if (tid == 0) atomicAdd(errors, 1ull << 40); return; }
+    for (int k = tid; k < 6 * P; k += nth) {   // (field, comp) x pitch
+      const int fc = k / P, x = k % P, f = fc / 3, c = fc % 3;
+      if (me.has_lo && me.self.eb_lo[fc * P + x] != st_row(me.lower, e, 1 + f, c, g.ny - 1, x)) ++bad;
+      if (me.has_hi && (me.self.eb_hi[(fc * 2) * P + x] != st_row(me.upper, e, 1 + f, c, 0, x) ||
+                        me.self.eb_hi[(fc * 2 + 1) * P + x] != st_row(me.upper, e, 1 + f, c, 1, x)))
+        ++bad;
+    }
+    __syncthreads();   // every thread verified this epoch's areas before the next epoch's round 1
+  }
+  if (bad) atomicAdd(errors, bad);
+}
+
 }  // namespace zpic
+
+using namespace zpic;
+
+extern "C" zpic_status zpic_peer_selftest(int32_t ranks, int32_t epochs, int32_t nx, int32_t ny, int32_t pcap,
+                                          int32_t periodic, int64_t budget_cycles, int32_t fault, int64_t* errors_out) {
+  if (ranks < 1 || ranks > 64 || epochs < 1 || nx < 1 || ny < 4 || pcap < 32 || !errors_out) return ZPIC_E_INVALID;
+  GridDesc g;
+  g.nx = nx; g.ny = ny;
+  g.pitch = (nx + kXOff + 2 + 31) / 32 * 32;
+  g.rows = ny + 3;
+  g.plane = (long)g.rows * g.pitch;
+  std::vector<void*> mem;
+  auto dalloc = [&](size_t b) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, b) != cudaSuccess) return nullptr;
+    mem.push_back(p);
+    cudaMemset(p, 0, b);
+    return p;
+  };
+  zpic_status st = ZPIC_OK;
+  std::vector<SelfRank> hr(ranks);
+  std::vector<PeerView> views(ranks);
+  for (int r = 0; r < ranks && st == ZPIC_OK; ++r) {
+    void* blk = dalloc(peer_block_bytes(g.pitch, pcap));
+    float* J = (float*)dalloc(3 * g.plane * sizeof(float));
+    float* E = (float*)dalloc(3 * g.plane * sizeof(float));
+    float* B = (float*)dalloc(3 * g.plane * sizeof(float));
+    char* s0 = (char*)dalloc(msg_bytes(pcap));
+    char* s1 = (char*)dalloc(msg_bytes(pcap));
+    if (!blk || !J || !E || !B || !s0 || !s1) { st = ZPIC_E_CUDA; break; }
+    views[r] = peer_view(blk, g.pitch, pcap);
+    hr[r].J = J; hr[r].E = E; hr[r].B = B; hr[r].send[0] = s0; hr[r].send[1] = s1;
+  }
+  if (st == ZPIC_OK) {
+    for (int r = 0; r < ranks; ++r) {
+      hr[r].lower = (r + ranks - 1) % ranks;
+      hr[r].upper = (r + 1) % ranks;
+      hr[r].has_lo = periodic || r > 0;
+      hr[r].has_hi = periodic || r < ranks - 1;
+      hr[r].self = views[r];
+      hr[r].lo = views[hr[r].lower];
+      hr[r].hi = views[hr[r].upper];
+    }
+    SelfRank* dr = (SelfRank*)dalloc(sizeof(SelfRank) * ranks);
+    unsigned long long* derr = (unsigned long long*)dalloc(sizeof(unsigned long long));
+    if (!dr || !derr) st = ZPIC_E_CUDA;
+    if (st == ZPIC_OK) {
+      cudaMemcpy(dr, hr.data(), sizeof(SelfRank) * ranks, cudaMemcpyHostToDevice);
+      long long budget = budget_cycles;
+      int pc = pcap, ep = epochs, fl = fault;
+      void* args[] = {&dr, &g, &pc, &ep, &budget, &fl, &derr};
+      if (cudaLaunchCooperativeKernel((const void*)k_peer_selftest, dim3(ranks), dim3(256), args, 0, 0) != cudaSuccess ||
+          cudaDeviceSynchronize() != cudaSuccess) {
+        st = ZPIC_E_CUDA;
+      } else {
+        unsigned long long h = 0;
+        cudaMemcpy(&h, derr, sizeof(h), cudaMemcpyDeviceToHost);
+        *errors_out = (int64_t)h;
+      }
+    }
+  }
+  for (void* p : mem) cudaFree(p);
+  return st;
+}

@@ -92,18 +92,19 @@ _lib.zpic_counters.argtypes = [_P, _I64P, ctypes.c_int32]
 _lib.zpic_kernel_times.argtypes = [_P, ctypes.POINTER(ctypes.c_char_p), _F64P, _I32P, _I32P]
 _lib.zpic_step_group.argtypes = [ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_int32]
 _lib.zpic_nccl_unique_id.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
+_lib.zpic_peer_selftest.argtypes = [ctypes.c_int32] * 6 + [ctypes.c_int64, ctypes.c_int32, _I64P]
 _lib.zpic_free.argtypes = [_P]
 _lib.zpic_free.restype = None
 _lib.zpic_last_error.argtypes = [_P]
 _lib.zpic_last_error.restype = ctypes.c_char_p
 for _f in ("zpic_init", "zpic_set_particles", "zpic_set_fields", "zpic_step", "zpic_sync", "zpic_get_fields",
            "zpic_get_particles", "zpic_energy", "zpic_layout", "zpic_counters", "zpic_kernel_times",
-           "zpic_step_group", "zpic_nccl_unique_id"):
+           "zpic_step_group", "zpic_nccl_unique_id", "zpic_peer_selftest"):
     getattr(_lib, _f).restype = ctypes.c_int
 
 EXPORTED = ["zpic_init", "zpic_set_particles", "zpic_set_fields", "zpic_step", "zpic_step_group", "zpic_sync",
             "zpic_get_fields", "zpic_get_charge", "zpic_get_particles", "zpic_energy", "zpic_layout", "zpic_counters",
-            "zpic_kernel_times", "zpic_nccl_unique_id", "zpic_free", "zpic_last_error"]
+            "zpic_kernel_times", "zpic_nccl_unique_id", "zpic_peer_selftest", "zpic_free", "zpic_last_error"]
 
 
 class ZpicError(RuntimeError):
@@ -166,6 +167,14 @@ def zpic_nccl_unique_id():
     buf = ctypes.create_string_buffer(128)
     _check(_lib.zpic_nccl_unique_id(buf, 128), None)
     return buf.raw
+
+
+def zpic_peer_selftest(ranks, epochs, nx, ny, pcap, periodic=True, budget_cycles=4_000_000_000, fault=0):
+    """The PEER protocol self-test (include/zpic.h): returns (mismatched values, timed-out waits)."""
+    err = ctypes.c_int64(0)
+    _check(_lib.zpic_peer_selftest(ranks, epochs, nx, ny, pcap, 1 if periodic else 0, budget_cycles, fault,
+                                   ctypes.byref(err)), None)
+    return err.value & ((1 << 40) - 1), err.value >> 40
 
 
 def zpic_sync(ctx):
