@@ -223,7 +223,10 @@ zpic_status zpic_nccl_unique_id(void* out, size_t out_len);
  * cooperative launch on the current device, run `epochs` steps of round 1 (raw J rows -1, 0 /
  * ny, ny+1 and particle messages of up to pcap records), signal, wait, verify, round 2 (E/B rows),
  * signal, wait, verify, with the transport's own put / signal / wait code and receive-block
- * layout; the waits spin on flags the other CTAs store concurrently.  Every value is a hash of
+ * layout; the waits spin on flags the other CTAs store concurrently.  commutative = 1 replaces
+ * the J rows of round 1 by the cross-slab commutative current (J zeroed, "zeroed" signalled and
+ * awaited, the shared rows added into the neighbours' J with peer atomics; after round 1 each
+ * shared row must hold its own plus the neighbour's contribution).  Every value is a hash of
  * (sender, epoch, place), so a record that arrives late, twice, from the wrong neighbour or into
  * the wrong area is counted.  *errors_out = mismatched values + 2^40 per wait that exceeded
  * budget_cycles (GPU clocks).  fault: 0 none; 1 rank 0 corrupts one J value it sent at epoch 2;
@@ -231,7 +234,7 @@ zpic_status zpic_nccl_unique_id(void* out, size_t out_len);
  * and frees its own device memory.  ZPIC_E_INVALID for ranks outside [1, 64], epochs < 1, nx < 1,
  * ny < 4, pcap < 32 or a null errors_out; ZPIC_E_CUDA if allocation or the launch fails. */
 zpic_status zpic_peer_selftest(int32_t ranks, int32_t epochs, int32_t nx, int32_t ny, int32_t pcap, int32_t periodic,
-                               int64_t budget_cycles, int32_t fault, int64_t* errors_out);
+                               int32_t commutative, int64_t budget_cycles, int32_t fault, int64_t* errors_out);
 
 /* Block until all enqueued work is done; surface sticky device errors. */
 zpic_status zpic_sync(zpic_ctx* ctx);

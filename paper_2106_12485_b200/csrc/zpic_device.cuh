@@ -175,9 +175,13 @@ __host__ __device__ inline PList msg_list(void* buf, int cap) {
 // Cross-slab commutative current ("adjacent regions ... in any order"): a deposit
 // at node offset o (component c) on this slab's row y <= 0 is also added into the lower neighbour's
 // J at its row y + ny_lo, one on row y >= ny into the upper neighbour's row y - ny (same pitch).
+__device__ __forceinline__ void peer_add_j(float* Jlo, float* Jhi, long lo_plane, long hi_plane, int lo_ny,
+                                           const GridDesc& g, int c, int y, long o, float v) {
+  if (Jlo && y <= 0) atomicAdd(Jlo + c * lo_plane + o + (long)lo_ny * g.pitch, v);
+  if (Jhi && y >= g.ny) atomicAdd(Jhi + c * hi_plane + o - (long)g.ny * g.pitch, v);
+}
 __device__ __forceinline__ void peer_add_j(const PushParams& p, int c, int y, long o, float v) {
-  if (p.Jlo && y <= 0) atomicAdd(p.Jlo + c * p.lo_plane + o + (long)p.lo_ny * p.g.pitch, v);
-  if (p.Jhi && y >= p.g.ny) atomicAdd(p.Jhi + c * p.hi_plane + o - (long)p.g.ny * p.g.pitch, v);
+  peer_add_j(p.Jlo, p.Jhi, p.lo_plane, p.hi_plane, p.lo_ny, p.g, c, y, o, v);
 }
 // K1L's accumulator in that mode: the slab's own J plus the neighbour's copy of the shared rows
 struct PeerGlobalCurrent {

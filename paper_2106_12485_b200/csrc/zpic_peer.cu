@@ -199,6 +199,9 @@ struct SelfRank {
   char* send[2];
   PeerView self, lo, hi;
   int has_lo, has_hi, lower, upper;
+  float* Jn[2];              // the lower / upper neighbour's J (commutative mode)
+  long lo_plane, hi_plane;
+  int lo_ny;
 };
 __device__ __forceinline__ uint32_t st_hash(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
   uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u ^ (c + 0x165667B1u) * 0xC2B2AE3Du ^ d * 0x27D4EB2Fu;
@@ -215,17 +218,45 @@ __device__ __forceinline__ int st_count(int r, int e, int d, int pcap) { return 
 // fault (checks that the self-test can fail): 1 = rank 0 overwrites one value of its round-1 J rows in
 // the upper neighbour's area at epoch 2 after the put (a wrong value the receiver must see);
 // 2 = rank 0 does not signal round 1 at epoch 2 (its neighbours' waits must time out).
+// commutative = 1: the cross-slab commutative current instead of J rows in round 1: every epoch
+// each rank zeroes its J, signals "zeroed" (flags 4 / 5), waits for its neighbours' "zeroed", adds
+// its contributions on rows -1, 0, ny, ny + 1 into its own J and through peer_add_j into the
+// neighbours' J (RED over peer memory), fences, and round 1 then carries the particles only; after
+// the round-1 wait the shared rows must hold own + neighbour contribution exactly (small integers).
 __global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epochs, long long budget, int fault,
-                                unsigned long long* errors) {
+                                int commutative, unsigned long long* errors) {
   const SelfRank me = ranks[blockIdx.x];
   const int r = blockIdx.x, tid = threadIdx.x, nth = blockDim.x, P = g.pitch;
   __shared__ int s_ok;
   unsigned long long bad = 0;
   for (int e = 1; e <= epochs; ++e) {
-    // this rank's J rows and messages of epoch e (its own buffers)
-    for (int k = tid; k < 3 * 4 * P; k += nth) {
-      const int c = k / (4 * P), q = (k / P) % 4, x = k % P, row = q < 2 ? q - 1 : g.ny + q - 2;
-      me.J[c * g.plane + (long)(row + 1) * P + x] = st_row(r, e, 0, c, row, x);
+    if (commutative) {
+      for (long k = tid; k < 3 * g.plane; k += nth) me.J[k] = 0.f;
+      __threadfence_system();
+      __syncthreads();
+      if (tid == 0) {
+        if (me.has_hi) signal_flag(me.hi.flags + 4, e);
+        if (me.has_lo) signal_flag(me.lo.flags + 5, e);
+        s_ok = wait_flags(me.self.flags, me.has_lo ? 4 : -1, me.has_hi ? 5 : -1, e, budget);
+        __threadfence();
+      }
+      __syncthreads();
+      if (!s_ok) { if (tid == 0) atomicAdd(errors, 1ull << 40); return; }
+      float* Jlo = me.has_lo ? me.Jn[0] : nullptr;
+      float* Jhi = me.has_hi ? me.Jn[1] : nullptr;
+      for (int k = tid; k < 3 * 4 * P; k += nth) {
+        const int c = k / (4 * P), q = (k / P) % 4, x = k % P, row = q < 2 ? q - 1 : g.ny + q - 2;
+        const long o = (long)(row + 1) * P + x;
+        const float v = st_row(r, e, 0, c, row, x);
+        atomicAdd(me.J + c * g.plane + o, v);
+        peer_add_j(Jlo, Jhi, me.lo_plane, me.hi_plane, me.lo_ny, g, c, row, o, v);
+      }
+    } else {
+      // this rank's J rows and messages of epoch e (its own buffers)
+      for (int k = tid; k < 3 * 4 * P; k += nth) {
+        const int c = k / (4 * P), q = (k / P) % 4, x = k % P, row = q < 2 ? q - 1 : g.ny + q - 2;
+        me.J[c * g.plane + (long)(row + 1) * P + x] = st_row(r, e, 0, c, row, x);
+      }
     }
     for (int d = 0; d < 2; ++d) {
       const PList L = msg_list(me.send[d], pcap);
@@ -238,8 +269,11 @@ __global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epoch
       }
     }
     __syncthreads();
-    put1_body(me.J, g, me.send[0], me.send[1], pcap, me.lo, me.hi, me.has_lo, me.has_hi, 1, tid, nth);
-    if (fault == 1 && r == 0 && e == 2 && tid == 0 && me.has_hi) me.hi.jrdn[P + 3] += 1.0f;
+    put1_body(me.J, g, me.send[0], me.send[1], pcap, me.lo, me.hi, me.has_lo, me.has_hi, commutative ? 0 : 1, tid, nth);
+    if (fault == 1 && r == 0 && e == 2 && tid == 0 && me.has_hi) {
+      if (commutative) atomicAdd(me.Jn[1] + P + 3, 1.0f);   // (upper's row 0, column -1)
+      else me.hi.jrdn[P + 3] += 1.0f;
+    }
     __threadfence_system();
     __syncthreads();
     if (tid == 0) {
@@ -255,8 +289,16 @@ __global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epoch
     // and down-going particles
     for (int k = tid; k < 6 * P; k += nth) {
       const int c = k / (2 * P), q = (k / P) % 2, x = k % P;
-      if (me.has_lo && me.self.jrdn[(c * 2 + q) * P + x] != st_row(me.lower, e, 0, c, g.ny + q, x)) ++bad;
-      if (me.has_hi && me.self.jrup[(c * 2 + q) * P + x] != st_row(me.upper, e, 0, c, q - 1, x)) ++bad;
+      if (commutative) {   // rows 0, 1 = own + the lower's rows ny, ny + 1; rows ny - 1, ny = own + the upper's -1, 0
+        const float* Jc = me.J + c * g.plane;
+        const float lo0 = st_row(r, e, 0, c, q, x) * (q == 0 ? 1.f : 0.f);   // own deposits only on rows 0 (not 1)
+        const float hi0 = st_row(r, e, 0, c, g.ny - 1 + q, x) * (q == 1 ? 1.f : 0.f);   // own only on row ny
+        if (me.has_lo && Jc[(long)(q + 1) * P + x] != lo0 + st_row(me.lower, e, 0, c, g.ny + q, x)) ++bad;
+        if (me.has_hi && Jc[(long)(g.ny + q) * P + x] != hi0 + st_row(me.upper, e, 0, c, q - 1, x)) ++bad;
+      } else {
+        if (me.has_lo && me.self.jrdn[(c * 2 + q) * P + x] != st_row(me.lower, e, 0, c, g.ny + q, x)) ++bad;
+        if (me.has_hi && me.self.jrup[(c * 2 + q) * P + x] != st_row(me.upper, e, 0, c, q - 1, x)) ++bad;
+      }
     }
     for (int side = 0; side < 2; ++side) {   // pmsg[0] from the lower (its up messages), [1] from the upper
       if (side == 0 ? !me.has_lo : !me.has_hi) continue;
@@ -305,7 +347,8 @@ __global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epoch
 using namespace zpic;
 
 extern "C" zpic_status zpic_peer_selftest(int32_t ranks, int32_t epochs, int32_t nx, int32_t ny, int32_t pcap,
-                                          int32_t periodic, int64_t budget_cycles, int32_t fault, int64_t* errors_out) {
+                                          int32_t periodic, int32_t commutative, int64_t budget_cycles, int32_t fault,
+                                          int64_t* errors_out) {
   if (ranks < 1 || ranks > 64 || epochs < 1 || nx < 1 || ny < 4 || pcap < 32 || !errors_out) return ZPIC_E_INVALID;
   GridDesc g;
   g.nx = nx; g.ny = ny;
@@ -343,6 +386,10 @@ extern "C" zpic_status zpic_peer_selftest(int32_t ranks, int32_t epochs, int32_t
       hr[r].self = views[r];
       hr[r].lo = views[hr[r].lower];
       hr[r].hi = views[hr[r].upper];
+      hr[r].Jn[0] = hr[hr[r].lower].J;
+      hr[r].Jn[1] = hr[hr[r].upper].J;
+      hr[r].lo_plane = hr[r].hi_plane = g.plane;
+      hr[r].lo_ny = g.ny;
     }
     SelfRank* dr = (SelfRank*)dalloc(sizeof(SelfRank) * ranks);
     unsigned long long* derr = (unsigned long long*)dalloc(sizeof(unsigned long long));
@@ -350,8 +397,8 @@ extern "C" zpic_status zpic_peer_selftest(int32_t ranks, int32_t epochs, int32_t
     if (st == ZPIC_OK) {
       cudaMemcpy(dr, hr.data(), sizeof(SelfRank) * ranks, cudaMemcpyHostToDevice);
       long long budget = budget_cycles;
-      int pc = pcap, ep = epochs, fl = fault;
-      void* args[] = {&dr, &g, &pc, &ep, &budget, &fl, &derr};
+      int pc = pcap, ep = epochs, fl = fault, cm = commutative;
+      void* args[] = {&dr, &g, &pc, &ep, &budget, &fl, &cm, &derr};
       if (cudaLaunchCooperativeKernel((const void*)k_peer_selftest, dim3(ranks), dim3(256), args, 0, 0) != cudaSuccess ||
           cudaDeviceSynchronize() != cudaSuccess) {
         st = ZPIC_E_CUDA;

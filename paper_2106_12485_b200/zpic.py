@@ -92,7 +92,7 @@ _lib.zpic_counters.argtypes = [_P, _I64P, ctypes.c_int32]
 _lib.zpic_kernel_times.argtypes = [_P, ctypes.POINTER(ctypes.c_char_p), _F64P, _I32P, _I32P]
 _lib.zpic_step_group.argtypes = [ctypes.POINTER(_P), ctypes.c_int32, ctypes.c_int32]
 _lib.zpic_nccl_unique_id.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
-_lib.zpic_peer_selftest.argtypes = [ctypes.c_int32] * 6 + [ctypes.c_int64, ctypes.c_int32, _I64P]
+_lib.zpic_peer_selftest.argtypes = [ctypes.c_int32] * 7 + [ctypes.c_int64, ctypes.c_int32, _I64P]
 _lib.zpic_free.argtypes = [_P]
 _lib.zpic_free.restype = None
 _lib.zpic_last_error.argtypes = [_P]
@@ -169,11 +169,12 @@ def zpic_nccl_unique_id():
     return buf.raw
 
 
-def zpic_peer_selftest(ranks, epochs, nx, ny, pcap, periodic=True, budget_cycles=4_000_000_000, fault=0):
+def zpic_peer_selftest(ranks, epochs, nx, ny, pcap, periodic=True, commutative=False, budget_cycles=4_000_000_000,
+                       fault=0):
     """The PEER protocol self-test (include/zpic.h): returns (mismatched values, timed-out waits)."""
     err = ctypes.c_int64(0)
-    _check(_lib.zpic_peer_selftest(ranks, epochs, nx, ny, pcap, 1 if periodic else 0, budget_cycles, fault,
-                                   ctypes.byref(err)), None)
+    _check(_lib.zpic_peer_selftest(ranks, epochs, nx, ny, pcap, 1 if periodic else 0, 1 if commutative else 0,
+                                   budget_cycles, fault, ctypes.byref(err)), None)
     return err.value & ((1 << 40) - 1), err.value >> 40
 
 

@@ -304,14 +304,16 @@ def test_peer_transport_self_ring(name, current_mode):
     ref.close()
 
 
+@pytest.mark.parametrize("commutative", [False, True])
 @pytest.mark.parametrize("ranks,periodic", [(1, True), (2, True), (3, True), (8, True), (4, False), (17, True)])
-def test_peer_protocol_under_concurrency(ranks, periodic):
+def test_peer_protocol_under_concurrency(ranks, periodic, commutative):
     """The PEER halo protocol with the transport's own put / signal / wait code, every emulated
     slab a CTA of one cooperative launch (zpic_peer_selftest): 300 steps of both rounds with waits
     that really spin on flags other CTAs store concurrently (the loopback groups never spin), every
-    received value checked against what its sender wrote for that step."""
+    received value checked against what its sender wrote for that step; with the cross-slab
+    commutative current the shared J rows must hold exactly the own plus the neighbour's adds."""
     z = _z()
-    bad, timeouts = z.zpic.zpic_peer_selftest(ranks, 300, 200, 16, 256, periodic)
+    bad, timeouts = z.zpic.zpic_peer_selftest(ranks, 300, 200, 16, 256, periodic, commutative)
     assert (bad, timeouts) == (0, 0)
 
 
@@ -319,7 +321,8 @@ def test_peer_protocol_selftest_detects_faults():
     """The self-test is not vacuous: a value corrupted in flight is counted, and a signal that never
     comes ends the neighbours' waits at the cycle budget instead of hanging."""
     z = _z()
-    bad, timeouts = z.zpic.zpic_peer_selftest(4, 10, 200, 16, 256, True, fault=1)
-    assert bad >= 1 and timeouts == 0
-    bad, timeouts = z.zpic.zpic_peer_selftest(4, 10, 200, 16, 256, True, budget_cycles=200_000_000, fault=2)
-    assert timeouts >= 2
+    for cm in (False, True):
+        bad, timeouts = z.zpic.zpic_peer_selftest(4, 10, 200, 16, 256, True, cm, fault=1)
+        assert bad >= 1 and timeouts == 0
+        bad, timeouts = z.zpic.zpic_peer_selftest(4, 10, 200, 16, 256, True, cm, budget_cycles=200_000_000, fault=2)
+        assert timeouts >= 2
