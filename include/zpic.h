@@ -232,7 +232,9 @@ zpic_status zpic_nccl_unique_id(void* out, size_t out_len);
  * budget_cycles (GPU clocks).  fault: 0 none; 1 rank 0 corrupts one J value it sent at epoch 2;
  * 2 rank 0 skips its round-1 signal at epoch 2 (both must make *errors_out non-zero).  Allocates
  * and frees its own device memory.  ZPIC_E_INVALID for ranks outside [1, 64], epochs < 1, nx < 1,
- * ny < 4, pcap < 32 or a null errors_out; ZPIC_E_CUDA if allocation or the launch fails. */
+ * ny < 4, pcap outside [32, 4096] or a null errors_out; ZPIC_E_CUDA if allocation or the launch
+ * fails.  The particle records are appended into the neighbours' areas the way K3 / K1L append the
+ * slab exits (a slot from the receiver's count, any order) and checked as a set. */
 zpic_status zpic_peer_selftest(int32_t ranks, int32_t epochs, int32_t nx, int32_t ny, int32_t pcap, int32_t periodic,
                                int32_t commutative, int64_t budget_cycles, int32_t fault, int64_t* errors_out);
 

@@ -52,13 +52,10 @@ void launch_apply_j_halo(float* J, const GridDesc& g, const float* rup, const fl
 size_t particle_msg_bytes(int cap);
 PeerView peer_view(void* block, int pitch, int pcap);
 size_t peer_block_bytes(int pitch, int pcap);
-void launch_peer_put1(const float* J, const GridDesc& g, const void* send_dn, const void* send_up, int pcap,
-                      const PeerView& lo, const PeerView& up, int has_lo, int has_hi, int rows,
-                      cudaStream_t st);
+void launch_peer_put1(const float* J, const GridDesc& g, int pcap, const PeerView& lo, const PeerView& up, int has_lo,
+                      int has_hi, cudaStream_t st);
 void launch_peer_put2(const float* E, const float* B, const GridDesc& g, const PeerView& lo, const PeerView& up,
-                      int has_lo, int has_hi, cudaStream_t st);
-void launch_peer_apply2(float* E, float* B, const GridDesc& g, const PeerView& self, int has_lo, int has_hi,
-                        cudaStream_t st);
+                      int has_lo, int has_hi, int b, cudaStream_t st);
 void launch_peer_signal(unsigned long long* fa, unsigned long long* fb, unsigned long long e, cudaStream_t st);
 void launch_peer_wait(const unsigned long long* flags, int ia, int ib, unsigned long long e, int* err, cudaStream_t st);
 PList particle_msg_list(void* buf, int cap);
@@ -338,6 +335,11 @@ PushParams push_params(zpic_ctx* c) {
   if (c->slab) {
     p.send[0] = particle_msg_list(c->pmsg_send[0], c->pcap);
     p.send[1] = particle_msg_list(c->pmsg_send[1], c->pcap);
+    if (c->peer) {   // PEER: the slab exits go straight into the neighbours' receive areas (K3, K1L)
+      if (c->has_lo) p.send[0] = particle_msg_list(c->peer_lo.pmsg[1], c->pcap);
+      if (c->has_hi) p.send[1] = particle_msg_list(c->peer_hi.pmsg[0], c->pcap);
+      p.peer_send = 1;
+    }
   }
   if (c->peer_j) {   // cross-slab commutative current: the neighbours' J
     p.Jlo = c->has_lo ? c->jlo : nullptr;
@@ -484,7 +486,7 @@ static void size_lists(zpic_ctx* c, int64_t extra = 0);
 // PEER across processes: the CUDA IPC handles of every rank's receive block, all-gathered once on
 // the NCCL communicator; the y neighbours' blocks opened (peer access over NVLink).
 struct PeerRecord {
-  cudaIpcMemHandle_t block, j;   // the receive block; J (cross-slab commutative current only)
+  cudaIpcMemHandle_t block, j, eb;   // the receive block; J (cross-slab commutative current only); E/B
   int32_t ny;
   int32_t pad[15];
 };
@@ -492,6 +494,7 @@ static void open_peer_blocks(zpic_ctx* c) {
   PeerRecord mine{};
   CUDA_OR_THROW(cudaIpcGetMemHandle(&mine.block, c->peer_block));
   if (c->peer_j) CUDA_OR_THROW(cudaIpcGetMemHandle(&mine.j, c->j_block));
+  CUDA_OR_THROW(cudaIpcGetMemHandle(&mine.eb, c->eb_block));
   mine.ny = c->g.ny;
   const size_t hb = sizeof(PeerRecord);
   char* dbuf = alloc_n<char>(c, hb * (c->world + 1));
@@ -502,19 +505,28 @@ static void open_peer_blocks(zpic_ctx* c) {
   CUDA_OR_THROW(cudaMemcpyAsync(all.data(), dbuf, hb * c->world, cudaMemcpyDeviceToHost, c->stream));
   CUDA_OR_THROW(cudaStreamSynchronize(c->stream));
   dev_free(c, dbuf);
-  std::vector<void*> opened(2 * c->world, nullptr);   // each peer allocation opened once per process
-  auto open_ptr = [&](int rank, int which) -> void* {
-    if (rank == c->rank) return which ? c->j_block : c->peer_block;
-    void*& p = opened[2 * rank + which];
+  std::vector<void*> opened(3 * c->world, nullptr);   // each peer allocation opened once per process
+  auto open_ptr = [&](int rank, int which) -> void* {   // 0 receive block, 1 J, 2 E/B
+    if (rank == c->rank) return which == 2 ? c->eb_block : which ? c->j_block : c->peer_block;
+    void*& p = opened[3 * rank + which];
     if (!p) {
-      CUDA_OR_THROW(cudaIpcOpenMemHandle(&p, which ? all[rank].j : all[rank].block, cudaIpcMemLazyEnablePeerAccess));
+      const cudaIpcMemHandle_t& h = which == 2 ? all[rank].eb : which ? all[rank].j : all[rank].block;
+      CUDA_OR_THROW(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
       c->ipc_open.push_back(p);
     }
     return p;
   };
   const long row_floats = c->g.pitch;
+  auto view_of = [&](int rank) {
+    PeerView v = peer_view(open_ptr(rank, 0), c->g.pitch, c->pcap);
+    float* eb = (float*)open_ptr(rank, 2);
+    v.ny = all[rank].ny;
+    v.plane = (long)(all[rank].ny + 3) * row_floats;
+    for (int b = 0; b < 2; ++b) { v.E[b] = eb + (size_t)b * 3 * v.plane; v.B[b] = eb + (size_t)(2 + b) * 3 * v.plane; }
+    return v;
+  };
   if (c->has_lo) {
-    c->peer_lo = peer_view(open_ptr(c->lower, 0), c->g.pitch, c->pcap);
+    c->peer_lo = view_of(c->lower);
     if (c->peer_j) {
       c->jlo = (float*)open_ptr(c->lower, 1);
       c->lo_ny = all[c->lower].ny;
@@ -522,7 +534,7 @@ static void open_peer_blocks(zpic_ctx* c) {
     }
   }
   if (c->has_hi) {
-    c->peer_hi = peer_view(open_ptr(c->upper, 0), c->g.pitch, c->pcap);
+    c->peer_hi = view_of(c->upper);
     if (c->peer_j) {
       c->jhi = (float*)open_ptr(c->upper, 1);
       c->hi_plane = (long)(all[c->upper].ny + 3) * row_floats;
@@ -659,7 +671,17 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
       k.ke_scale = q * sp.m_q * grid->dx * grid->dy;
     }
     // fields
-    for (int b = 0; b < 2; ++b) { c->E[b] = alloc_n<float>(c, 3 * g.plane); c->B[b] = alloc_n<float>(c, 3 * g.plane); }
+    const bool peer_tr = c->slab && (c->transport == ZPIC_TRANSPORT_PEER || c->transport == ZPIC_TRANSPORT_LOOPBACK_PEER);
+    if (peer_tr) {   // PEER: the neighbours write their round-2 rows into these buffers (CUDA IPC export)
+      CUDA_OR_THROW(cudaMalloc(&c->eb_block, sizeof(float) * 12 * g.plane));
+      CUDA_OR_THROW(cudaMemsetAsync(c->eb_block, 0, sizeof(float) * 12 * g.plane, c->stream));
+      for (int b = 0; b < 2; ++b) {
+        c->E[b] = (float*)c->eb_block + (size_t)b * 3 * g.plane;
+        c->B[b] = (float*)c->eb_block + (size_t)(2 + b) * 3 * g.plane;
+      }
+    } else {
+      for (int b = 0; b < 2; ++b) { c->E[b] = alloc_n<float>(c, 3 * g.plane); c->B[b] = alloc_n<float>(c, 3 * g.plane); }
+    }
     for (int b = 0; b < 2; ++b) {   // TMA maps for K1's staging of a tile's fields (+1 cell halo)
       make_field_tmap(&c->tm[0][b], c->E[b], g, c->T);
       make_field_tmap(&c->tm[1][b], c->B[b], g, c->T);
@@ -814,6 +836,9 @@ zpic_status zpic_init(zpic_ctx** out, const zpic_grid* grid, double dt, const zp
         CUDA_OR_THROW(cudaMalloc(&c->peer_block, pb));
         CUDA_OR_THROW(cudaMemsetAsync(c->peer_block, 0, pb, c->stream));
         c->peer_self = peer_view(c->peer_block, g.pitch, c->pcap);
+        for (int b = 0; b < 2; ++b) { c->peer_self.E[b] = c->E[b]; c->peer_self.B[b] = c->B[b]; }
+        c->peer_self.plane = g.plane;
+        c->peer_self.ny = g.ny;
         c->peer_lo = c->peer_hi = c->peer_self;   // a one-rank ring; loopback groups bind at zpic_step_group
         c->jrup = c->peer_self.jrup;
         c->jrdn = c->peer_self.jrdn;
@@ -1231,8 +1256,10 @@ bool overlap_round1(const zpic_ctx* c) {
 // (every rank of a chain steps in lockstep, so the epochs agree).
 void peer_round1_send(zpic_ctx* c) {
   c->peer_e1 += 1;
-  launch_peer_put1(c->J, c->g, c->pmsg_send[0], c->pmsg_send[1], c->pcap, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi,
-                   c->peer_j ? 0 : 1, c->stream);
+  // the particles are already in the neighbours' areas (K3 / K1L wrote them there); the raw J rows
+  // too with the cross-slab commutative current (K1 / K1L added them): then only the signal
+  if (!c->peer_j)
+    launch_peer_put1(c->J, c->g, c->pcap, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi, c->stream);
   launch_peer_signal(c->has_hi ? c->peer_hi.flags + 0 : nullptr, c->has_lo ? c->peer_lo.flags + 1 : nullptr, c->peer_e1,
                      c->stream);
 }
@@ -1241,7 +1268,7 @@ void peer_round1_wait(zpic_ctx* c) {
 }
 void peer_round2_send(zpic_ctx* c, int b) {
   c->peer_e2 += 1;
-  launch_peer_put2(c->E[b], c->B[b], c->g, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi, c->stream);
+  launch_peer_put2(c->E[b], c->B[b], c->g, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi, b, c->stream);
   launch_peer_signal(c->has_hi ? c->peer_hi.flags + 2 : nullptr, c->has_lo ? c->peer_lo.flags + 3 : nullptr, c->peer_e2,
                      c->stream);
 }
@@ -1258,9 +1285,10 @@ void peer_zero_wait(zpic_ctx* c) {
   launch_peer_wait(c->peer_self.flags, c->has_lo ? 4 : -1, c->has_hi ? 5 : -1, c->peer_e0, c->err, c->stream);
   c->j_zeroed = false;
 }
+// (the rows are already in this slab's guard rows: waiting is all there is to receive)
 void peer_round2_recv(zpic_ctx* c, int b) {
+  (void)b;
   launch_peer_wait(c->peer_self.flags, c->has_lo ? 2 : -1, c->has_hi ? 3 : -1, c->peer_e2, c->err, c->stream);
-  launch_peer_apply2(c->E[b], c->B[b], c->g, c->peer_self, c->has_lo, c->has_hi, c->stream);
 }
 
 StepState step_phase_a(zpic_ctx* c) {
@@ -1290,7 +1318,15 @@ StepState step_phase_a(zpic_ctx* c) {
   }
   {
     ProfScope ps(c, K_PUSH);
-    if (c->r2_pending) {   // the E/B ghost rows of this step are still in flight
+    if (c->r2_pending && c->peer) {   // one grid: interior tile rows first, the slab-edge CTAs wait
+      PushParams q = p;                 // for the neighbours' rows themselves (NEXT-1 per tile row)
+      q.boundary_last = 1;
+      q.r2_flags = c->peer_self.flags;
+      q.r2_epoch = c->peer_e2;
+      launch_push_tiles(q, 0, c->ntiles, c->stream);
+      c->r2_pending = false;
+      ++s.launches;
+    } else if (c->r2_pending) {   // the E/B ghost rows of this step are still in flight
       const int tb = c->ntx, te = std::max(c->ntx, (c->nty - 1) * c->ntx);
       launch_push_tiles(p, tb, te, c->stream);
       if (c->peer) peer_round2_recv(c, c->cur);   // the neighbours' E/B rows into this buffer's guards
@@ -1367,6 +1403,8 @@ void step_phase_b(zpic_ctx* c, StepState& s) {
     launch_recv_insert(s.p, particle_msg_list(c->pmsg_recv[0], c->pcap), particle_msg_list(c->pmsg_recv[1], c->pcap),
                        c->stream);
     s.launches += 2;
+    if (c->peer)   // consumed: the senders append the next step's exits from zero (after round 2)
+      for (int d = 0; d < 2; ++d) CUDA_OR_THROW(cudaMemsetAsync(c->pmsg_recv[d], 0, 4, c->stream));
   }
   const float* Jyee = c->J;
   if (c->opt.filter_passes > 0) {
@@ -1530,7 +1568,9 @@ static void run_step_nccl(zpic_ctx* c) {
   step_phase_b(c, s);
   if (c->slab && c->peer) {   // round 2 by the peer-put kernels; received before the next boundary K1
     peer_round2_send(c, c->cur ^ 1);
-    c->r2_pending = true;
+    static const bool no_overlap = [] { const char* e = getenv("ZPIC_NO_R2_OVERLAP"); return e && atoi(e); }();
+    if (no_overlap) peer_round2_recv(c, c->cur ^ 1);
+    else c->r2_pending = true;
   } else if (c->slab) {
     ncclResult_t r;
     if (c->comm_stream) {   // round 2 on the comm stream, the next step's interior K1 meanwhile
@@ -1941,6 +1981,7 @@ void zpic_free(zpic_ctx* c) {
   for (void* p : c->ipc_open) cudaIpcCloseMemHandle(p);
   if (c->peer_block) cudaFree(c->peer_block);
   if (c->j_block) cudaFree(c->j_block);
+  if (c->eb_block) cudaFree(c->eb_block);
   for (auto e : c->prof_ev) cudaEventDestroy(e);
   for (void* p : c->allocations) {
     if (c->opt.free) c->opt.free(p, c->opt.alloc_user);

@@ -194,4 +194,28 @@ struct PeerGlobalCurrent {
   }
 };
 
+// ---- PEER transport epoch flags (zpic_peer.cu; also K1's fused round-2 wait) -------------------
+// Release-store the epoch into a receiver's flag (system scope: NVLink peers).
+__device__ __forceinline__ void signal_flag(unsigned long long* f, unsigned long long e) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
+}
+// Acquire-spin until flags[ia] (and flags[ib]) reach the epoch (-1: not waited for); false when
+// `budget` GPU clock cycles pass first.
+__device__ __forceinline__ bool wait_flags(const unsigned long long* flags, int ia, int ib, unsigned long long e,
+                                           long long budget) {
+  const long long t0 = clock64();
+  for (int q = 0; q < 2; ++q) {
+    const int i = q ? ib : ia;
+    if (i < 0) continue;
+    unsigned long long v;
+    for (;;) {
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + i) : "memory");
+      if (v >= e) break;
+      if (clock64() - t0 > budget) return false;
+      __nanosleep(256);
+    }
+  }
+  return true;
+}
+
 }  // namespace zpic

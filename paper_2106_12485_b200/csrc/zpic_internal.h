@@ -103,6 +103,8 @@ struct PushParams {
   // slab go to send[0] (down, iy += ny) or send[1] (up, iy -= ny).
   int slab, has_lo, has_hi;
   PList send[2];
+  int peer_send;        // 1: send[] are the neighbours' receive areas (PEER transport): the kernels
+                        // that append to them (K3, K1L) end with a system-scope fence
   int skip_cell_store;  // tuning switch: write the cell word only when it changed
   int commutative;      // 1: K1 adds its current block into J with global atomics (no Jt, no K4)
   int use_mail;         // 1: tile leavers go through the per-tile mailboxes (K3m), else the mover list
@@ -119,6 +121,13 @@ struct PushParams {
   int check_occ;        // 1: K1s verifies hist against a recount (ZPIC_CHECK_OCC; tests)
   float qmax;           // max_s |q_s|
   int tile0;            // K1 launches over tiles [tile0, tile0 + grid) (the slab overlap splits it)
+  // PEER round 2 fused into K1 (NEXT-1, per tile row): boundary_last = 1 runs the interior tile rows
+  // first and the slab-edge rows last in one grid; a slab-edge CTA first acquire-waits until
+  // r2_flags[2] (from the lower) / [3] (from the upper) reach r2_epoch: the neighbours' E/B rows of
+  // this step are then in this slab's guard rows (null: no wait)
+  int boundary_last;
+  const unsigned long long* r2_flags;
+  unsigned long long r2_epoch;
   // Cross-slab "commutative" current (PEER transport + current_mode 1): deposits on
   // this slab's rows -1, 0 are also added into the lower neighbour's J rows ny_lo - 1, ny_lo, those on
   // rows ny, ny + 1 into the upper neighbour's rows 0, 1 (peer pointers; null = not this mode / edge)
@@ -165,8 +174,11 @@ struct PeerView {
   float* jrup;       // [3][2][pitch] the upper neighbour's raw J rows -1, 0 (round 1)
   float* jrdn;       // [3][2][pitch] the lower neighbour's raw J rows ny, ny+1 (round 1)
   char* pmsg[2];     // particle messages from the lower [0] / upper [1] neighbour (round 1)
-  float* eb_lo;      // [E/B][3][pitch] the lower neighbour's row ny-1: this slab's guard row -1 (round 2)
-  float* eb_hi;      // [E/B][3][2][pitch] the upper neighbour's rows 0, 1: guard rows ny, ny+1 (round 2)
+  // round 2 writes straight into the owner's field buffers (their guard rows -1, ny, ny + 1):
+  float* E[2];       // the owner's E / B buffers (both parities), each [3][ny + 3][pitch]
+  float* B[2];
+  long plane;        // (ny + 3) * pitch of the owner
+  int ny;            // the owner's interior rows
   unsigned long long* flags;   // [6] epochs: round 1 from lower / upper, round 2 from lower / upper,
                                // J zeroed by the lower / upper neighbour (cross-slab commutative current)
 };
@@ -245,6 +257,7 @@ struct zpic_ctx {
   // the neighbours' J, their planes and the lower's ny; e0 counts the "J zeroed" signals
   bool peer_j = false, j_zeroed = false;
   void* j_block = nullptr;
+  void* eb_block = nullptr;   // PEER: E[0], E[1], B[0], B[1] in one cudaMalloc (exported by CUDA IPC)
   float* jlo = nullptr;
   float* jhi = nullptr;
   long lo_plane = 0, hi_plane = 0;

@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(kBlock) k_insert(PushParams p) {
       }
     }
   }
+  if (p.peer_send) __threadfence_system();   // slab exits written into a neighbour's memory
 }
 
 // =============================================================================================
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(kBlock) k_push_loose(PushParams p) {
     if (domain_bc(ix, iy, p)) insert_particle(p, s, ix, iy, x, y, ux, uy, uz, id);
   }
   for (int s = 0; s < p.nspecies; ++s) block_add_double((double)ke[s], p.ke_slots + s * kEnergySlots + (blockIdx.x & (kEnergySlots - 1)));
-  if (p.Jlo || p.Jhi) __threadfence_system();
+  if (p.Jlo || p.Jhi || p.peer_send) __threadfence_system();
 }
 
 // =============================================================================================

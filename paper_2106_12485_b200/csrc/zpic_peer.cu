@@ -2,20 +2,24 @@
 // neighbours' receive areas (ZPIC_TRANSPORT_PEER / _LOOPBACK_PEER).
 //
 // Every context owns one "peer block" (cudaMalloc'd, so it can be exported with CUDA IPC): the
-// raw J rows and the particle messages of round 1, the E/B ghost rows of round 2, and four epoch
+// raw J rows and the particle messages of round 1, the E/B ghost rows of round 2, and six epoch
 // flags.  A neighbour's block is reached through a PeerView (its own pointers in a loopback
 // group, CUDA IPC pointers across processes over NVLink, this context's own block in a one-rank
-// ring).  A round is one copy kernel (the sender's rows and messages into the receiver's area, every
-// thread ending with a system-scope fence), one signal kernel (a system-scope release store of the
-// round's epoch into the receiver's flag) and, on the receiver, one wait kernel (an acquire spin
-// until the flag reaches the epoch, bounded: a neighbour that never signals sets ERR_HALO instead
-// of hanging the GPU).  Flags in the receiver's block: [0] round 1 from its lower neighbour, [1]
+// ring).  The particles leaving the slab are appended straight into the neighbour's message area
+// by the kernels that route them (K3, K1L: a slot from the receiver's count, then the record; the
+// receiver zeroes its counts once it inserted them).  A round is then at most one copy kernel (the
+// sender's raw J rows, or E/B rows, into the receiver's area; none for round 1 with the cross-slab
+// commutative current), every writer ending with a system-scope fence, one signal kernel (a
+// system-scope release store of the round's epoch into the receiver's flag) and, on the receiver,
+// one wait kernel (an acquire spin until the flag reaches the epoch, bounded: a neighbour that
+// never signals sets ERR_HALO instead of hanging the GPU).  Flags in the receiver's block: [0] round 1 from its lower neighbour, [1]
 // round 1 from its upper one, [2] round 2 from the lower, [3] round 2 from the upper, [4] / [5] J
 // zeroed by the lower / upper neighbour (cross-slab commutative current: from then on the
 // neighbours' K1 may add into this slab's J).
-// Reuse of an area is ordered by the protocol: a sender overwrites the receiver's round-1 area only
-// after it waited for the receiver's round 2 of the previous step, which the receiver sends after it
-// consumed that area.
+// Reuse of an area is ordered by the protocol: a sender writes the receiver's round-1 area (J rows,
+// message records) only after it waited for the receiver's round 2 of the previous step, which the
+// receiver sends after it consumed that area (and zeroed its message counts); the slab exits are
+// appended by K3 / K1L, which run after that wait (the next step's boundary K1).
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -28,24 +32,27 @@ namespace zpic {
 
 // the peer block's layout (bytes), for a slab of row pitch `pitch` and message capacity pcap
 struct PeerLayout {
-  size_t jrup, jrdn, pmsg0, pmsg1, eb_lo, eb_hi, flags, bytes;
+  size_t jrup, jrdn, pmsg0, pmsg1, flags, bytes;
   PeerLayout(int pitch, int pcap) {
     const size_t rows2 = (size_t)3 * 2 * pitch * 4, mb = (msg_bytes(pcap) + 255) & ~(size_t)255;
     jrup = 0;
     jrdn = jrup + rows2;
     pmsg0 = jrdn + rows2;
     pmsg1 = pmsg0 + mb;
-    eb_lo = pmsg1 + mb;
-    eb_hi = eb_lo + (size_t)2 * 3 * pitch * 4;
-    flags = eb_hi + (size_t)2 * 3 * 2 * pitch * 4;
+    flags = pmsg1 + mb;
     bytes = flags + 6 * sizeof(unsigned long long);
   }
 };
 PeerView peer_view(void* block, int pitch, int pcap) {
   const PeerLayout L(pitch, pcap);
   char* b = (char*)block;
-  return PeerView{(float*)(b + L.jrup), (float*)(b + L.jrdn), {b + L.pmsg0, b + L.pmsg1}, (float*)(b + L.eb_lo),
-                  (float*)(b + L.eb_hi), (unsigned long long*)(b + L.flags)};
+  PeerView v{};
+  v.jrup = (float*)(b + L.jrup);
+  v.jrdn = (float*)(b + L.jrdn);
+  v.pmsg[0] = b + L.pmsg0;
+  v.pmsg[1] = b + L.pmsg1;
+  v.flags = (unsigned long long*)(b + L.flags);
+  return v;   // E, B, plane, ny: set by the owner (field buffers)
 }
 size_t peer_block_bytes(int pitch, int pcap) { return PeerLayout(pitch, pcap).bytes; }
 
@@ -53,100 +60,48 @@ __device__ __forceinline__ const float* crow(const float* F, const GridDesc& g, 
   return F + comp * g.plane + (long)(row + 1) * g.pitch;
 }
 
-// the first `count` records of a particle message (count in its header) into another message buffer
-__device__ __forceinline__ void copy_msg(const char* src, char* dst, int pcap, long tid, long nthreads) {
-  const PList S = msg_list(const_cast<char*>(src), pcap), D = msg_list(dst, pcap);
-  const int n = min(*S.count, pcap);
-  if (tid == 0) *D.count = n;
-  for (long k = tid; k < 8L * n; k += nthreads) {
-    const int f = (int)(k / n), q = (int)(k - (long)f * n);
-    const uint32_t* s = f == 0 ? (const uint32_t*)S.cell : f == 1 ? (const uint32_t*)S.x : f == 2 ? (const uint32_t*)S.y
-                      : f == 3 ? (const uint32_t*)S.ux : f == 4 ? (const uint32_t*)S.uy : f == 5 ? (const uint32_t*)S.uz
-                      : f == 6 ? (const uint32_t*)S.id : (const uint32_t*)S.species;
-    uint32_t* d = f == 0 ? (uint32_t*)D.cell : f == 1 ? (uint32_t*)D.x : f == 2 ? (uint32_t*)D.y : f == 3 ? (uint32_t*)D.ux
-                : f == 4 ? (uint32_t*)D.uy : f == 5 ? (uint32_t*)D.uz : f == 6 ? (uint32_t*)D.id : (uint32_t*)D.species;
-    d[q] = s[q];
-  }
-}
-
-// Round 1: raw J rows ny, ny+1 and the up-going particles into the upper neighbour's area, raw J
-// rows -1, 0 and the down-going particles into the lower neighbour's area (rows = 0: particles
-// only; the cross-slab commutative current already added the rows into the neighbours' J).
-// Thread tid of nth; the caller fences (system scope) before the round is signalled.
-__device__ __forceinline__ void put1_body(const float* J, const GridDesc& g, const char* send_dn, const char* send_up,
-                                          int pcap, const PeerView& lo, const PeerView& up, int has_lo, int has_hi,
-                                          int rows, long tid, long nth) {
+// Round 1: raw J rows ny, ny+1 into the upper neighbour's area, raw J rows -1, 0 into the lower
+// neighbour's.  The particles leaving the slab need no copy: K3 and K1L append them straight into
+// the neighbours' message areas (PushParams.send, peer_send).  With the cross-slab commutative
+// current there is nothing to put (K1 / K1L added the rows into the neighbours' J).  Thread tid of
+// nth; the caller fences (system scope) before the round is signalled.
+__device__ __forceinline__ void put1_body(const float* J, const GridDesc& g, const PeerView& lo, const PeerView& up,
+                                          int has_lo, int has_hi, long tid, long nth) {
   const int P = g.pitch;
-  for (long k = tid; k < (rows ? 6L * P : 0L); k += nth) {
+  for (long k = tid; k < 6L * P; k += nth) {
     const int c = (int)(k / (2 * P)), r = (int)((k / P) % 2), x = (int)(k % P);
     if (has_hi) up.jrdn[(c * 2 + r) * P + x] = crow(J, g, c, g.ny + r)[x];
     if (has_lo) lo.jrup[(c * 2 + r) * P + x] = crow(J, g, c, r - 1)[x];
   }
-  if (has_hi) copy_msg(send_up, up.pmsg[0], pcap, tid, nth);
-  if (has_lo) copy_msg(send_dn, lo.pmsg[1], pcap, tid, nth);
 }
-__global__ void k_peer_put1(const float* J, GridDesc g, const char* send_dn, const char* send_up, int pcap,
-                            PeerView lo, PeerView up, int has_lo, int has_hi, int rows) {
-  put1_body(J, g, send_dn, send_up, pcap, lo, up, has_lo, has_hi, rows, (long)blockIdx.x * blockDim.x + threadIdx.x,
-            (long)gridDim.x * blockDim.x);
+__global__ void k_peer_put1(const float* J, GridDesc g, PeerView lo, PeerView up, int has_lo, int has_hi) {
+  put1_body(J, g, lo, up, has_lo, has_hi, (long)blockIdx.x * blockDim.x + threadIdx.x, (long)gridDim.x * blockDim.x);
   __threadfence_system();
 }
 
-// Round 2: E/B row ny-1 into the upper neighbour's guard-row area, rows 0, 1 into the lower's.
+// Round 2: E/B row ny-1 (buffer b) into the upper neighbour's guard row -1, rows 0, 1 into the
+// lower neighbour's guard rows ny, ny + 1 — straight into their field buffers of the same parity
+// (no receive area, no apply pass: the slab-edge CTAs of the next K1 wait for the flag and read
+// them with their TMA field boxes).
 __device__ __forceinline__ void put2_body(const float* E, const float* B, const GridDesc& g, const PeerView& lo,
-                                          const PeerView& up, int has_lo, int has_hi, long tid, long nth) {
+                                          const PeerView& up, int has_lo, int has_hi, int b, long tid, long nth) {
   const int P = g.pitch;
   for (long k = tid; k < 6L * P; k += nth) {   // (field, comp) pairs x pitch
     const int fc = (int)(k / P), x = (int)(k % P), f = fc / 3, c = fc % 3;
     const float* F = f ? B : E;
-    if (has_hi) up.eb_lo[fc * P + x] = crow(F, g, c, g.ny - 1)[x];
+    if (has_hi) (f ? up.B[b] : up.E[b])[c * up.plane + x] = crow(F, g, c, g.ny - 1)[x];
     if (has_lo) {
-      lo.eb_hi[(fc * 2 + 0) * P + x] = crow(F, g, c, 0)[x];
-      lo.eb_hi[(fc * 2 + 1) * P + x] = crow(F, g, c, 1)[x];
+      float* D = (f ? lo.B[b] : lo.E[b]) + c * lo.plane + (long)(lo.ny + 1) * P + x;
+      D[0] = crow(F, g, c, 0)[x];
+      D[P] = crow(F, g, c, 1)[x];
     }
   }
 }
-__global__ void k_peer_put2(const float* E, const float* B, GridDesc g, PeerView lo, PeerView up, int has_lo, int has_hi) {
-  put2_body(E, B, g, lo, up, has_lo, has_hi, (long)blockIdx.x * blockDim.x + threadIdx.x, (long)gridDim.x * blockDim.x);
+__global__ void k_peer_put2(const float* E, const float* B, GridDesc g, PeerView lo, PeerView up, int has_lo, int has_hi,
+                            int b) {
+  put2_body(E, B, g, lo, up, has_lo, has_hi, b, (long)blockIdx.x * blockDim.x + threadIdx.x,
+            (long)gridDim.x * blockDim.x);
   __threadfence_system();
-}
-
-// The receiver's guard rows from its round-2 area.
-__global__ void k_peer_apply2(float* E, float* B, GridDesc g, const float* eb_lo, const float* eb_hi, int has_lo,
-                              int has_hi) {
-  const int P = g.pitch;
-  for (long k = (long)blockIdx.x * blockDim.x + threadIdx.x; k < 6L * P; k += (long)gridDim.x * blockDim.x) {
-    const int fc = (int)(k / P), x = (int)(k % P), f = fc / 3, c = fc % 3;
-    float* F = f ? B : E;
-    if (has_lo) F[c * g.plane + (long)(-1 + 1) * P + x] = eb_lo[fc * P + x];
-    if (has_hi) {
-      F[c * g.plane + (long)(g.ny + 1) * P + x] = eb_hi[(fc * 2 + 0) * P + x];
-      F[c * g.plane + (long)(g.ny + 2) * P + x] = eb_hi[(fc * 2 + 1) * P + x];
-    }
-  }
-}
-
-// Release-store the epoch into a receiver's flag (system scope: NVLink peers).
-__device__ __forceinline__ void signal_flag(unsigned long long* f, unsigned long long e) {
-  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f), "l"(e) : "memory");
-}
-// Acquire-spin until flags[ia] (and flags[ib]) reach the epoch (-1: not waited for); false when
-// `budget` GPU clock cycles pass first.
-__device__ __forceinline__ bool wait_flags(const unsigned long long* flags, int ia, int ib, unsigned long long e,
-                                           long long budget) {
-  const long long t0 = clock64();
-  for (int q = 0; q < 2; ++q) {
-    const int i = q ? ib : ia;
-    if (i < 0) continue;
-    unsigned long long v;
-    for (;;) {
-      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + i) : "memory");
-      if (v >= e) break;
-      if (clock64() - t0 > budget) return false;
-      __nanosleep(256);
-    }
-  }
-  return true;
 }
 
 // One thread: release-store the epoch into up to two receivers' flags.
@@ -163,18 +118,14 @@ __global__ void k_peer_wait(const unsigned long long* flags, int ia, int ib, uns
   if (!wait_flags(flags, ia, ib, e, 40000000000LL)) atomicOr(err, ERR_HALO);
 }
 
-void launch_peer_put1(const float* J, const GridDesc& g, const void* send_dn, const void* send_up, int pcap,
-                      const PeerView& lo, const PeerView& up, int has_lo, int has_hi, int rows, cudaStream_t st) {
-  k_peer_put1<<<148, 256, 0, st>>>(J, g, (const char*)send_dn, (const char*)send_up, pcap, lo, up, has_lo, has_hi,
-                                   rows);
+void launch_peer_put1(const float* J, const GridDesc& g, int pcap, const PeerView& lo, const PeerView& up, int has_lo,
+                      int has_hi, cudaStream_t st) {
+  (void)pcap;
+  k_peer_put1<<<48, 256, 0, st>>>(J, g, lo, up, has_lo, has_hi);
 }
 void launch_peer_put2(const float* E, const float* B, const GridDesc& g, const PeerView& lo, const PeerView& up,
-                      int has_lo, int has_hi, cudaStream_t st) {
-  k_peer_put2<<<148, 256, 0, st>>>(E, B, g, lo, up, has_lo, has_hi);
-}
-void launch_peer_apply2(float* E, float* B, const GridDesc& g, const PeerView& self, int has_lo, int has_hi,
-                        cudaStream_t st) {
-  k_peer_apply2<<<148, 256, 0, st>>>(E, B, g, self.eb_lo, self.eb_hi, has_lo, has_hi);
+                      int has_lo, int has_hi, int b, cudaStream_t st) {
+  k_peer_put2<<<48, 256, 0, st>>>(E, B, g, lo, up, has_lo, has_hi, b);
 }
 void launch_peer_signal(unsigned long long* fa, unsigned long long* fb, unsigned long long e, cudaStream_t st) {
   k_peer_signal<<<1, 1, 0, st>>>(fa, fb, e);
@@ -196,7 +147,6 @@ struct SelfRank {
   float* J;
   float* E;
   float* B;
-  char* send[2];
   PeerView self, lo, hi;
   int has_lo, has_hi, lower, upper;
   float* Jn[2];              // the lower / upper neighbour's J (commutative mode)
@@ -228,6 +178,7 @@ __global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epoch
   const SelfRank me = ranks[blockIdx.x];
   const int r = blockIdx.x, tid = threadIdx.x, nth = blockDim.x, P = g.pitch;
   __shared__ int s_ok;
+  __shared__ unsigned s_seen[4096 / 32];   // records received this epoch (pcap <= 4096)
   unsigned long long bad = 0;
   for (int e = 1; e <= epochs; ++e) {
     if (commutative) {
@@ -258,18 +209,20 @@ __global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epoch
         me.J[c * g.plane + (long)(row + 1) * P + x] = st_row(r, e, 0, c, row, x);
       }
     }
+    // this epoch's slab exits, appended straight into the neighbours' message areas as K3 / K1L do
+    // (list_append: a slot from the receiver's count, then the record); record k carries id = k
     for (int d = 0; d < 2; ++d) {
-      const PList L = msg_list(me.send[d], pcap);
+      if (d == 0 ? !me.has_lo : !me.has_hi) continue;
+      const PList L = msg_list(d == 0 ? me.lo.pmsg[1] : me.hi.pmsg[0], pcap);
       const int n = st_count(r, e, d, pcap);
-      if (tid == 0) *L.count = n;
       for (int k = tid; k < n; k += nth) {
         const uint32_t h = st_hash(r, e, 100 + d, k);
-        L.cell[k] = (int)h; L.x[k] = st_val(h ^ 1); L.y[k] = st_val(h ^ 2); L.ux[k] = st_val(h ^ 3);
-        L.uy[k] = st_val(h ^ 4); L.uz[k] = st_val(h ^ 5); L.id[k] = h ^ 6; L.species[k] = (int)(h & 3);
+        list_append(L, reinterpret_cast<int*>(errors), (int)h, st_val(h ^ 1), st_val(h ^ 2), st_val(h ^ 3),
+                    st_val(h ^ 4), st_val(h ^ 5), (uint32_t)k, (int)(h & 3));
       }
     }
     __syncthreads();
-    put1_body(me.J, g, me.send[0], me.send[1], pcap, me.lo, me.hi, me.has_lo, me.has_hi, commutative ? 0 : 1, tid, nth);
+    if (!commutative) put1_body(me.J, g, me.lo, me.hi, me.has_lo, me.has_hi, tid, nth);
     if (fault == 1 && r == 0 && e == 2 && tid == 0 && me.has_hi) {
       if (commutative) atomicAdd(me.Jn[1] + P + 3, 1.0f);   // (upper's row 0, column -1)
       else me.hi.jrdn[P + 3] += 1.0f;
@@ -305,13 +258,19 @@ __global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epoch
       const int from = side == 0 ? me.lower : me.upper, d = side == 0 ? 1 : 0;
       const PList L = msg_list(me.self.pmsg[side], pcap);
       const int n = st_count(from, e, d, pcap);
+      for (int k = tid; k < 4096 / 32; k += nth) s_seen[k] = 0u;
+      __syncthreads();
       if (tid == 0 && *L.count != n) ++bad;
-      for (int k = tid; k < n; k += nth) {
+      for (int q = tid; q < min(*L.count, pcap); q += nth) {   // any order; every record k < n exactly once
+        const uint32_t k = L.id[q];
         const uint32_t h = st_hash(from, e, 100 + d, k);
-        if (L.cell[k] != (int)h || L.x[k] != st_val(h ^ 1) || L.y[k] != st_val(h ^ 2) || L.ux[k] != st_val(h ^ 3) ||
-            L.uy[k] != st_val(h ^ 4) || L.uz[k] != st_val(h ^ 5) || L.id[k] != (h ^ 6) || L.species[k] != (int)(h & 3))
+        if (k >= (uint32_t)n || L.cell[q] != (int)h || L.x[q] != st_val(h ^ 1) || L.y[q] != st_val(h ^ 2) ||
+            L.ux[q] != st_val(h ^ 3) || L.uy[q] != st_val(h ^ 4) || L.uz[q] != st_val(h ^ 5) ||
+            L.species[q] != (int)(h & 3) || (atomicOr(&s_seen[k >> 5], 1u << (k & 31)) >> (k & 31)) & 1u)
           ++bad;
       }
+      __syncthreads();
+      if (tid == 0) *L.count = 0;   // consumed (as after k_recv_insert): the sender appends from zero
     }
     // round 2: this rank's E / B rows 0, 1, ny - 1 of epoch e
     for (int k = tid; k < 2 * 3 * 3 * P; k += nth) {
@@ -319,7 +278,7 @@ __global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epoch
       (f ? me.B : me.E)[c * g.plane + (long)(row + 1) * P + x] = st_row(r, e, 1 + f, c, row, x);
     }
     __syncthreads();
-    put2_body(me.E, me.B, g, me.lo, me.hi, me.has_lo, me.has_hi, tid, nth);
+    put2_body(me.E, me.B, g, me.lo, me.hi, me.has_lo, me.has_hi, 0, tid, nth);
     __threadfence_system();
     __syncthreads();
     if (tid == 0) {
@@ -332,9 +291,10 @@ __global__ void k_peer_selftest(SelfRank* ranks, GridDesc g, int pcap, int epoch
     if (!s_ok) { if (tid == 0) atomicAdd(errors, 1ull << 40); return; }
     for (int k = tid; k < 6 * P; k += nth) {   // (field, comp) x pitch
       const int fc = k / P, x = k % P, f = fc / 3, c = fc % 3;
-      if (me.has_lo && me.self.eb_lo[fc * P + x] != st_row(me.lower, e, 1 + f, c, g.ny - 1, x)) ++bad;
-      if (me.has_hi && (me.self.eb_hi[(fc * 2) * P + x] != st_row(me.upper, e, 1 + f, c, 0, x) ||
-                        me.self.eb_hi[(fc * 2 + 1) * P + x] != st_row(me.upper, e, 1 + f, c, 1, x)))
+      const float* F = (f ? me.B : me.E) + c * g.plane;   // this rank's guard rows -1, ny, ny + 1
+      if (me.has_lo && F[x] != st_row(me.lower, e, 1 + f, c, g.ny - 1, x)) ++bad;
+      if (me.has_hi && (F[(long)(g.ny + 1) * P + x] != st_row(me.upper, e, 1 + f, c, 0, x) ||
+                        F[(long)(g.ny + 2) * P + x] != st_row(me.upper, e, 1 + f, c, 1, x)))
         ++bad;
     }
     __syncthreads();   // every thread verified this epoch's areas before the next epoch's round 1
@@ -349,7 +309,8 @@ using namespace zpic;
 extern "C" zpic_status zpic_peer_selftest(int32_t ranks, int32_t epochs, int32_t nx, int32_t ny, int32_t pcap,
                                           int32_t periodic, int32_t commutative, int64_t budget_cycles, int32_t fault,
                                           int64_t* errors_out) {
-  if (ranks < 1 || ranks > 64 || epochs < 1 || nx < 1 || ny < 4 || pcap < 32 || !errors_out) return ZPIC_E_INVALID;
+  if (ranks < 1 || ranks > 64 || epochs < 1 || nx < 1 || ny < 4 || pcap < 32 || pcap > 4096 || !errors_out)
+    return ZPIC_E_INVALID;
   GridDesc g;
   g.nx = nx; g.ny = ny;
   g.pitch = (nx + kXOff + 2 + 31) / 32 * 32;
@@ -371,11 +332,13 @@ extern "C" zpic_status zpic_peer_selftest(int32_t ranks, int32_t epochs, int32_t
     float* J = (float*)dalloc(3 * g.plane * sizeof(float));
     float* E = (float*)dalloc(3 * g.plane * sizeof(float));
     float* B = (float*)dalloc(3 * g.plane * sizeof(float));
-    char* s0 = (char*)dalloc(msg_bytes(pcap));
-    char* s1 = (char*)dalloc(msg_bytes(pcap));
-    if (!blk || !J || !E || !B || !s0 || !s1) { st = ZPIC_E_CUDA; break; }
+    if (!blk || !J || !E || !B) { st = ZPIC_E_CUDA; break; }
     views[r] = peer_view(blk, g.pitch, pcap);
-    hr[r].J = J; hr[r].E = E; hr[r].B = B; hr[r].send[0] = s0; hr[r].send[1] = s1;
+    views[r].E[0] = views[r].E[1] = E;
+    views[r].B[0] = views[r].B[1] = B;
+    views[r].plane = g.plane;
+    views[r].ny = g.ny;
+    hr[r].J = J; hr[r].E = E; hr[r].B = B;
   }
   if (st == ZPIC_OK) {
     for (int r = 0; r < ranks; ++r) {

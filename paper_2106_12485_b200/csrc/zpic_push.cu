@@ -124,7 +124,15 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   __shared__ int s_occ;            // the tile current's scale exponent S
   if (threadIdx.x < kMaxSpecies) s_ke[threadIdx.x] = 0.0;
 
-  const int t = blockIdx.x + p.tile0;
+  // tile of this CTA; with boundary_last the interior tile rows come first, the slab-edge rows last
+#ifndef ZPIC_AB_NO_FUSED_R2
+  const int t = p.boundary_last ? [&] {
+    const int nint = p.nty > 2 ? (p.nty - 2) * p.ntx : 0, b = (int)blockIdx.x;
+    return b < nint ? p.ntx + b : (b - nint < p.ntx ? b - nint : (p.nty - 1) * p.ntx + (b - nint - p.ntx));
+  }() : (int)blockIdx.x + p.tile0;
+#else
+  const int t = (int)blockIdx.x + p.tile0;
+#endif
   const int tx = t % p.ntx, ty = t / p.ntx;
   const int i0 = tx * T, j0 = ty * T;
   const int tw = min(T, p.g.nx - i0), th = min(T, p.g.ny - j0);
@@ -141,6 +149,16 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
     const float* landB = reinterpret_cast<const float*>(smem_raw + L::BOFF);
     const unsigned bar = smem_u32(&s_bar);
     if (threadIdx.x == 0) {
+      // PEER round 2 fused (boundary_last): a slab-edge tile waits for its neighbour's E/B rows in
+      // its guard rows (acquire), then orders them before its TMA (async proxy) reads
+#ifndef ZPIC_AB_NO_FUSED_R2
+      if (p.r2_flags) {
+        const int ia = (ty == 0 && p.has_lo) ? 2 : -1, ib = (ty == p.nty - 1 && p.has_hi) ? 3 : -1;
+        if ((ia >= 0 || ib >= 0) && !wait_flags(p.r2_flags, ia, ib, p.r2_epoch, 40000000000LL))
+          atomicOr(p.err, ERR_HALO);
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+      }
+#endif
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(2 * L::BOX) : "memory");
