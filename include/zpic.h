@@ -164,8 +164,9 @@ typedef struct {
  *     the context's own buffers;
  *   ZPIC_TRANSPORT_LOOPBACK_PEER: the PEER kernels in a loopback group (zpic_step_group; every
  *     signal is enqueued before the wait that reads it, so no kernel ever waits on another).
- * PEER with current_mode = 1 allocates J with cudaMalloc (exported by CUDA IPC like the receive
- * block), independent of zpic_options.alloc.
+ * The PEER transports allocate the receive block and the E / B field buffers (and, with
+ * current_mode = 1, J) with cudaMalloc, independent of zpic_options.alloc: the neighbours write
+ * into them (CUDA IPC across processes).
  * Pass NULL for the unsplit single-GPU domain. */
 typedef enum { ZPIC_TRANSPORT_NCCL = 0, ZPIC_TRANSPORT_LOOPBACK = 1, ZPIC_TRANSPORT_PEER = 2,
                ZPIC_TRANSPORT_LOOPBACK_PEER = 3 } zpic_transport;
