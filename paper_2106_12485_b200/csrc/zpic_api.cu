@@ -1332,9 +1332,10 @@ StepState step_phase_a(zpic_ctx* c) {
       if (c->peer) peer_round2_recv(c, c->cur);   // the neighbours' E/B rows into this buffer's guards
       else CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
       c->r2_pending = false;
-      launch_push_tiles(p, 0, std::min(tb, c->ntiles), c->stream);
-      launch_push_tiles(p, std::max(te, tb), c->ntiles, c->stream);
-      s.launches += 3;
+      PushParams q = p;   // both slab-edge tile rows in one grid (one wave tail instead of two)
+      q.boundary_last = 2;
+      launch_push_tiles(q, 0, c->nty >= 2 ? 2 * c->ntx : c->ntx, c->stream);
+      s.launches += 2;
     } else {
       launch_push_tiles(p, 0, c->ntiles, c->stream);
       ++s.launches;

@@ -122,7 +122,8 @@ struct PushParams {
   float qmax;           // max_s |q_s|
   int tile0;            // K1 launches over tiles [tile0, tile0 + grid) (the slab overlap splits it)
   // PEER round 2 fused into K1 (NEXT-1, per tile row): boundary_last = 1 runs the interior tile rows
-  // first and the slab-edge rows last in one grid; a slab-edge CTA first acquire-waits until
+  // first and the slab-edge rows last in one grid (2: the slab-edge rows only, in one grid: the
+  // NCCL path after its round-2 event); a slab-edge CTA first acquire-waits until
   // r2_flags[2] (from the lower) / [3] (from the upper) reach r2_epoch: the neighbours' E/B rows of
   // this step are then in this slab's guard rows (null: no wait)
   int boundary_last;

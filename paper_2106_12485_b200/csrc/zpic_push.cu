@@ -124,10 +124,11 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   __shared__ int s_occ;            // the tile current's scale exponent S
   if (threadIdx.x < kMaxSpecies) s_ke[threadIdx.x] = 0.0;
 
-  // tile of this CTA; with boundary_last the interior tile rows come first, the slab-edge rows last
+  // tile of this CTA; with boundary_last = 1 the interior tile rows come first, the slab-edge rows
+  // last; 2: the slab-edge rows only (row 0, then row nty - 1)
 #ifndef ZPIC_AB_NO_FUSED_R2
   const int t = p.boundary_last ? [&] {
-    const int nint = p.nty > 2 ? (p.nty - 2) * p.ntx : 0, b = (int)blockIdx.x;
+    const int nint = (p.boundary_last == 1 && p.nty > 2) ? (p.nty - 2) * p.ntx : 0, b = (int)blockIdx.x;
     return b < nint ? p.ntx + b : (b - nint < p.ntx ? b - nint : (p.nty - 1) * p.ntx + (b - nint - p.ntx));
   }() : (int)blockIdx.x + p.tile0;
 #else
