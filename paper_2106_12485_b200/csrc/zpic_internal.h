@@ -17,8 +17,17 @@ constexpr int kXOff = 4;          // interior column 0 sits at column 4 of a pad
 constexpr int kEnergySlots = 256; // fp64 partial-sum slots (spread the atomics), per quantity
 constexpr int kBlock = 256;       // threads per CTA of the particle kernels
 constexpr int kSMin = 22;         // smallest tile scale exponent of the one-word int32 current
-constexpr int kYeeTX = 32;        // K5 tile: columns
-constexpr int kYeeTY = 32;        // K5 tile: rows
+// K5 tile: 128 x 8 (same-box sweep at C5, profiles/r2_ab_yee_tiles.log: 0.70 ms vs 0.72 for 64 x 16,
+// 0.79 for 32 x 32 and 128 x 4, 0.87 for 128 x 16: wide rows make long TMA rows and coalesced
+// stores; 8 rows keep 4 CTAs / SM in 48 KB of staged boxes)
+#ifndef ZPIC_YEE_TX
+#define ZPIC_YEE_TX 128
+#endif
+#ifndef ZPIC_YEE_TY
+#define ZPIC_YEE_TY 8
+#endif
+constexpr int kYeeTX = ZPIC_YEE_TX;   // K5 tile: columns
+constexpr int kYeeTY = ZPIC_YEE_TY;   // K5 tile: rows
 
 // A guard-extended field grid: 3 planes of `rows` x `pitch` floats; interior cell (i, j) of a
 // plane is at (j + 1) * pitch + (i + kXOff), valid for -1 <= i <= nx + 1, -1 <= j <= ny + 1

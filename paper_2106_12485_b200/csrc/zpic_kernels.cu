@@ -6,7 +6,7 @@
 //   K4 k_assemble_j   per-tile current blocks -> guard-extended J grid (plain stores, no atomics)
 //   K1L k_push_loose  the loose list: same physics, global-memory fields / current
 //   K4b k_guard_x/y   ghost-current reduction and guard refresh
-//   K5 k_yee          fused B half step, E step, B half step on a 32x32 tile
+//   K5 k_yee          fused B half step, E step, B half step on a 128x8 tile
 //   K0 k_inject       counter-based lattice injection; k_ramp_rows, k_laser:
 //                     the C4 density ramp (R16) and laser fields (R17) at zpic_init
 //   k_inject_column   moving-window injection (R15); k_filter_x the compensated filter (R12)
@@ -472,7 +472,7 @@ __global__ void k_guard_y(float* F, GridDesc g, int mode, int keep_mask) {
 }
 
 // =============================================================================================
-// K5: Yee advance (R2) on a 32 x 32 output tile.  E^n is staged on local
+// K5: Yee advance (R2) on a kYeeTX x kYeeTY (128 x 8) output tile.  E^n is staged on local
 // [-1, T+2), B^n on [-1, T+1), J on [0, T+1).  B^{n+1/2} is computed on [-1, T], E^{n+1} on
 // [0, T] (the row/column T redundantly, so no second exchange is needed), B^{n+1} on [0, T).
 // Outputs go to the other buffer (E1, B1), interior plus periodic guard images, so no tile
