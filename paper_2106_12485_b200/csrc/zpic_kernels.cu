@@ -186,7 +186,10 @@ __global__ void __launch_bounds__(kBlock, K3M_MINB) k_mail_gather(PushParams p) 
 // K4b folds them ("the reduction is only required for ghost cells").
 // Each thread assembles K4R nodes of one column (rows j, j + 1, ...): all their block loads are
 // issued before the sums (more bytes in flight per thread; K4 is latency-bound otherwise).
-constexpr int K4R = 4;
+#ifndef ZPIC_K4R   // rows per thread (tools/gpu/k4_ab.sh)
+#define ZPIC_K4R 4
+#endif
+constexpr int K4R = ZPIC_K4R;
 template <int T>
 __global__ void __launch_bounds__(kBlock) k_assemble_j(float* __restrict__ J, const float* __restrict__ Jt, GridDesc g,
                                                        int ntx, int nty) {
