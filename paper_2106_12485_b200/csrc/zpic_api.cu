@@ -1266,6 +1266,17 @@ void peer_round1_send(zpic_ctx* c) {
 void peer_round1_wait(zpic_ctx* c) {
   launch_peer_wait(c->peer_self.flags, c->has_lo ? 0 : -1, c->has_hi ? 1 : -1, c->peer_e1, c->err, c->stream);
 }
+// PEER: the per-step round 2 is written by K5's slab-edge tiles (ZPIC_PEER_PUT2=1: by the separate
+// put kernel, for A/B); only the signal follows K5.
+static bool peer_fused_r2() {
+  static const bool put = [] { const char* e = getenv("ZPIC_PEER_PUT2"); return e && atoi(e); }();
+  return !put;
+}
+void peer_round2_signal(zpic_ctx* c) {
+  c->peer_e2 += 1;
+  launch_peer_signal(c->has_hi ? c->peer_hi.flags + 2 : nullptr, c->has_lo ? c->peer_lo.flags + 3 : nullptr, c->peer_e2,
+                     c->stream);
+}
 void peer_round2_send(zpic_ctx* c, int b) {
   c->peer_e2 += 1;
   launch_peer_put2(c->E[b], c->B[b], c->g, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi, b, c->stream);
@@ -1381,6 +1392,17 @@ void step_phase_b(zpic_ctx* c, StepState& s) {
   y.yhi_edge = !c->slab || !c->has_hi;
   y.fe_slots = c->fe_slots;
   y.fe_scale = 0.5 * c->dx * c->dy;
+  if (c->slab && c->peer && peer_fused_r2()) {   // round 2 written by the slab-edge Yee tiles
+    const int b = c->cur ^ 1;
+    if (c->has_lo) {
+      y.peer_lo_E = c->peer_lo.E[b]; y.peer_lo_B = c->peer_lo.B[b];
+      y.peer_lo_plane = c->peer_lo.plane; y.peer_lo_ny = c->peer_lo.ny;
+    }
+    if (c->has_hi) {
+      y.peer_hi_E = c->peer_hi.E[b]; y.peer_hi_B = c->peer_hi.B[b];
+      y.peer_hi_plane = c->peer_hi.plane;
+    }
+  }
   int yee_done_to = 0;   // tile rows [1, yee_done_to) already advanced (round 1 overlap)
   if (s.r1_async) {
     const int hi = (c->g.ny - 2) / kYeeTY;   // tile rows r < hi: J rows [TY r, TY r + TY] avoid ny - 1, ny
@@ -1567,8 +1589,9 @@ static void run_step_nccl(zpic_ctx* c) {
     if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL round 1: ") + ncclGetErrorString(r)};
   }
   step_phase_b(c, s);
-  if (c->slab && c->peer) {   // round 2 by the peer-put kernels; received before the next boundary K1
-    peer_round2_send(c, c->cur ^ 1);
+  if (c->slab && c->peer) {   // round 2 (K5 wrote the rows, or the put kernel); received in the next K1
+    if (peer_fused_r2()) peer_round2_signal(c);
+    else peer_round2_send(c, c->cur ^ 1);
     static const bool no_overlap = [] { const char* e = getenv("ZPIC_NO_R2_OVERLAP"); return e && atoi(e); }();
     if (no_overlap) peer_round2_recv(c, c->cur ^ 1);
     else c->r2_pending = true;
@@ -1752,7 +1775,10 @@ zpic_status zpic_step_group(zpic_ctx** cs, int32_t count, int32_t n) {
       else loop_exchange_round1(cs, count);
       for (int r = 0; r < count; ++r) step_phase_b(cs[r], st[r]);
       if (peer) {
-        for (int r = 0; r < count; ++r) peer_round2_send(cs[r], cs[r]->cur ^ 1);
+        for (int r = 0; r < count; ++r) {
+          if (peer_fused_r2()) peer_round2_signal(cs[r]);
+          else peer_round2_send(cs[r], cs[r]->cur ^ 1);
+        }
         for (int r = 0; r < count; ++r) peer_round2_recv(cs[r], cs[r]->cur ^ 1);
       } else {
         loop_exchange_round2(cs, count, cs[0]->cur ^ 1);

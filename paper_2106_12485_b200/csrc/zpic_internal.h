@@ -162,7 +162,17 @@ struct YeeParams {
   int ylo_edge, yhi_edge;           // the slab's low / high y boundary is a domain edge
   double* fe_slots;
   double fe_scale;  // dx dy / 2
-  int row0;         // first 32-row tile row of this launch (the slab overlap splits the grid)
+  int row0;         // first tile row of this launch (the slab overlap splits the grid)
+  // PEER round 2 fused into K5: the slab-edge tiles also write their output rows 0, 1 into the lower
+  // neighbour's guard rows ny_lo, ny_lo + 1 and row ny - 1 into the upper neighbour's guard row -1
+  // of the buffers of the same parity (null: not this mode / no neighbour)
+  float* peer_lo_E;
+  float* peer_lo_B;
+  long peer_lo_plane;
+  int peer_lo_ny;
+  float* peer_hi_E;
+  float* peer_hi_B;
+  long peer_hi_plane;
 };
 
 struct InjectParams {

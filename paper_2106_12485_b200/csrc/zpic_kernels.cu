@@ -745,6 +745,36 @@ __global__ void __launch_bounds__(kBlock) k_yee(const __grid_constant__ YeeParam
 #undef EI
 #undef BI
 #undef JI
+  // PEER round 2 (fused): the rows a slab-edge tile just stored, also into the neighbours' guard
+  // rows, for the columns this CTA wrote (its output columns and the x guard columns it owns: the
+  // periodic images of columns 0, 1 (first tile) and nx - 1 (last tile), the Mur node column nx of
+  // an open x edge (last tile); the other guard columns are never written, zero on both sides)
+  const bool lo_rows = p.peer_lo_E && j0 == 0, hi_rows = p.peer_hi_E && j0 + th == g.ny;
+  if (lo_rows || hi_rows) {
+    __syncthreads();   // this CTA's stores of the rows are visible to the whole CTA
+    const bool xlo = i0 == 0, xhi = i0 + tw == g.nx, per = p.bcx == ZPIC_BC_PERIODIC;
+    const int c0 = max(0, i0 - p.shift), c1 = xhi ? g.nx : i0 + tw - p.shift;
+    const int nmain = c1 - c0;
+    const int nguard = per ? (xlo ? 2 : 0) + (xhi ? 1 : 0) : (xhi && p.bcx == ZPIC_BC_OPEN ? 1 : 0);
+    const int ncol = nmain + nguard;
+    const int nrow = (lo_rows ? 2 : 0) + (hi_rows ? 1 : 0);
+    const long P = g.pitch;
+    for (int k = threadIdx.x; k < nrow * 6 * ncol; k += kBlock) {
+      const int q = k % ncol, fc = (k / ncol) % 6, rr = k / (6 * ncol);
+      int col;
+      if (q < nmain) col = c0 + q;
+      else if (per) col = (xlo && q - nmain < 2) ? g.nx + (q - nmain) : -1;
+      else col = g.nx;
+      const int f = fc / 3, c = fc % 3;
+      const int row = (lo_rows && rr < 2) ? rr : g.ny - 1;
+      const float v = (f ? p.B1 : p.E1)[c * pl + g.at(col, row)];
+      if (lo_rows && rr < 2)
+        (f ? p.peer_lo_B : p.peer_lo_E)[c * p.peer_lo_plane + (long)(p.peer_lo_ny + 1 + rr) * P + col + kXOff] = v;
+      else
+        (f ? p.peer_hi_B : p.peer_hi_E)[c * p.peer_hi_plane + col + kXOff] = v;
+    }
+    __threadfence_system();   // before the round's signal (the kernel after this one)
+  }
   block_add_double((double)fe * p.fe_scale,
                    p.fe_slots + (((blockIdx.y + p.row0) * gridDim.x + blockIdx.x) & (kEnergySlots - 1)));
 }

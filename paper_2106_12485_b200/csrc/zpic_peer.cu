@@ -7,9 +7,10 @@
 // group, CUDA IPC pointers across processes over NVLink, this context's own block in a one-rank
 // ring).  The particles leaving the slab are appended straight into the neighbour's message area
 // by the kernels that route them (K3, K1L: a slot from the receiver's count, then the record; the
-// receiver zeroes its counts once it inserted them).  A round is then at most one copy kernel (the
-// sender's raw J rows, or E/B rows, into the receiver's area; none for round 1 with the cross-slab
-// commutative current), every writer ending with a system-scope fence, one signal kernel (a
+// receiver zeroes its counts once it inserted them), and the E/B rows of round 2 by K5's slab-edge
+// tiles straight into the neighbours' guard rows (k_peer_put2 below only after zpic_set_fields).
+// A round is then at most one copy kernel (the sender's raw J rows into the receiver's area; none
+// with the cross-slab commutative current), every writer ending with a system-scope fence, one signal kernel (a
 // system-scope release store of the round's epoch into the receiver's flag) and, on the receiver,
 // one wait kernel (an acquire spin until the flag reaches the epoch, bounded: a neighbour that
 // never signals sets ERR_HALO instead of hanging the GPU).  Flags in the receiver's block: [0] round 1 from its lower neighbour, [1]
