@@ -511,7 +511,10 @@ void launch_push_tiles(const PushParams& p_in, int tile_begin, int tile_end, cud
   p.tile0 = tile_begin;
   const int ntiles = tile_end - tile_begin;
   switch (p.T) {
-    case 8: launch_push_T<8, 128, 8>(p, ntiles, st); break;
+    case 8:   // a grid of at most two tiles per SM (C1): 256 threads per tile halve each CTA's path
+      if (p.ntx * p.nty <= 2 * 148) launch_push_T<8, 256, 4>(p, ntiles, st);
+      else launch_push_T<8, 128, 8>(p, ntiles, st);
+      break;
     case 16:
       switch (k1_shape()) {
         case 0: launch_push_T<16, 256, 3>(p, ntiles, st); break;
