@@ -83,13 +83,20 @@ def _gpu_run(name, precision, cont_every):
     return cfg, np.array(fe), np.array(ke), cont, fields, cnt
 
 
+# C3 and C4 for their whole 1000 / 4000 steps: the oracle needs ~27 / ~46 minutes, so these run
+# only with ZPIC_FULLRUN_LONG=1 (reports: profiles/r2_fullrun_whole/)
+_LONG = [pytest.param("C3-whole", "auto", 50, marks=pytest.mark.oracle_run("C3-whole")),
+         pytest.param("C4-whole", "auto", 100, marks=pytest.mark.oracle_run("C4-whole"))] \
+    if os.environ.get("ZPIC_FULLRUN_LONG") == "1" else []
+
+
 @pytest.mark.parametrize("name,precision,cont_every", [
     pytest.param("C1", "auto", 1, marks=pytest.mark.oracle_run("C1")),
     pytest.param("C2", "auto", 1, marks=pytest.mark.oracle_run("C2")),
     pytest.param("C2", "exact", 1, marks=pytest.mark.oracle_run("C2")),
     pytest.param("C3", "auto", 10, marks=pytest.mark.oracle_run("C3")),
     pytest.param("C4", "auto", 10, marks=pytest.mark.oracle_run("C4")),
-])
+] + _LONG)
 def test_full_run_parity(name, precision, cont_every, oracle_run):
     cfg, fe, ke, cont, fields, cnt = _gpu_run(name, precision, cont_every)
     o = oracle_run(name)
