@@ -52,7 +52,7 @@ void launch_apply_j_halo(float* J, const GridDesc& g, const float* rup, const fl
 size_t particle_msg_bytes(int cap);
 PeerView peer_view(void* block, int pitch, int pcap);
 size_t peer_block_bytes(int pitch, int pcap);
-void launch_peer_put1(const float* J, const GridDesc& g, int pcap, const PeerView& lo, const PeerView& up, int has_lo,
+void launch_peer_put1(const float* J, const GridDesc& g, const PeerView& lo, const PeerView& up, int has_lo,
                       int has_hi, cudaStream_t st);
 void launch_peer_put2(const float* E, const float* B, const GridDesc& g, const PeerView& lo, const PeerView& up,
                       int has_lo, int has_hi, int b, cudaStream_t st);
@@ -1259,7 +1259,7 @@ void peer_round1_send(zpic_ctx* c) {
   // the particles are already in the neighbours' areas (K3 / K1L wrote them there); the raw J rows
   // too with the cross-slab commutative current (K1 / K1L added them): then only the signal
   if (!c->peer_j)
-    launch_peer_put1(c->J, c->g, c->pcap, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi, c->stream);
+    launch_peer_put1(c->J, c->g, c->peer_lo, c->peer_hi, c->has_lo, c->has_hi, c->stream);
   launch_peer_signal(c->has_hi ? c->peer_hi.flags + 0 : nullptr, c->has_lo ? c->peer_lo.flags + 1 : nullptr, c->peer_e1,
                      c->stream);
 }
@@ -1297,8 +1297,7 @@ void peer_zero_wait(zpic_ctx* c) {
   c->j_zeroed = false;
 }
 // (the rows are already in this slab's guard rows: waiting is all there is to receive)
-void peer_round2_recv(zpic_ctx* c, int b) {
-  (void)b;
+void peer_round2_wait(zpic_ctx* c) {
   launch_peer_wait(c->peer_self.flags, c->has_lo ? 2 : -1, c->has_hi ? 3 : -1, c->peer_e2, c->err, c->stream);
 }
 
@@ -1337,11 +1336,10 @@ StepState step_phase_a(zpic_ctx* c) {
       launch_push_tiles(q, 0, c->ntiles, c->stream);
       c->r2_pending = false;
       ++s.launches;
-    } else if (c->r2_pending) {   // the E/B ghost rows of this step are still in flight
+    } else if (c->r2_pending) {   // NCCL: the E/B ghost rows of this step are still in flight
       const int tb = c->ntx, te = std::max(c->ntx, (c->nty - 1) * c->ntx);
       launch_push_tiles(p, tb, te, c->stream);
-      if (c->peer) peer_round2_recv(c, c->cur);   // the neighbours' E/B rows into this buffer's guards
-      else CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
+      CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));   // round 2 landed (comm stream)
       c->r2_pending = false;
       PushParams q = p;   // both slab-edge tile rows in one grid (one wave tail instead of two)
       q.boundary_last = 2;
@@ -1593,7 +1591,7 @@ static void run_step_nccl(zpic_ctx* c) {
     if (peer_fused_r2()) peer_round2_signal(c);
     else peer_round2_send(c, c->cur ^ 1);
     static const bool no_overlap = [] { const char* e = getenv("ZPIC_NO_R2_OVERLAP"); return e && atoi(e); }();
-    if (no_overlap) peer_round2_recv(c, c->cur ^ 1);
+    if (no_overlap) peer_round2_wait(c);
     else c->r2_pending = true;
   } else if (c->slab) {
     ncclResult_t r;
@@ -1613,7 +1611,7 @@ static void run_step_nccl(zpic_ctx* c) {
 }
 static void slab_join(zpic_ctx* c) {
   if (c->r2_pending) {
-    if (c->peer) peer_round2_recv(c, c->cur);
+    if (c->peer) peer_round2_wait(c);
     else CUDA_OR_THROW(cudaStreamWaitEvent(c->stream, c->ev[3], 0));
     c->r2_pending = false;
   }
@@ -1701,7 +1699,7 @@ zpic_status zpic_step(zpic_ctx* c, int32_t n) {
     if (c->slab && c->halo_dirty) {
       if (c->peer) {
         peer_round2_send(c, c->cur);
-        peer_round2_recv(c, c->cur);
+        peer_round2_wait(c);
       } else {
         ncclResult_t r = nccl_exchange_round2(c, c->cur, c->stream);
         if (r != ncclSuccess) throw Fail{ZPIC_E_NCCL, std::string("NCCL halo: ") + ncclGetErrorString(r)};
@@ -1759,7 +1757,7 @@ zpic_status zpic_step_group(zpic_ctx** cs, int32_t count, int32_t n) {
     if (cs[0]->halo_dirty) {
       if (peer) {   // every signal is enqueued before the wait that reads it
         for (int r = 0; r < count; ++r) peer_round2_send(cs[r], cs[r]->cur);
-        for (int r = 0; r < count; ++r) peer_round2_recv(cs[r], cs[r]->cur);
+        for (int r = 0; r < count; ++r) peer_round2_wait(cs[r]);
       } else {
         loop_exchange_round2(cs, count, cs[0]->cur);
       }
@@ -1779,7 +1777,7 @@ zpic_status zpic_step_group(zpic_ctx** cs, int32_t count, int32_t n) {
           if (peer_fused_r2()) peer_round2_signal(cs[r]);
           else peer_round2_send(cs[r], cs[r]->cur ^ 1);
         }
-        for (int r = 0; r < count; ++r) peer_round2_recv(cs[r], cs[r]->cur ^ 1);
+        for (int r = 0; r < count; ++r) peer_round2_wait(cs[r]);
       } else {
         loop_exchange_round2(cs, count, cs[0]->cur ^ 1);
       }

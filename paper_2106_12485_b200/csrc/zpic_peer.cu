@@ -119,9 +119,8 @@ __global__ void k_peer_wait(const unsigned long long* flags, int ia, int ib, uns
   if (!wait_flags(flags, ia, ib, e, 40000000000LL)) atomicOr(err, ERR_HALO);
 }
 
-void launch_peer_put1(const float* J, const GridDesc& g, int pcap, const PeerView& lo, const PeerView& up, int has_lo,
+void launch_peer_put1(const float* J, const GridDesc& g, const PeerView& lo, const PeerView& up, int has_lo,
                       int has_hi, cudaStream_t st) {
-  (void)pcap;
   k_peer_put1<<<48, 256, 0, st>>>(J, g, lo, up, has_lo, has_hi);
 }
 void launch_peer_put2(const float* E, const float* B, const GridDesc& g, const PeerView& lo, const PeerView& up,
