@@ -156,12 +156,15 @@ typedef struct {
  *   ZPIC_TRANSPORT_LOOPBACK: `world` contexts in one process on one device and one stream,
  *     stepped together with zpic_step_group (validation of the slab logic on one GPU);
  *   ZPIC_TRANSPORT_PEER: one process per GPU of one node; no NCCL send / recv in the step: the
- *     library's own kernels copy the halo rows and the migrating particles straight into the
- *     neighbours' receive areas over NVLink (CUDA IPC pointers, exchanged once at zpic_init with
- *     an all-gather on the NCCL communicator given as for ZPIC_TRANSPORT_NCCL) and signal them with
- *     system-scope epoch flags the receiver's wait kernel acquires (a wait that never completes
- *     stops the run with ZPIC_E_OVERFLOW after ~20 s instead of hanging); world = 1 is a ring on
- *     the context's own buffers;
+ *     library's own kernels write the halo straight into the neighbours' memory over NVLink (the
+ *     particles leaving the slab appended by the kernels that route them, the E / B rows of
+ *     round 2 by the Yee kernel's slab-edge tiles into the neighbours' guard rows, the raw J rows
+ *     by a put kernel or, with current_mode = 1, added by the push kernel into the neighbours' J;
+ *     CUDA IPC pointers exchanged once at zpic_init with an all-gather on the NCCL communicator
+ *     given as for ZPIC_TRANSPORT_NCCL) and signal each round with a system-scope epoch flag that
+ *     the receiver acquires (a wait kernel, or the slab-edge CTAs of the next push for round 2; a
+ *     wait that never completes stops the run with ZPIC_E_OVERFLOW after ~20 s instead of
+ *     hanging); world = 1 is a ring on the context's own buffers;
  *   ZPIC_TRANSPORT_LOOPBACK_PEER: the PEER kernels in a loopback group (zpic_step_group; every
  *     signal is enqueued before the wait that reads it, so no kernel ever waits on another).
  * The PEER transports allocate the receive block and the E / B field buffers (and, with
