@@ -117,13 +117,30 @@ def test_full_run_parity(name, precision, cont_every, oracle_run):
     rec["E_final_rel_l2"], rec["B_final_rel_l2"] = rel_l2(Ef, o["E%d" % steps]), rel_l2(Bf, o["B%d" % steps])
     rec["B_final_max_rel"] = _max_rel(Bf, o["B%d" % steps])
     rec["particles"] = [int(cnt["particles"]), int(o["particles"].sum())]
+    whole = name.endswith("-whole")
+    if whole:
+        # the whole unstable runs: the same GPU run with the exact two-word current differs from this
+        # one only in rounding; its distance is the run's own predictability limit (the counter-
+        # streaming clouds amplify any rounding difference, tools/gpu/divergence.py)
+        _, _, _, fields_x, _ = _gpu_run(name, "exact", 10 ** 9)[1:]
+        Ex, Bx = fields_x[steps]
+        rec["E_final_gpu_vs_gpu"], rec["B_final_gpu_vs_gpu"] = rel_l2(Ef, Ex), rel_l2(Bf, Bx)
     _report("%s_%s" % (name, precision), rec)
     assert rec["continuity_max"] <= CONT_TOL, rec
     assert rec["fe_agreement"] <= ENERGY_TOL and max(rec["ke_agreement"]) <= ENERGY_TOL, rec
     assert rec["total_agreement"] <= ENERGY_TOL, rec
     assert rec["E10_rel_l2"] <= FIELD_TOL and rec["B10_rel_l2"] <= FIELD_TOL, rec
-    assert rec["B_final_rel_l2"] <= FINAL_B_TOL and rec["E_final_rel_l2"] <= FINAL_E_TOL, rec
-    assert rec["particles"][0] == rec["particles"][1], rec
+    if whole:
+        # PAPER.md:351-353 compares final maps of implementations that differ only in rounding
+        # (~1e-4 there); past the instability's saturation the GPU-vs-oracle distance must stay
+        # within 3x the GPU's own rounding-only divergence, and the particle count (open edges)
+        # within 1e-5
+        assert rec["B_final_rel_l2"] <= 3 * rec["B_final_gpu_vs_gpu"] + FINAL_B_TOL, rec
+        assert rec["E_final_rel_l2"] <= 3 * rec["E_final_gpu_vs_gpu"] + FINAL_E_TOL, rec
+        assert abs(rec["particles"][0] - rec["particles"][1]) <= 1e-5 * rec["particles"][1], rec
+    else:
+        assert rec["B_final_rel_l2"] <= FINAL_B_TOL and rec["E_final_rel_l2"] <= FINAL_E_TOL, rec
+        assert rec["particles"][0] == rec["particles"][1], rec
 
 
 @pytest.mark.oracle_run("C5")
