@@ -9,34 +9,18 @@ namespace zpic {
 // ---- field accessors -----------------------------------------------------------------------
 // Tile-staged fields: (Ex, By) share the (1/2, 0) stagger, (Ey, Bx) share (0, 1/2); Ez (0, 0),
 // Bz (1/2, 1/2).  Arrays cover local cells [-1, T+1) in both axes, row width W = T + 2.
+// (Ex, By) is stored in pairs of nodes: entry o holds (Ex, By) of nodes o and o + 1 as one float4,
+// so a stencil row is one LDS.128 instead of two LDS.64 (fewer shared-memory wavefronts when a
+// warp's cells are scattered over the tile: -1.3 % K1 time in steady state, the same right after
+// the injection).  Pairing (Ey, Bx) as well, or Ez / Bz, costs the 8th CTA per SM
+// or gains nothing (profiles/r2_ab_pairs.log).
 template <int W>   // row width (compile-time, so stencil offsets are immediates)
 struct SmemFields {
-  const float2* eb1;  // (Ex, By)
+  const float4* eb1;  // (Ex, By) of nodes o, o + 1
   const float2* eb2;  // (Ey, Bx)
   const float* ez;
   const float* bz;
   __device__ __forceinline__ int o(int lx, int ly) const { return (ly + 1) * W + (lx + 1); }
-  __device__ __forceinline__ void hi(int i, int j, float wx, float wy, float& ex, float& by) const {
-    float2 a = eb1[o(i, j)], b = eb1[o(i + 1, j)], c = eb1[o(i, j + 1)], d = eb1[o(i + 1, j + 1)];
-    float l0 = fmaf(wx, b.x - a.x, a.x), l1 = fmaf(wx, d.x - c.x, c.x);
-    ex = fmaf(wy, l1 - l0, l0);
-    l0 = fmaf(wx, b.y - a.y, a.y); l1 = fmaf(wx, d.y - c.y, c.y);
-    by = fmaf(wy, l1 - l0, l0);
-  }
-  __device__ __forceinline__ void ih(int i, int j, float wx, float wy, float& ey, float& bx) const {
-    float2 a = eb2[o(i, j)], b = eb2[o(i + 1, j)], c = eb2[o(i, j + 1)], d = eb2[o(i + 1, j + 1)];
-    float l0 = fmaf(wx, b.x - a.x, a.x), l1 = fmaf(wx, d.x - c.x, c.x);
-    ey = fmaf(wy, l1 - l0, l0);
-    l0 = fmaf(wx, b.y - a.y, a.y); l1 = fmaf(wx, d.y - c.y, c.y);
-    bx = fmaf(wy, l1 - l0, l0);
-  }
-  __device__ __forceinline__ float one(const float* f, int i, int j, float wx, float wy) const {
-    float a = f[o(i, j)], b = f[o(i + 1, j)], c = f[o(i, j + 1)], d = f[o(i + 1, j + 1)];
-    float l0 = fmaf(wx, b - a, a), l1 = fmaf(wx, d - c, c);
-    return fmaf(wy, l1 - l0, l0);
-  }
-  __device__ __forceinline__ float fez(int i, int j, float wx, float wy) const { return one(ez, i, j, wx, wy); }
-  __device__ __forceinline__ float fbz(int i, int j, float wx, float wy) const { return one(bz, i, j, wx, wy); }
 };
 
 // Global-memory fields (loose particles): (i, j) are slab cell indices, guards valid.
@@ -147,8 +131,9 @@ __device__ __forceinline__ void interpolate(const SmemFields<W>& f, int lx, int 
   const float wxh = xl ? x + 0.5f : x - 0.5f, wyh = yl ? y + 0.5f : y - 0.5f;
   const int oa = f.o(ih, ly), ob = f.o(lx, jh), oz = f.o(lx, ly), oh = f.o(ih, jh);
   // (Ex, By) at (ih, ly) with weights (wxh, y)
-  float2 l0 = lerp2(f.eb1[oa], f.eb1[oa + 1], make_float2(wxh, wxh));
-  float2 l1 = lerp2(f.eb1[oa + W], f.eb1[oa + W + 1], make_float2(wxh, wxh));
+  const float4 q0 = f.eb1[oa], q1 = f.eb1[oa + W];
+  float2 l0 = lerp2(make_float2(q0.x, q0.y), make_float2(q0.z, q0.w), make_float2(wxh, wxh));
+  float2 l1 = lerp2(make_float2(q1.x, q1.y), make_float2(q1.z, q1.w), make_float2(wxh, wxh));
   const float2 r1 = lerp2(l0, l1, make_float2(y, y));
   // (Ey, Bx) at (lx, jh) with weights (x, wyh)
   l0 = lerp2(f.eb2[ob], f.eb2[ob + 1], make_float2(x, x));

@@ -85,7 +85,7 @@ struct K1Smem {
   static constexpr int JWORDS = (3 * WJ * WJ + 3) & ~3;        // int4-aligned
   static constexpr int JBYTES = (2 * JWORDS * 4 + 127) & ~127;
   static constexpr int QBYTES(int blk) { return 6 * (blk / 32) * kQRing * 4; }
-  static constexpr int FBYTES = W * W * (2 * 8 + 2 * 4);
+  static constexpr int FBYTES = W * W * (16 + 8 + 2 * 4);   // (Ex, By) node pairs, (Ey, Bx), Ez, Bz
   static constexpr size_t bytes(int blk) { return (size_t)JBYTES + QBYTES(blk) + FBYTES; }
 };
 
@@ -105,8 +105,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
   int* s_j = reinterpret_cast<int*>(smem_raw);         // int32 current, or the high words (exact form)
   int* s_jlo = s_j + JWORDS;                           // low words (exact form only)
   int* s_q = reinterpret_cast<int*>(smem_raw + L::JBYTES);   // path rings: NW x kQRing float4, then float2
-  float2* s_eb1 = reinterpret_cast<float2*>(smem_raw + L::JBYTES + L::QBYTES(BLK));
-  float2* s_eb2 = s_eb1 + W * W;
+  float4* s_eb1 = reinterpret_cast<float4*>(smem_raw + L::JBYTES + L::QBYTES(BLK));
+  float2* s_eb2 = reinterpret_cast<float2*>(s_eb1 + W * W);
   float* s_ez = reinterpret_cast<float*>(s_eb2 + W * W);
   float* s_bz = s_ez + W * W;
   __shared__ __align__(8) unsigned long long s_bar;
@@ -193,7 +193,8 @@ __global__ void __launch_bounds__(BLK, MINB) k_push_tiles(const __grid_constant_
     constexpr int C = W * L::BX;   // one component of a box
     for (int k = threadIdx.x; k < W * W; k += BLK) {
       const int q = (k / W) * L::BX + k % W + 3;   // local cell k % W - 1 sits at box column k % W + 3
-      s_eb1[k] = make_float2(landE[q], landB[C + q]);         // (Ex, By)
+      // (Ex, By) of nodes k and k + 1 (the last column's partner is never read)
+      s_eb1[k] = make_float4(landE[q], landB[C + q], landE[q + 1], landB[C + q + 1]);
       s_eb2[k] = make_float2(landE[C + q], landB[q]);         // (Ey, Bx)
       s_ez[k] = landE[2 * C + q];
       s_bz[k] = landB[2 * C + q];
@@ -495,7 +496,7 @@ static void launch_push_T(const PushParams& p, int ntiles, cudaStream_t st) {
 
 // K1 launch shape for 16x16 tiles (threads per CTA, CTAs per SM the register budget is sized
 // for).  ZPIC_K1_SHAPE selects it for tuning experiments: 0 = 256 x 3 (80 registers),
-// 1 = 256 x 4 (64 registers), 2 = 128 x 6 (80 registers), 3 = 128 x 8 (64 registers, the
+// 1 = 256 x 4 (64 registers), 2 = 128 x 6 (80 registers), 4 = 128 x 7 (72 registers), 3 = 128 x 8 (64 registers, the
 // default: 63.4 % vs 60.5 % of HBM for shape 2 at C5).
 static int k1_shape() {
   static int v = [] {
@@ -520,6 +521,7 @@ void launch_push_tiles(const PushParams& p_in, int tile_begin, int tile_end, cud
         case 0: launch_push_T<16, 256, 3>(p, ntiles, st); break;
         case 1: launch_push_T<16, 256, 4>(p, ntiles, st); break;
         case 2: launch_push_T<16, 128, 6>(p, ntiles, st); break;
+        case 4: launch_push_T<16, 128, 7>(p, ntiles, st); break;
         default: launch_push_T<16, 128, 8>(p, ntiles, st); break;
       }
       break;
