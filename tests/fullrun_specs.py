@@ -12,7 +12,8 @@ RUNS = {
     "C2": ("C2", 500, (10, 500)),     # configs[1], its whole run (Weibel growth and saturation)
     "C3": ("C3", 200, (10, 200)),     # configs[2], full grid, the first 200 of 1000 steps
     "C4": ("C4", 200, (10, 200)),     # configs[3], full grid, the first 200 of 4000 steps
-    # their whole runs (oracle ~27 / ~46 min: only with ZPIC_FULLRUN_LONG=1, test_fullrun_gpu.py)
+    # their whole runs (oracle ~30 / > 46 min, C4 beyond a 60-min gpurun call beside C3: only with
+    # ZPIC_FULLRUN_LONG=1, test_fullrun_gpu.py)
     "C3-whole": ("C3", 1000, (10, 1000)),
     "C4-whole": ("C4", 4000, (10, 4000)),
 }
